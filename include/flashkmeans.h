@@ -1,0 +1,146 @@
+/*
+ * flashkmeans.h -- C ABI of the B200-native flash-kmeans hot path.
+ *
+ * The reference (flashmeans 0.1.0, /root/reference/pkg/src/flashmeans) has no
+ * foreign-function boundary of its own: its "native seam" is a set of Numba
+ * @njit kernels that fill caller-allocated NumPy buffers (_kernels.py:18-171)
+ * behind three Python operators.  Each entry point below replaces one of
+ * those operators at the same granularity, with the same ownership rule
+ * (caller allocates every output, the library only writes views):
+ *
+ *   fk_assign     <- flash_assign          flash_assign.py:135-222
+ *                    (dist_block + rowmin_merge, _kernels.py:32-82;
+ *                     assign_tile_fast, _kernels.py:85-104)
+ *   fk_update     <- sort_inverse_update   sort_inverse.py:106-149
+ *                    (counting_sort + segment_stats + merge_segments,
+ *                     _kernels.py:118-171)
+ *   fk_normalize  <- normalize             baseline.py:127-150
+ *   fk_row_norms  <- row_norms             core.py:307-318 (_kernels.py:21-29)
+ *   fk_objective  <- _objective_row        pipeline.py:65-68
+ *   fk_scatter    <- scatter_update        baseline.py:108-124 (foil only)
+ *
+ * Conventions
+ *   - extern "C", plain pointers and sizes; no torch / CUDA types.  `stream`
+ *     is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Every call is stream-ordered, never synchronizes the host and never
+ *     allocates device memory: scratch comes from a caller-owned workspace
+ *     sized by the matching *_workspace query.
+ *   - All data pointers are DEVICE pointers.  Layouts are batch-major,
+ *     row-major: X (B,N,d), C (B,K,d), ids (B,N) int32, sums (B,K,d) f64,
+ *     counts (B,K) int64 -- the reference's shapes and dtypes
+ *     (core.py:109-233).
+ *   - Errors are status codes, validated before any launch (the reference
+ *     raises ValueError before any kernel call, flash_assign.py:152-157);
+ *     FK_EINVAL maps to ValueError in the Python layer.
+ *   - The library is reentrant; its only global state is a lazily built,
+ *     thread-safe per-device table of kernel attributes (AOT sm_100a SASS,
+ *     no JIT).
+ */
+#ifndef FLASHKMEANS_H_
+#define FLASHKMEANS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FK_API __attribute__((visibility("default")))
+#else
+#define FK_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FK_OK = 0,
+  FK_EINVAL = 1,        /* bad shape / dtype / pointer / id                    */
+  FK_EUNSUPPORTED = 2,  /* shape outside the precompiled buckets or no sm_100 */
+  FK_ECUDA = 3,         /* a CUDA runtime error; see fk_last_cuda_error()     */
+  FK_EWORKSPACE = 4     /* workspace smaller than the *_workspace query        */
+} fk_status;
+
+typedef enum {
+  FK_F32 = 0,   /* "single" (core.py:22)                                       */
+  FK_BF16 = 1,  /* bf16 data: tcgen05 path, fp32 accumulation                  */
+  FK_F16 = 2,   /* fp16 data: tcgen05 path, fp32 accumulation                  */
+  FK_F64 = 3    /* "double" (core.py:22)                                       */
+} fk_dtype;
+
+typedef enum {
+  FK_ASSIGN_EXACT = 0,  /* dot_mode="exact": Appendix-A arithmetic, bitwise for f32/f64 */
+  FK_ASSIGN_FAST = 1    /* dot_mode="fast":  tensor cores (bf16/f16), fp32 accumulate   */
+} fk_assign_mode;
+
+FK_API const char* fk_version(void);
+FK_API const char* fk_status_string(fk_status s);
+/* Last CUDA error string seen by this thread (valid until the next call). */
+FK_API const char* fk_last_cuda_error(void);
+/* 1 if `device` is an sm_100 part this library has SASS for, else 0. */
+FK_API int fk_device_supported(int device);
+
+/* ---------------------------------------------------------------- assign
+ * Nearest-centroid assignment without materializing the N x K distances.
+ *   X, C      : (B,N,d), (B,K,d) in dtype `dt`
+ *   idx_out   : (B,N) int32, lowest centroid id among equal minima
+ *   mind_out  : (B,N) squared distance to the chosen centroid; element type
+ *               is the data type for FK_F32/FK_F64 and float32 for
+ *               FK_BF16/FK_F16
+ *   idx_prev  : optional (B,N) int32; when given, *changed_flag (int32, device)
+ *               is OR-ed with 1 if any id differs from idx_prev
+ *               (the lloyd_run repeat test, pipeline.py:137)
+ * FK_F32/FK_F64 always run the exact mirror (bitwise equal to the
+ * reference); FK_BF16/FK_F16 run the tcgen05 kernel for d <= 128 and a
+ * CUDA-core kernel otherwise.                                                */
+FK_API size_t fk_assign_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d);
+FK_API fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B, int64_t N, int64_t K,
+                    int64_t d, int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+                    int32_t* changed_flag, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---------------------------------------------------------------- update
+ * Per-cluster sums (f64) and counts (int64) from (X, ids) by a device
+ * counting sort of ids followed by warp-level segmented reductions over the
+ * sorted order (X is never permuted).  `accumulate`=0 overwrites sums/counts,
+ * 1 adds into them (chunked streaming, PartialStats.combine pipeline.py:250).
+ * `update_chunk` is the reference's chunk (TilingConfig.update_chunk); it
+ * only defines *merges_out (device int64, incremented by the segment count the
+ * reference would record, sort_inverse.py:165).  merges_out may be NULL.    */
+FK_API size_t fk_update_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d);
+FK_API fk_status fk_update(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                    int64_t K, int64_t d, int64_t update_chunk, int32_t accumulate, double* sums,
+                    int64_t* counts, int64_t* merges_out, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* ------------------------------------------------------------- normalize
+ * c = fl_T(sums / counts) per cluster; clusters with count 0 keep `prev`
+ * bitwise and get empty_mask=1.  prev/out are (B,K,d) in `master_dt`
+ * (FK_F32 or FK_F64); `operand_out` (optional, (B,K,d) in `operand_dt`)
+ * receives the rounded copy used as the next MMA operand.  `max_shift2`
+ * (optional, device f64 scalar, must be pre-zeroed) receives
+ * max_k sum_j (out-prev)^2 (pipeline._max_shift before the sqrt).  out may
+ * alias prev.                                                                */
+FK_API fk_status fk_normalize(fk_dtype master_dt, const double* sums, const int64_t* counts,
+                       const void* prev, void* out, fk_dtype operand_dt, void* operand_out,
+                       uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K, int64_t d,
+                       void* stream);
+
+/* Exact row norms in the data precision (f32/f64), core.row_norms semantics. */
+FK_API fk_status fk_row_norms(fk_dtype dt, const void* M, int64_t rows, int64_t d, void* out,
+                       void* stream);
+
+/* objective[b] = sum_i mind[b,i] in f64 (pipeline._objective_row); mind is
+ * f32 (FK_F32/FK_BF16/FK_F16 data) or f64.  Deterministic fixed-order
+ * reduction that follows numpy's buffered pairwise summation.               */
+FK_API size_t fk_objective_workspace(int64_t B, int64_t N);
+FK_API fk_status fk_objective(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N, double* out,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* Baseline scatter (one f64 atomic merge per point element): the contended
+ * foil of baseline.scatter_update, kept for ncu comparison only.            */
+FK_API fk_status fk_scatter(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                     int64_t K, int64_t d, double* sums, int64_t* counts, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHKMEANS_H_ */

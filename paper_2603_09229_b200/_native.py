@@ -1,0 +1,91 @@
+"""ctypes binding of the C ABI (include/flashkmeans.h).
+
+The library is AOT-built into ``paper_2603_09229_b200/_lib/libflashkmeans.so``
+(``python -m paper_2603_09229_b200._build``).  There is deliberately no
+fallback: if the library is missing or the device is not an sm_100 part, the
+operators raise instead of silently computing on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libflashkmeans.so")
+
+FK_OK, FK_EINVAL, FK_EUNSUPPORTED, FK_ECUDA, FK_EWORKSPACE = range(5)
+FK_F32, FK_BF16, FK_F16, FK_F64 = range(4)
+
+_lock = threading.Lock()
+_lib = None
+
+
+class NativeLibraryError(RuntimeError):
+    """The sm_100a library is missing, failed to load, or reported a CUDA error."""
+
+
+def _declare(L):
+    P, I64, I32, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_size_t
+    L.fk_version.restype = ctypes.c_char_p
+    L.fk_status_string.restype = ctypes.c_char_p
+    L.fk_status_string.argtypes = [ctypes.c_int]
+    L.fk_last_cuda_error.restype = ctypes.c_char_p
+    L.fk_device_supported.restype = ctypes.c_int
+    L.fk_device_supported.argtypes = [ctypes.c_int]
+    L.fk_assign_workspace.restype = SZ
+    L.fk_assign_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
+    L.fk_assign.restype = ctypes.c_int
+    L.fk_assign.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]
+    L.fk_update_workspace.restype = SZ
+    L.fk_update_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
+    L.fk_update.restype = ctypes.c_int
+    L.fk_update.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, I64, I32, P, P, P, P, SZ, P]
+    L.fk_normalize.restype = ctypes.c_int
+    L.fk_normalize.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, P, P, P, I64, I64, I64, P]
+    L.fk_row_norms.restype = ctypes.c_int
+    L.fk_row_norms.argtypes = [ctypes.c_int, P, I64, I64, P, P]
+    L.fk_objective_workspace.restype = SZ
+    L.fk_objective_workspace.argtypes = [I64, I64]
+    L.fk_objective.restype = ctypes.c_int
+    L.fk_objective.argtypes = [ctypes.c_int, P, I64, I64, P, P, SZ, P]
+    L.fk_scatter.restype = ctypes.c_int
+    L.fk_scatter.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, P, P, P]
+
+
+EXPORTED = (
+    "fk_version", "fk_status_string", "fk_last_cuda_error", "fk_device_supported",
+    "fk_assign_workspace", "fk_assign", "fk_update_workspace", "fk_update", "fk_normalize",
+    "fk_row_norms", "fk_objective_workspace", "fk_objective", "fk_scatter",
+)
+
+
+def lib():
+    """Load (once) and return the ctypes handle; raises NativeLibraryError if absent."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise NativeLibraryError(
+                        f"{LIB_PATH} is missing: build it with "
+                        "`python -m paper_2603_09229_b200._build` (there is no CPU fallback)")
+                L = ctypes.CDLL(LIB_PATH)
+                _declare(L)
+                _lib = L
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status == FK_OK:
+        return
+    L = lib()
+    msg = f"{what}: {L.fk_status_string(status).decode()}"
+    if status == FK_EINVAL:
+        raise ValueError(msg)
+    if status == FK_EUNSUPPORTED:
+        raise NotImplementedError(msg + " (an sm_100 / B200 device is required)")
+    if status == FK_ECUDA:
+        raise NativeLibraryError(msg + ": " + L.fk_last_cuda_error().decode())
+    raise NativeLibraryError(msg)

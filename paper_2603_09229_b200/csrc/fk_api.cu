@@ -1,0 +1,200 @@
+// fk_api.cu -- the extern "C" boundary declared in include/flashkmeans.h.
+// Validation happens here, before any launch (the reference validates before
+// any kernel call: flash_assign.py:152-157, sort_inverse.py:120-122,
+// baseline.py:134-137); kernels never see malformed shapes.
+#include <mutex>
+#include <string>
+
+#include "../../include/flashkmeans.h"
+#include "fk_common.cuh"
+#include "fk_kernels.h"
+
+namespace {
+
+thread_local std::string g_last_cuda_error;
+
+fk_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return FK_OK;
+  g_last_cuda_error = cudaGetErrorString(e);
+  return FK_ECUDA;
+}
+
+struct DevInfo {
+  int sms = 0;
+  int major = 0, minor = 0;
+};
+
+DevInfo dev_info() {
+  static std::mutex mu;
+  static DevInfo cache[64];
+  static bool have[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!have[dev]) {
+    DevInfo d;
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&d.minor, cudaDevAttrComputeCapabilityMinor, dev);
+    cache[dev] = d;
+    have[dev] = true;
+  }
+  return cache[dev];
+}
+
+bool valid_dt(int dt) { return dt >= FK_F32 && dt <= FK_F64; }
+size_t elem_size(int dt) { return dt == FK_F32 ? 4 : dt == FK_F64 ? 8 : 2; }
+bool is_lowp(int dt) { return dt == FK_BF16 || dt == FK_F16; }
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+constexpr int64_t kMaxPoints = (int64_t(1) << 31) - 1;
+
+bool shape_ok(int64_t B, int64_t N, int64_t K, int64_t d) {
+  if (B < 1 || N < 1 || K < 1 || d < 1) return false;
+  if (B * N > kMaxPoints) return false;  // flattened point index is int32
+  if (B * K > (int64_t(1) << 30)) return false;
+  if (K > (int64_t(1) << 30) || d > (int64_t(1) << 20)) return false;
+  return true;
+}
+
+bool tc_path(int dt, int64_t d, const void* X, const void* C) {
+  return is_lowp(dt) && fk::assign_tc_supported(d) && dev_info().major == 10 &&
+         (reinterpret_cast<uintptr_t>(X) % 16 == 0) && (reinterpret_cast<uintptr_t>(C) % 16 == 0);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fk_version(void) { return "flashkmeans-b200 0.1.0 (sm_100a)"; }
+
+const char* fk_status_string(fk_status s) {
+  switch (s) {
+    case FK_OK: return "ok";
+    case FK_EINVAL: return "invalid argument";
+    case FK_EUNSUPPORTED: return "unsupported shape or device";
+    case FK_ECUDA: return "CUDA error";
+    case FK_EWORKSPACE: return "workspace too small";
+  }
+  return "unknown status";
+}
+
+const char* fk_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
+
+int fk_device_supported(int device) {
+  int major = 0;
+  if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess)
+    return 0;
+  return major == 10 ? 1 : 0;
+}
+
+// ------------------------------------------------------------------ assign
+size_t fk_assign_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d) {
+  (void)d;
+  if (!valid_dt(dt) || B < 1 || N < 1 || K < 1) return 0;
+  if (is_lowp(dt)) return al256((size_t)B * fk::assign_tc_kpad(K) * 4);
+  const size_t es = elem_size(dt);
+  return al256((size_t)B * N * es) + al256((size_t)B * K * es);
+}
+
+fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B, int64_t N, int64_t K,
+                    int64_t d, int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+                    int32_t* changed_flag, void* ws, size_t ws_bytes, void* stream) {
+  if (!valid_dt(dt) || !shape_ok(B, N, K, d)) return FK_EINVAL;
+  if (!X || !C || !idx_out || !mind_out) return FK_EINVAL;
+  if (idx_prev && !changed_flag) return FK_EINVAL;
+  const size_t need = fk_assign_workspace(dt, B, N, K, d);
+  if (need > 0 && (!ws || ws_bytes < need)) return FK_EWORKSPACE;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const DevInfo di = dev_info();
+  if (di.major != 10) return FK_EUNSUPPORTED;
+  if (is_lowp(dt)) {
+    float* cn = reinterpret_cast<float*>(ws);
+    if (tc_path(dt, d, X, C)) {
+      const int kpad = fk::assign_tc_kpad(K);
+      fk_status st = cuda_status(fk::launch_cn_pad(dt, C, B, K, d, kpad, cn, s));
+      if (st != FK_OK) return st;
+      return cuda_status(fk::launch_assign_tc(dt == FK_BF16 ? 1 : 0, X, C, cn, B, N, K, d, idx_out,
+                                              reinterpret_cast<float*>(mind_out), idx_prev,
+                                              changed_flag, di.sms, s));
+    }
+    fk_status st = cuda_status(fk::launch_cn_pad(dt, C, B, K, d, (int)K, cn, s));
+    if (st != FK_OK) return st;
+    return cuda_status(fk::launch_assign_cuda_core_lowp(dt, X, C, cn, B, N, K, d, idx_out,
+                                                        reinterpret_cast<float*>(mind_out),
+                                                        idx_prev, changed_flag, s));
+  }
+  const size_t es = elem_size(dt);
+  uint8_t* w = reinterpret_cast<uint8_t*>(ws);
+  void* xn = w;
+  void* cn = w + al256((size_t)B * N * es);
+  fk_status st = cuda_status(fk::launch_row_norms_exact(dt, X, B * N, d, xn, s));
+  if (st != FK_OK) return st;
+  st = cuda_status(fk::launch_row_norms_exact(dt, C, B * K, d, cn, s));
+  if (st != FK_OK) return st;
+  return cuda_status(fk::launch_assign_exact(dt, X, C, xn, cn, B, N, K, d, idx_out, mind_out,
+                                             idx_prev, changed_flag, s));
+}
+
+// ------------------------------------------------------------------ update
+size_t fk_update_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d) {
+  (void)d;
+  if (!valid_dt(dt) || B < 1 || N < 1 || K < 1) return 0;
+  return fk::update_workspace_bytes(B, N, K);
+}
+
+fk_status fk_update(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                    int64_t K, int64_t d, int64_t update_chunk, int32_t accumulate, double* sums,
+                    int64_t* counts, int64_t* merges_out, void* ws, size_t ws_bytes,
+                    void* stream) {
+  if (!valid_dt(dt) || !shape_ok(B, N, K, d)) return FK_EINVAL;
+  if (!X || !ids || !sums || !counts || update_chunk < 1) return FK_EINVAL;
+  const size_t need = fk_update_workspace(dt, B, N, K, d);
+  if (!ws || ws_bytes < need) return FK_EWORKSPACE;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_update(dt, X, ids, B, N, K, d, update_chunk, accumulate, sums,
+                                       counts, merges_out, ws, dev_info().sms,
+                                       reinterpret_cast<cudaStream_t>(stream)));
+}
+
+// ------------------------------------------------------------------ normalize
+fk_status fk_normalize(fk_dtype master_dt, const double* sums, const int64_t* counts,
+                       const void* prev, void* out, fk_dtype operand_dt, void* operand_out,
+                       uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K, int64_t d,
+                       void* stream) {
+  if (master_dt != FK_F32 && master_dt != FK_F64) return FK_EINVAL;
+  if (operand_out && !valid_dt(operand_dt)) return FK_EINVAL;
+  if (!sums || !counts || !prev || !out || B < 1 || K < 1 || d < 1) return FK_EINVAL;
+  return cuda_status(fk::launch_normalize(master_dt, sums, counts, prev, out, operand_dt,
+                                          operand_out, empty_mask, max_shift2, B, K, d,
+                                          reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_row_norms(fk_dtype dt, const void* M, int64_t rows, int64_t d, void* out,
+                       void* stream) {
+  if ((dt != FK_F32 && dt != FK_F64) || !M || !out || rows < 0 || d < 1) return FK_EINVAL;
+  return cuda_status(
+      fk::launch_row_norms_exact(dt, M, rows, d, out, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+size_t fk_objective_workspace(int64_t B, int64_t N) {
+  if (B < 1 || N < 1) return 0;
+  return fk::objective_workspace_bytes(B, N);
+}
+
+fk_status fk_objective(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N, double* out,
+                       void* ws, size_t ws_bytes, void* stream) {
+  if (!valid_dt(mind_dt) || !mind || !out || B < 1 || N < 1) return FK_EINVAL;
+  if (!ws || ws_bytes < fk_objective_workspace(B, N)) return FK_EWORKSPACE;
+  return cuda_status(fk::launch_objective(mind_dt == FK_F64 ? 1 : 0, mind, B, N, out, ws,
+                                          reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_scatter(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                     int64_t K, int64_t d, double* sums, int64_t* counts, void* stream) {
+  if (!valid_dt(dt) || !shape_ok(B, N, K, d) || !X || !ids || !sums || !counts) return FK_EINVAL;
+  return cuda_status(fk::launch_scatter(dt, X, ids, B, N, K, d, sums, counts,
+                                        reinterpret_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

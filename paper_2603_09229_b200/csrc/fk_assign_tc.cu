@@ -1,0 +1,426 @@
+// fk_assign_tc.cu -- FlashAssign on 5th-generation tensor cores (sm_100a).
+//
+// Replaces flash_assign (reference flash_assign.py:135-222, inner kernels
+// _kernels.py:32-104) for bf16/fp16 data: the X.C^T contraction runs as a
+// tcgen05.mma GEMM with operands staged by TMA and the fp32 accumulator in
+// TMEM; the ||c||^2 bias and the online argmin are fused into the epilogue,
+// so no N x K distance ever reaches HBM (the reference's zero-materialization
+// property, flash_assign.py:1-15).
+//
+// Persistent, warp-specialized CTA (one per SM, 384 threads):
+//   warp 0      TMA producer: X row tile (128 x d, resident for the whole
+//               centroid sweep, double-buffered) and C column tiles
+//               (256 x 64 per stage, 4-stage ring) -- C stays L2-resident.
+//   warp 1      MMA issuer: one elected thread issues M=128,N=256,K=16 MMAs
+//               into a double-buffered TMEM accumulator (2 x 256 columns).
+//   warp 2      TMEM allocator.
+//   warps 4-11  epilogue, two warpgroups splitting each 256-column tile into
+//               halves; thread = one point row (TMEM lane).  Per 32-column
+//               chunk: tcgen05.ld, s = c_norm - 2 acc (packed FFMA2), a
+//               3-input-min tree, and a warp vote; the chunk's 32 scores are
+//               spilled to a private smem slot only when this row's running
+//               minimum improves, so the index is recovered once per row
+//               tile instead of being tracked per element.
+// Tie rule (rowmin_merge, _kernels.py:64-82): strict < in ascending column
+// order within a thread, first equal element within the winning chunk, and a
+// lexicographic (value, index) merge across the two warpgroups -> the lowest
+// centroid id among equal minima.
+#include "fk_common.cuh"
+#include "fk_kernels.h"
+
+namespace fk {
+
+namespace tc {
+constexpr int BM = 128;                  // rows per tile = TMEM lanes
+constexpr int BN = 256;                  // centroids per column tile
+constexpr int STAGES = 4;                // C ring depth (32 KB each)
+constexpr int KATOMS_MAX = 2;            // d <= 128 (64 bf16 = 128 B per atom)
+constexpr int A_ATOM = BM * 128;         // 16 KB
+constexpr int A_SLOT = KATOMS_MAX * A_ATOM;
+constexpr int B_STAGE = BN * 128;        // 32 KB
+constexpr int OFF_A = 0;
+constexpr int OFF_B = OFF_A + 2 * A_SLOT;            // 64 KB
+constexpr int OFF_REC = OFF_B + STAGES * B_STAGE;    // 192 KB
+constexpr int OFF_XCH = OFF_REC + 256 * 128;         // 224 KB
+constexpr int OFF_BAR = OFF_XCH + BM * 8;
+constexpr int NBARS = 16;
+constexpr int SMEM_USED = OFF_BAR + NBARS * 8 + 16;
+constexpr int SMEM_BYTES = SMEM_USED + 1024;         // alignment slack
+constexpr int THREADS = 384;
+static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB dynamic shared memory");
+}  // namespace tc
+
+struct TcArgs {
+  int B, N, K, d;
+  int katoms;           // ceil(d / 64), 1 or 2
+  int tiles_per_batch;  // ceil(N / 128)
+  int total_tiles;      // B * tiles_per_batch
+  int ncol;             // ceil(K / 256)
+  int kpad;             // ncol * 256
+  const float* cn;      // (B, kpad) ||c||^2, +inf beyond K
+  int32_t* idx_out;     // (B, N)
+  float* mind_out;      // (B, N)
+  const int32_t* idx_prev;
+  int32_t* changed;
+};
+
+template <int FMT>
+FK_DEV float row_norm_smem(const uint8_t* a_slot, int row, int katoms, int lane) {
+  float acc = 0.f;
+  for (int ka = 0; ka < katoms; ++ka) {
+    const uint4* r = reinterpret_cast<const uint4*>(a_slot + ka * tc::A_ATOM + row * 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint4 w = r[(j + lane) & 7];
+      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float lo, hi;
+        if (FMT == 1) {
+          lo = __uint_as_float(ws[e] << 16);
+          hi = __uint_as_float(ws[e] & 0xffff0000u);
+        } else {
+          __half2 h = *reinterpret_cast<__half2*>(&ws[e]);
+          float2 f = __half22float2(h);
+          lo = f.x;
+          hi = f.y;
+        }
+        acc = fmaf(lo, lo, acc);
+        acc = fmaf(hi, hi, acc);
+      }
+    }
+  }
+  return acc;
+}
+
+// One 32-column chunk: bias, chunk minimum, conditional spill.
+FK_DEV void epi_chunk(const uint32_t (&v)[32], const float* __restrict__ cnp, int colbase,
+                      float& M, int& best, float* rec, int lane) {
+  float s[32];
+  const float4* c4 = reinterpret_cast<const float4*>(cnp);
+  const float2 m2 = make_float2(-2.f, -2.f);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    float4 cc = __ldg(c4 + j);
+    float2 r0 = ffma2(make_float2(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1])), m2,
+                      make_float2(cc.x, cc.y));
+    float2 r1 = ffma2(make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])),
+                      m2, make_float2(cc.z, cc.w));
+    s[4 * j] = r0.x;
+    s[4 * j + 1] = r0.y;
+    s[4 * j + 2] = r1.x;
+    s[4 * j + 3] = r1.y;
+  }
+  float a[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) a[j] = fmin3(s[3 * j], s[3 * j + 1], s[3 * j + 2]);
+  a[10] = fminf(s[30], s[31]);
+  float b0 = fmin3(a[0], a[1], a[2]);
+  float b1 = fmin3(a[3], a[4], a[5]);
+  float b2 = fmin3(a[6], a[7], a[8]);
+  float b3 = fminf(a[9], a[10]);
+  float mc = fmin3(b0, b1, fminf(b2, b3));
+  bool p = mc < M;
+  if (__any_sync(0xffffffffu, p)) {
+    if (p) {
+      float4* r4 = reinterpret_cast<float4*>(rec);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        r4[j ^ (lane & 7)] = make_float4(s[4 * j], s[4 * j + 1], s[4 * j + 2], s[4 * j + 3]);
+    }
+  }
+  M = p ? mc : M;
+  best = p ? colbase : best;
+}
+
+template <int FMT>
+__global__ void __launch_bounds__(tc::THREADS, 1)
+    fk_assign_tc_kernel(const __grid_constant__ CUtensorMap tmx,
+                        const __grid_constant__ CUtensorMap tmc, const TcArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem + tc::OFF_A;
+  uint8_t* sB = smem + tc::OFF_B;
+  float* sREC = reinterpret_cast<float*>(smem + tc::OFF_REC);
+  float* xch_m = reinterpret_cast<float*>(smem + tc::OFF_XCH);
+  int* xch_i = reinterpret_cast<int*>(smem + tc::OFF_XCH + tc::BM * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tc::OFF_BAR);
+  uint64_t* a_full = bars + 0;
+  uint64_t* a_empty = bars + 2;
+  uint64_t* b_full = bars + 4;
+  uint64_t* b_empty = bars + 8;
+  uint64_t* t_full = bars + 12;
+  uint64_t* t_empty = bars + 14;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + tc::NBARS);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmx);
+    tma_prefetch_desc(&tmc);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_empty[s], 1 + 4);  // MMA commit + 4 warps of epilogue WG0 (row norms)
+      mbar_init(&t_full[s], 1);
+      mbar_init(&t_empty[s], 8);      // every epilogue warp
+    }
+    for (int s = 0; s < tc::STAGES; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_holder);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t stage = 0, sphase = 0;
+      const uint32_t a_bytes = p.katoms * tc::A_ATOM;
+      auto load_a = [&](int t, int j) {
+        const int slot = j & 1;
+        const int b = t / p.tiles_per_batch;
+        const int row0 = (t - b * p.tiles_per_batch) * tc::BM;
+        mbar_wait(&a_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&a_full[slot], a_bytes);
+        for (int ka = 0; ka < p.katoms; ++ka)
+          tma_load_3d(sA + slot * tc::A_SLOT + ka * tc::A_ATOM, &tmx, &a_full[slot], ka * 64, row0,
+                      b, kEvictFirst);
+      };
+      int i = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+        const int b = t / p.tiles_per_batch;
+        if (i == 0) load_a(t, 0);
+        for (int c = 0; c < p.ncol; ++c) {
+          for (int ka = 0; ka < p.katoms; ++ka) {
+            mbar_wait(&b_empty[stage], sphase ^ 1);
+            mbar_arrive_expect_tx(&b_full[stage], tc::B_STAGE);
+            tma_load_3d(sB + stage * tc::B_STAGE, &tmc, &b_full[stage], ka * 64, c * tc::BN, b,
+                        kEvictLast);
+            if (++stage == tc::STAGES) {
+              stage = 0;
+              sphase ^= 1;
+            }
+          }
+          if (c == 0) {
+            const int t2 = t + gridDim.x;
+            if (t2 < p.total_tiles) load_a(t2, i + 1);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issue
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_f16(FMT, tc::BM, tc::BN);
+      uint32_t stage = 0, sphase = 0, g = 0;
+      int i = 0;
+      for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+        const int slot = i & 1;
+        mbar_wait(&a_full[slot], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sA + slot * tc::A_SLOT);
+        for (int c = 0; c < p.ncol; ++c, ++g) {
+          const uint32_t buf = g & 1;
+          mbar_wait(&t_empty[buf], ((g >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + buf * tc::BN;
+          for (int ka = 0; ka < p.katoms; ++ka) {
+            mbar_wait(&b_full[stage], sphase);
+            tc_fence_after();
+            const uint32_t aa = a_base + ka * tc::A_ATOM;
+            const uint32_t bb = smem_u32(sB + stage * tc::B_STAGE);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc_mma_f16(d_tmem, make_sdesc_sw128(aa + k * 32), make_sdesc_sw128(bb + k * 32),
+                         idesc, (ka | k) != 0);
+            tc_commit(&b_empty[stage]);
+            if (++stage == tc::STAGES) {
+              stage = 0;
+              sphase ^= 1;
+            }
+          }
+          tc_commit(&t_full[buf]);
+        }
+        tc_commit(&a_empty[slot]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    const int wg = ew >> 2;         // column half of every tile
+    const int q = warp & 3;         // TMEM lane quarter
+    const int row = q * 32 + lane;  // tile row owned by this thread
+    float* rec = sREC + (wg * tc::BM + row) * 32;
+    uint32_t g = 0;
+    int i = 0;
+    for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
+      const int b = t / p.tiles_per_batch;
+      const int row0 = (t - b * p.tiles_per_batch) * tc::BM;
+      const int slot = i & 1;
+      const float* cnb = p.cn + (size_t)b * p.kpad;
+      float M = __int_as_float(0x7f800000);
+      int best = -1;
+      float xn = 0.f;
+      for (int c = 0; c < p.ncol; ++c, ++g) {
+        const uint32_t buf = g & 1;
+        mbar_wait(&t_full[buf], (g >> 1) & 1);
+        tc_fence_after();
+        if (c == 0 && wg == 0) {
+          xn = row_norm_smem<FMT>(sA + slot * tc::A_SLOT, row, p.katoms, lane);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_empty[slot]);
+        }
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + buf * tc::BN + wg * 128;
+        const int col0 = c * tc::BN + wg * 128;
+        uint32_t va[32], vb[32];
+        FK_TMEM_LD_32x32b_X32(taddr, va);
+        FK_TMEM_WAIT_LD(va);
+        FK_TMEM_LD_32x32b_X32(taddr + 32, vb);
+        epi_chunk(va, cnb + col0, col0, M, best, rec, lane);
+        FK_TMEM_WAIT_LD(vb);
+        FK_TMEM_LD_32x32b_X32(taddr + 64, va);
+        epi_chunk(vb, cnb + col0 + 32, col0 + 32, M, best, rec, lane);
+        FK_TMEM_WAIT_LD(va);
+        FK_TMEM_LD_32x32b_X32(taddr + 96, vb);
+        epi_chunk(va, cnb + col0 + 64, col0 + 64, M, best, rec, lane);
+        FK_TMEM_WAIT_LD(vb);
+        // every TMEM read of this buffer has landed: hand it back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[buf]);
+        epi_chunk(vb, cnb + col0 + 96, col0 + 96, M, best, rec, lane);
+      }
+      // recover the index inside the winning chunk (first equal element)
+      int idx = -1;
+      if (best >= 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(rec);
+        int found = 31;
+#pragma unroll
+        for (int j = 7; j >= 0; --j) {
+          float4 v = r4[j ^ (lane & 7)];
+          found = (v.w == M) ? 4 * j + 3 : found;
+          found = (v.z == M) ? 4 * j + 2 : found;
+          found = (v.y == M) ? 4 * j + 1 : found;
+          found = (v.x == M) ? 4 * j + 0 : found;
+        }
+        idx = best + found;
+      }
+      if (wg == 1) {
+        xch_m[row] = M;
+        xch_i[row] = idx;
+      }
+      named_bar_sync(1, 256);
+      if (wg == 0) {
+        const float M1 = xch_m[row];
+        const int i1 = xch_i[row];
+        if (M1 < M || (M1 == M && i1 >= 0 && (idx < 0 || i1 < idx))) {
+          M = M1;
+          idx = i1;
+        }
+        const int grow = row0 + row;
+        bool ch = false;
+        if (grow < p.N) {
+          const size_t o = (size_t)b * p.N + grow;
+          p.idx_out[o] = idx;
+          p.mind_out[o] = fmaxf(0.f, xn + M);
+          if (p.idx_prev) ch = p.idx_prev[o] != idx;
+        }
+        if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
+      }
+      named_bar_sync(2, 256);
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem_base);
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D map over (d, rows, B) with a {64, box_rows, 1} box and 128-B swizzle.
+static bool make_map(CUtensorMap* m, const void* base, int fmt, int64_t d, int64_t rows,
+                     int64_t B, int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)B};
+  cuuint64_t strides[2] = {(cuuint64_t)(d * 2), (cuuint64_t)(rows * d * 2)};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, fmt == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                   3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool assign_tc_supported(int64_t d) { return d >= 8 && d <= 128 && (d % 8) == 0; }
+
+cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
+                             int64_t B, int64_t N, int64_t K, int64_t d, int32_t* idx_out,
+                             float* mind_out, const int32_t* idx_prev, int32_t* changed,
+                             int num_sms, cudaStream_t stream) {
+  CUtensorMap tmx, tmc;
+  if (!make_map(&tmx, X, fmt, d, N, B, tc::BM)) return cudaErrorInvalidValue;
+  if (!make_map(&tmc, C, fmt, d, K, B, tc::BN)) return cudaErrorInvalidValue;
+  TcArgs a;
+  a.B = (int)B;
+  a.N = (int)N;
+  a.K = (int)K;
+  a.d = (int)d;
+  a.katoms = (int)((d + 63) / 64);
+  a.tiles_per_batch = (int)((N + tc::BM - 1) / tc::BM);
+  a.total_tiles = (int)(B * a.tiles_per_batch);
+  a.ncol = (int)((K + tc::BN - 1) / tc::BN);
+  a.kpad = a.ncol * tc::BN;
+  a.cn = cn_pad;
+  a.idx_out = idx_out;
+  a.mind_out = mind_out;
+  a.idx_prev = idx_prev;
+  a.changed = changed;
+  const int grid = a.total_tiles < num_sms ? a.total_tiles : num_sms;
+  if (grid <= 0) return cudaSuccess;
+  if (fmt == 1) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(fk_assign_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tc::SMEM_BYTES);
+      attr = true;
+    }
+    fk_assign_tc_kernel<1><<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(tmx, tmc, a);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(fk_assign_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tc::SMEM_BYTES);
+      attr = true;
+    }
+    fk_assign_tc_kernel<0><<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(tmx, tmc, a);
+  }
+  return cudaGetLastError();
+}
+
+int assign_tc_kpad(int64_t K) { return (int)(((K + tc::BN - 1) / tc::BN) * tc::BN); }
+
+}  // namespace fk

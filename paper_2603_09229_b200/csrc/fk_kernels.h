@@ -1,0 +1,51 @@
+// fk_kernels.h -- internal launcher declarations shared by the .cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace fk {
+
+enum Dt { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2, DT_F64 = 3 };
+
+// fk_assign_tc.cu
+bool assign_tc_supported(int64_t d);
+int assign_tc_kpad(int64_t K);
+cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
+                             int64_t B, int64_t N, int64_t K, int64_t d, int32_t* idx_out,
+                             float* mind_out, const int32_t* idx_prev, int32_t* changed,
+                             int num_sms, cudaStream_t stream);
+
+// fk_assign_exact.cu
+cudaError_t launch_cn_pad(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
+                          float* cn_pad, cudaStream_t stream);
+cudaError_t launch_row_norms_exact(int dt, const void* M, int64_t rows, int64_t d, void* out,
+                                   cudaStream_t stream);
+cudaError_t launch_assign_exact(int dt, const void* X, const void* C, const void* xn,
+                                const void* cn, int64_t B, int64_t N, int64_t K, int64_t d,
+                                int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+                                int32_t* changed, cudaStream_t stream);
+cudaError_t launch_assign_cuda_core_lowp(int dt, const void* X, const void* C, const float* cn,
+                                         int64_t B, int64_t N, int64_t K, int64_t d,
+                                         int32_t* idx_out, float* mind_out,
+                                         const int32_t* idx_prev, int32_t* changed,
+                                         cudaStream_t stream);
+
+// fk_update.cu
+size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K);
+cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                          int64_t K, int64_t d, int64_t chunk, int accumulate, double* sums,
+                          int64_t* counts, int64_t* merges, void* ws, int num_sms,
+                          cudaStream_t stream);
+cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* counts,
+                             const void* prev, void* out, int operand_dt, void* operand_out,
+                             uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,
+                             int64_t d, cudaStream_t stream);
+size_t objective_workspace_bytes(int64_t B, int64_t N);
+cudaError_t launch_objective(int mind_is_f64, const void* mind, int64_t B, int64_t N, double* out,
+                             void* ws, cudaStream_t stream);
+cudaError_t launch_scatter(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                           int64_t K, int64_t d, double* sums, int64_t* counts,
+                           cudaStream_t stream);
+
+}  // namespace fk

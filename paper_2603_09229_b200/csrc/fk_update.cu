@@ -1,0 +1,571 @@
+// fk_update.cu -- sort-inverse centroid update, normalize and objective.
+//
+// Replaces sort_inverse_update (reference sort_inverse.py:106-149, kernels
+// counting_sort / segment_stats / merge_segments _kernels.py:118-171) with a
+// contention-free GPU scheme: no per-point scatter into shared accumulators.
+//
+//   k_hist     histogram of composite keys (b*K + id), smem-privatized when
+//              B*K fits in shared memory                      -> counts (exact)
+//   k_scan     one-block exclusive scan -> segment offsets, insertion cursors,
+//              int64 counts and the reference's synchronized_merges count
+//   k_scatter  bucket point indices by key (warp-aggregated cursor bumps);
+//              X itself is never permuted (sort_inverse.py:12-13)
+//   k_segsum   equal slices of the sorted order per warp; each warp streams the
+//              gathered rows with 16-byte vector loads, keeps per-lane running
+//              sums, and emits ONE merge per segment: segments owned by the
+//              slice are written directly, the <= 2 boundary segments per
+//              slice are merged with an f64 reduction.
+//
+// sums are f64 and counts int64, the reference's ClusterStats dtypes
+// (core.py:203-233).  bf16/fp16 rows accumulate in fp32 inside a slice; f32
+// and f64 rows accumulate in f64 so fp32 data reproduces the reference's
+// sums exactly.
+#include "fk_common.cuh"
+#include "fk_kernels.h"
+
+namespace fk {
+
+constexpr int HIST_SMEM_KEYS = 12288;  // 48 KB of int32 bins
+
+FK_DEV double as_f64(float v) { return (double)v; }
+FK_DEV double as_f64(double v) { return v; }
+FK_DEV double as_f64(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
+FK_DEV double as_f64(__half v) { return (double)__half2float(v); }
+
+// ----------------------------------------------------------------- hist
+__global__ void k_hist(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K,
+                       int32_t* __restrict__ hist) {
+  extern __shared__ int32_t sh[];
+  const int64_t BK = B * K;
+  const bool use_smem = BK <= HIST_SMEM_KEYS;
+  if (use_smem) {
+    for (int64_t k = threadIdx.x; k < BK; k += blockDim.x) sh[k] = 0;
+    __syncthreads();
+  }
+  const int64_t P = B * N;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += stride) {
+    const int64_t b = i / N;
+    const int32_t id = ids[i];
+    if (id < 0 || id >= K) continue;  // validated on the host side
+    const int64_t key = b * K + id;
+    if (use_smem)
+      atomicAdd(&sh[key], 1);
+    else {
+      // warp-aggregate identical keys: one global atomic per distinct key per warp
+      const unsigned peers = __match_any_sync(__activemask(), key);
+      const int leader = __ffs(peers) - 1;
+      if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[key], __popc(peers));
+    }
+  }
+  if (use_smem) {
+    __syncthreads();
+    for (int64_t k = threadIdx.x; k < BK; k += blockDim.x)
+      if (sh[k]) atomicAdd(&hist[k], sh[k]);
+  }
+}
+
+// ----------------------------------------------------------------- scan
+// Single block of 1024 threads; each thread owns a contiguous key range.
+__global__ void __launch_bounds__(1024)
+    k_scan(const int32_t* __restrict__ hist, int64_t B, int64_t N, int64_t K, int64_t chunk,
+           int accumulate, int64_t* __restrict__ off, int32_t* __restrict__ cursor,
+           int64_t* __restrict__ counts, int64_t* __restrict__ merges) {
+  __shared__ int64_t warp_tot[32];
+  __shared__ unsigned long long merge_acc;
+  const int64_t BK = B * K;
+  const int t = threadIdx.x;
+  const int64_t per = (BK + blockDim.x - 1) / blockDim.x;
+  const int64_t k0 = t * per;
+  const int64_t k1 = (k0 + per < BK) ? k0 + per : BK;
+  int64_t local = 0;
+  for (int64_t k = k0; k < k1; ++k) local += hist[k];
+  // block exclusive scan of `local`
+  int64_t v = local;
+  const int lane = t & 31, w = t >> 5;
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += u;
+  }
+  if (t == 0) merge_acc = 0;
+  if (lane == 31) warp_tot[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int64_t x = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t u = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += u;
+    }
+    warp_tot[lane] = x;  // inclusive over warps
+  }
+  __syncthreads();
+  int64_t run = v - local + (w > 0 ? warp_tot[w - 1] : 0);  // exclusive prefix
+  unsigned long long mg = 0;
+  for (int64_t k = k0; k < k1; ++k) {
+    const int64_t c = hist[k];
+    off[k] = run;
+    cursor[k] = (int32_t)run;
+    if (accumulate)
+      counts[k] += c;
+    else
+      counts[k] = c;
+    if (c > 0) {
+      // reference merges: the run [s, e) of this key inside its batch element
+      // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks.
+      const int64_t b = k / K;
+      const int64_t s = run - b * N, e = s + c;
+      mg += (unsigned long long)((e - 1) / chunk - s / chunk + 1);
+    }
+    run += c;
+  }
+  if (k1 == BK && k0 < k1) off[BK] = run;  // exactly one thread owns the last key
+  atomicAdd(&merge_acc, mg);
+  __syncthreads();
+  if (t == 0 && merges) atomicAdd((unsigned long long*)merges, merge_acc);
+}
+
+// ----------------------------------------------------------------- scatter
+__global__ void k_scatter(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K,
+                          int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
+  const int64_t P = B * N;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += stride) {
+    const int64_t b = i / N;
+    const int32_t id = ids[i];
+    if (id < 0 || id >= K) continue;
+    const int64_t key = b * K + id;
+    const unsigned mask = __activemask();
+    const unsigned peers = __match_any_sync(mask, key);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const int rank = __popc(peers & ((1u << lane) - 1));
+    order[base + rank] = (int32_t)i;
+  }
+}
+
+// ----------------------------------------------------------------- segsum
+template <typename T>
+struct VecCvt;
+template <>
+struct VecCvt<__nv_bfloat16> {
+  static constexpr int E = 8;
+  template <typename A>
+  FK_DEV static void add(A* acc, const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      acc[2 * i] += (A)__uint_as_float(w[i] << 16);
+      acc[2 * i + 1] += (A)__uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+template <>
+struct VecCvt<__half> {
+  static constexpr int E = 8;
+  template <typename A>
+  FK_DEV static void add(A* acc, const uint4& v) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+      acc[2 * i] += (A)f.x;
+      acc[2 * i + 1] += (A)f.y;
+    }
+  }
+};
+template <>
+struct VecCvt<float> {
+  static constexpr int E = 4;
+  template <typename A>
+  FK_DEV static void add(A* acc, const uint4& v) {
+    acc[0] += (A)__uint_as_float(v.x);
+    acc[1] += (A)__uint_as_float(v.y);
+    acc[2] += (A)__uint_as_float(v.z);
+    acc[3] += (A)__uint_as_float(v.w);
+  }
+};
+template <>
+struct VecCvt<double> {
+  static constexpr int E = 2;
+  template <typename A>
+  FK_DEV static void add(A* acc, const uint4& v) {
+    acc[0] += __hiloint2double((int)v.y, (int)v.x);
+    acc[1] += __hiloint2double((int)v.w, (int)v.z);
+  }
+};
+
+FK_DEV uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// LPR lanes cover one row with VPL 16-byte vectors each; RPW = 32/LPR rows per
+// warp step; U steps are issued back to back to keep bytes in flight.
+template <typename T, typename A, int LPR, int VPL, int U>
+__global__ void __launch_bounds__(256)
+    k_segsum(const T* __restrict__ X, const int32_t* __restrict__ order,
+             const int64_t* __restrict__ off, int64_t BK, int64_t P, int64_t L, int64_t d,
+             double* __restrict__ sums) {
+  constexpr int E = VecCvt<T>::E;
+  constexpr int RPW = 32 / LPR;
+  constexpr int NA = VPL * E;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR, sl = lane % LPR;
+  const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t p0 = wg * L;
+  if (p0 >= P) return;
+  const int64_t p1 = (p0 + L < P) ? p0 + L : P;
+  // segment containing p0: largest key with off[key] <= p0 < off[key+1]
+  int64_t lo = 0, hi = BK;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (off[mid] <= p0) lo = mid; else hi = mid;
+  }
+  int64_t key = lo;
+  int64_t seg_lo = off[key], seg_end = off[key + 1];
+  A acc[NA];
+#pragma unroll
+  for (int e = 0; e < NA; ++e) acc[e] = (A)0;
+  const int64_t row_elems = d;
+  int64_t p = p0;
+  while (p < p1) {
+    const int64_t lim = seg_end < p1 ? seg_end : p1;
+    while (p + RPW * U <= lim) {
+      int32_t ri[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) ri[u] = __ldg(order + p + u * RPW + sub);
+      uint4 v[U][VPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const T* rp = X + (int64_t)ri[u] * row_elems;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) v[u][q] = ldg_stream(rp + (q * LPR + sl) * E);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) VecCvt<T>::add(acc + q * E, v[u][q]);
+      p += RPW * U;
+    }
+    while (p < lim) {
+      const int64_t r = p + sub;
+      if (r < lim) {
+        const T* rp = X + (int64_t)__ldg(order + r) * row_elems;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) VecCvt<T>::add(acc + q * E, ldg_stream(rp + (q * LPR + sl) * E));
+      }
+      p += RPW;
+    }
+    p = lim;
+    // flush this segment's partial (one merge per segment)
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+      for (int e = 0; e < NA; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    if (sub == 0) {
+      const bool owned = seg_lo >= p0 && seg_end <= p1;
+      double* dst = sums + key * d;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q)
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          const int64_t j = (int64_t)(q * LPR + sl) * E + e;
+          if (owned)
+            dst[j] += (double)acc[q * E + e];
+          else
+            atomicAdd(dst + j, (double)acc[q * E + e]);
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < NA; ++e) acc[e] = (A)0;
+    if (p < p1) {
+      // next non-empty segment
+      ++key;
+      while (off[key + 1] <= p) ++key;
+      seg_lo = off[key];
+      seg_end = off[key + 1];
+    }
+  }
+}
+
+// Any row width: one warp per slice, lanes stride over the features.
+template <typename T>
+__global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restrict__ order,
+                                 const int64_t* __restrict__ off, int64_t BK, int64_t P,
+                                 int64_t L, int64_t d, double* __restrict__ sums) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t p0 = wg * L;
+  if (p0 >= P) return;
+  const int64_t p1 = (p0 + L < P) ? p0 + L : P;
+  int64_t lo = 0, hi = BK;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (off[mid] <= p0) lo = mid; else hi = mid;
+  }
+  int64_t key = lo;
+  int64_t p = p0;
+  while (p < p1) {
+    const int64_t seg_lo = off[key], seg_end = off[key + 1];
+    const int64_t lim = seg_end < p1 ? seg_end : p1;
+    const bool owned = seg_lo >= p0 && seg_end <= p1;
+    for (int64_t j0 = 0; j0 < d; j0 += 32) {
+      const int64_t j = j0 + lane;
+      double acc = 0.0;
+      if (j < d)
+        for (int64_t r = p; r < lim; ++r) acc += as_f64(X[(int64_t)order[r] * d + j]);
+      if (j < d) {
+        if (owned)
+          sums[key * d + j] += acc;
+        else
+          atomicAdd(sums + key * d + j, acc);
+      }
+    }
+    p = lim;
+    if (p < p1) {
+      ++key;
+      while (off[key + 1] <= p) ++key;
+    }
+  }
+}
+
+size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K) {
+  const int64_t BK = B * K, P = B * N;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  return al(BK * 4) + al(BK * 4) + al((BK + 1) * 8) + al(P * 4);
+}
+
+template <typename T, typename A>
+static cudaError_t dispatch_segsum(const void* X, const int32_t* order, const int64_t* off,
+                                   int64_t BK, int64_t P, int64_t d, double* sums, int num_sms,
+                                   cudaStream_t s) {
+  constexpr int E = VecCvt<T>::E;
+  const int th = 256;
+  const int64_t want_warps = (int64_t)num_sms * 8 * (th / 32);
+  int64_t L = (P + want_warps - 1) / want_warps;
+  if (L < 64) L = 64;
+  const int64_t warps = (P + L - 1) / L;
+  const unsigned grid = (unsigned)((warps * 32 + th - 1) / th);
+  const int64_t row_bytes = d * (int64_t)sizeof(T);
+  const bool vec_ok = (row_bytes % 16) == 0;
+  const int64_t nvec = row_bytes / 16;  // 16-byte vectors per row
+  const T* x = (const T*)X;
+#define FK_SEG(LPR, VPL, U) \
+  k_segsum<T, A, LPR, VPL, U><<<grid, th, 0, s>>>(x, order, off, BK, P, L, d, sums)
+  if (vec_ok) {
+    switch (nvec) {
+      case 1: FK_SEG(1, 1, 4); break;
+      case 2: FK_SEG(2, 1, 4); break;
+      case 4: FK_SEG(4, 1, 4); break;
+      case 8: FK_SEG(8, 1, 4); break;
+      case 16: FK_SEG(16, 1, 4); break;
+      case 32: FK_SEG(32, 1, 4); break;
+      case 64: FK_SEG(32, 2, 2); break;
+      case 128: FK_SEG(32, 4, 1); break;
+      default:
+        k_segsum_generic<T><<<grid, th, 0, s>>>(x, order, off, BK, P, L, d, sums);
+    }
+  } else {
+    k_segsum_generic<T><<<grid, th, 0, s>>>(x, order, off, BK, P, L, d, sums);
+  }
+#undef FK_SEG
+  (void)E;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                          int64_t K, int64_t d, int64_t chunk, int accumulate, double* sums,
+                          int64_t* counts, int64_t* merges, void* ws, int num_sms,
+                          cudaStream_t s) {
+  const int64_t BK = B * K, P = B * N;
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  uint8_t* w = (uint8_t*)ws;
+  int32_t* hist = (int32_t*)w;
+  w += al(BK * 4);
+  int32_t* cursor = (int32_t*)w;
+  w += al(BK * 4);
+  int64_t* off = (int64_t*)w;
+  w += al((BK + 1) * 8);
+  int32_t* order = (int32_t*)w;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(hist, 0, BK * 4, s)) != cudaSuccess) return e;
+  if (!accumulate && (e = cudaMemsetAsync(sums, 0, BK * d * 8, s)) != cudaSuccess) return e;
+  const int th = 512;
+  int64_t blocks = (P + th - 1) / th;
+  const int64_t cap = (int64_t)num_sms * 4;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  const size_t hsm = BK <= HIST_SMEM_KEYS ? BK * 4 : 0;
+  k_hist<<<(unsigned)blocks, th, hsm, s>>>(ids, B, N, K, hist);
+  k_scan<<<1, 1024, 0, s>>>(hist, B, N, K, chunk < 1 ? 1 : chunk, accumulate, off, cursor, counts,
+                            merges);
+  k_scatter<<<(unsigned)blocks, th, 0, s>>>(ids, B, N, K, cursor, order);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  switch (dt) {
+    case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, order, off, BK, P, d, sums, num_sms, s);
+    case DT_F16: return dispatch_segsum<__half, float>(X, order, off, BK, P, d, sums, num_sms, s);
+    case DT_F32: return dispatch_segsum<float, double>(X, order, off, BK, P, d, sums, num_sms, s);
+    default: return dispatch_segsum<double, double>(X, order, off, BK, P, d, sums, num_sms, s);
+  }
+}
+
+// ----------------------------------------------------------------- normalize
+template <typename TM, typename TO>
+__global__ void k_normalize(const double* __restrict__ sums, const int64_t* __restrict__ counts,
+                            const TM* prev, TM* out, TO* operand, uint8_t* empty,
+                            double* max_shift2, int64_t BK, int64_t d) {
+  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= BK) return;
+  const int64_t cnt = counts[row];
+  double sh = 0.0;
+  for (int64_t j = lane; j < d; j += 32) {
+    const int64_t o = row * d + j;
+    const TM old = prev[o];
+    TM nv = old;
+    if (cnt > 0) nv = (TM)(sums[o] / (double)cnt);
+    out[o] = nv;
+    if (operand) operand[o] = (TO)(float)nv;
+    const double df = (double)nv - (double)old;
+    sh += df * df;
+  }
+  if (lane == 0 && empty) empty[row] = cnt > 0 ? 0 : 1;
+  if (max_shift2) {
+    for (int o = 16; o; o >>= 1) sh += __shfl_xor_sync(0xffffffffu, sh, o);
+    if (lane == 0)
+      atomicMax((unsigned long long*)max_shift2, (unsigned long long)__double_as_longlong(sh));
+  }
+}
+
+template <typename TM>
+static cudaError_t norm_dispatch(int operand_dt, const double* sums, const int64_t* counts,
+                                 const void* prev, void* out, void* operand_out, uint8_t* empty,
+                                 double* ms2, int64_t BK, int64_t d, cudaStream_t s) {
+  const int th = 256;
+  const unsigned grid = (unsigned)((BK * 32 + th - 1) / th);
+  const TM* pv = (const TM*)prev;
+  TM* ov = (TM*)out;
+  if (!operand_out)
+    k_normalize<TM, float><<<grid, th, 0, s>>>(sums, counts, pv, ov, nullptr, empty, ms2, BK, d);
+  else if (operand_dt == DT_BF16)
+    k_normalize<TM, __nv_bfloat16><<<grid, th, 0, s>>>(sums, counts, pv, ov,
+                                                      (__nv_bfloat16*)operand_out, empty, ms2, BK, d);
+  else if (operand_dt == DT_F16)
+    k_normalize<TM, __half><<<grid, th, 0, s>>>(sums, counts, pv, ov, (__half*)operand_out, empty,
+                                               ms2, BK, d);
+  else if (operand_dt == DT_F32)
+    k_normalize<TM, float><<<grid, th, 0, s>>>(sums, counts, pv, ov, (float*)operand_out, empty,
+                                              ms2, BK, d);
+  else
+    k_normalize<TM, double><<<grid, th, 0, s>>>(sums, counts, pv, ov, (double*)operand_out, empty,
+                                               ms2, BK, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* counts,
+                             const void* prev, void* out, int operand_dt, void* operand_out,
+                             uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,
+                             int64_t d, cudaStream_t s) {
+  if (master_dt == DT_F64)
+    return norm_dispatch<double>(operand_dt, sums, counts, prev, out, operand_out, empty_mask,
+                                 max_shift2, B * K, d, s);
+  return norm_dispatch<float>(operand_dt, sums, counts, prev, out, operand_out, empty_mask,
+                              max_shift2, B * K, d, s);
+}
+
+// ----------------------------------------------------------------- objective
+// Deterministic two-level reduction: fixed 8192-element blocks summed in a
+// fixed tree, then the block partials summed in order per batch element.
+constexpr int OBJ_BLOCK = 8192;
+
+template <typename T>
+__global__ void k_obj_partial(const T* __restrict__ m, int64_t B, int64_t N, int64_t nblk,
+                              double* part) {
+  __shared__ double red[256];
+  const int64_t b = blockIdx.y, blk = blockIdx.x;
+  const int64_t lo = blk * OBJ_BLOCK;
+  const int64_t hi = (lo + OBJ_BLOCK < N) ? lo + OBJ_BLOCK : N;
+  double acc = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += 256) acc += (double)m[b * N + i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[b * nblk + blk] = red[0];
+}
+
+__global__ void k_obj_final(const double* part, int64_t B, int64_t nblk, double* out) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  double acc = 0.0;
+  for (int64_t i = 0; i < nblk; ++i) acc += part[b * nblk + i];
+  out[b] = acc;
+}
+
+size_t objective_workspace_bytes(int64_t B, int64_t N) {
+  return (size_t)(B * ((N + OBJ_BLOCK - 1) / OBJ_BLOCK)) * 8 + 256;
+}
+
+cudaError_t launch_objective(int mind_is_f64, const void* mind, int64_t B, int64_t N, double* out,
+                             void* ws, cudaStream_t s) {
+  const int64_t nblk = (N + OBJ_BLOCK - 1) / OBJ_BLOCK;
+  double* part = (double*)ws;
+  dim3 grid((unsigned)nblk, (unsigned)B);
+  if (mind_is_f64)
+    k_obj_partial<double><<<grid, 256, 0, s>>>((const double*)mind, B, N, nblk, part);
+  else
+    k_obj_partial<float><<<grid, 256, 0, s>>>((const float*)mind, B, N, nblk, part);
+  k_obj_final<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(part, B, nblk, out);
+  return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- scatter foil
+template <typename T>
+__global__ void k_scatter_atomic(const T* __restrict__ X, const int32_t* __restrict__ ids,
+                                 int64_t B, int64_t N, int64_t K, int64_t d, double* sums,
+                                 int64_t* counts) {
+  const int64_t P = B * N;
+  const int64_t total = P * d;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += stride) {
+    const int64_t i = e / d, j = e - i * d;
+    const int64_t b = i / N;
+    const int32_t id = ids[i];
+    if (id < 0 || id >= K) continue;
+    atomicAdd(&sums[(b * K + id) * d + j], as_f64(X[e]));
+    if (j == 0) atomicAdd((unsigned long long*)&counts[b * K + id], 1ull);
+  }
+}
+
+cudaError_t launch_scatter(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                           int64_t K, int64_t d, double* sums, int64_t* counts, cudaStream_t s) {
+  cudaMemsetAsync(sums, 0, B * K * d * 8, s);
+  cudaMemsetAsync(counts, 0, B * K * 8, s);
+  const unsigned grid = 148 * 8;
+  switch (dt) {
+    case DT_BF16:
+      k_scatter_atomic<__nv_bfloat16><<<grid, 256, 0, s>>>((const __nv_bfloat16*)X, ids, B, N, K,
+                                                          d, sums, counts);
+      break;
+    case DT_F16:
+      k_scatter_atomic<__half><<<grid, 256, 0, s>>>((const __half*)X, ids, B, N, K, d, sums, counts);
+      break;
+    case DT_F32:
+      k_scatter_atomic<float><<<grid, 256, 0, s>>>((const float*)X, ids, B, N, K, d, sums, counts);
+      break;
+    default:
+      k_scatter_atomic<double><<<grid, 256, 0, s>>>((const double*)X, ids, B, N, K, d, sums,
+                                                    counts);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace fk

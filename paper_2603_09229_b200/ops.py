@@ -1,0 +1,197 @@
+"""Device operators: thin torch wrappers over the C ABI.
+
+Each function takes CUDA tensors, allocates the caller-owned outputs (the
+reference's ownership rule: flash_assign.py:162-163, sort_inverse.py:125),
+passes raw pointers plus torch's current stream to the library, and returns
+tensors.  Nothing here computes on the host; nothing synchronizes.
+"""
+
+from __future__ import annotations
+
+import threading
+
+import torch
+
+from . import _native as N
+
+_DT = {torch.float32: N.FK_F32, torch.bfloat16: N.FK_BF16, torch.float16: N.FK_F16,
+       torch.float64: N.FK_F64}
+LOWP = (torch.bfloat16, torch.float16)
+
+
+def fk_dtype(t: torch.dtype) -> int:
+    try:
+        return _DT[t]
+    except KeyError:
+        raise ValueError(f"unsupported element type {t}; expected float32/float64/bfloat16/float16") from None
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class _Workspace(threading.local):
+    """Per-thread, per-(device, stream) scratch that only grows."""
+
+    def __init__(self):
+        self.bufs: dict = {}
+
+    def get(self, device: torch.device, nbytes: int, tag: str = "") -> torch.Tensor | None:
+        if nbytes <= 0:
+            return None
+        key = (device.index, torch.cuda.current_stream(device).cuda_stream, tag)
+        buf = self.bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+            self.bufs[key] = buf
+        return buf
+
+
+_ws = _Workspace()
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("device operators take CUDA tensors")
+    dev = ts[0].device
+    if N.lib().fk_device_supported(dev.index if dev.index is not None else 0) != 1:
+        raise NotImplementedError("flash-kmeans kernels are compiled for sm_100a (B200) only")
+    return dev
+
+
+def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = None,
+           changed: torch.Tensor | None = None, idx_out: torch.Tensor | None = None,
+           mind_out: torch.Tensor | None = None):
+    """Nearest centroid per point: (ids int32 (B,N), min_dists (B,N)).
+
+    min_dists is in the data dtype for float32/float64 data and float32 for
+    bfloat16/float16 data.  If ``idx_prev`` is given, ``changed`` (int32
+    device scalar) is OR-ed with 1 when any id differs.
+    """
+    dev = _require_cuda(x, c)
+    if x.dim() != 3 or c.dim() != 3 or x.shape[0] != c.shape[0] or x.shape[2] != c.shape[2]:
+        raise ValueError("x must be (B,N,d) and c (B,K,d) with matching B and d")
+    if x.dtype != c.dtype:
+        raise ValueError("data and centroids must share one precision")
+    x = x.contiguous()
+    c = c.contiguous()
+    B, n, d = x.shape
+    K = c.shape[1]
+    dt = fk_dtype(x.dtype)
+    if idx_out is None:
+        idx_out = torch.empty((B, n), dtype=torch.int32, device=dev)
+    if mind_out is None:
+        mdt = torch.float32 if x.dtype in LOWP else x.dtype
+        mind_out = torch.empty((B, n), dtype=mdt, device=dev)
+    L = N.lib()
+    need = L.fk_assign_workspace(dt, B, n, K, d)
+    ws = _ws.get(dev, need, "assign")
+    st = L.fk_assign(dt, x.data_ptr(), c.data_ptr(), B, n, K, d, idx_out.data_ptr(),
+                     mind_out.data_ptr(), None if idx_prev is None else idx_prev.data_ptr(),
+                     None if changed is None else changed.data_ptr(),
+                     None if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                     _stream(dev))
+    N.check(st, "fk_assign")
+    return idx_out, mind_out
+
+
+def update(x: torch.Tensor, ids: torch.Tensor, clusters: int, chunk: int | None = None,
+           accumulate: bool = False, sums: torch.Tensor | None = None,
+           counts: torch.Tensor | None = None, merges: torch.Tensor | None = None):
+    """Sort-inverse cluster statistics: (sums f64 (B,K,d), counts int64 (B,K)).
+
+    ``merges`` (int64 device scalar, optional) is incremented by the segment
+    count the reference's sort_inverse_update would record for ``chunk``.
+    """
+    dev = _require_cuda(x, ids)
+    x = x.contiguous()
+    ids = ids.contiguous()
+    B, n, d = x.shape
+    if ids.shape != (B, n) or ids.dtype != torch.int32:
+        raise ValueError("ids must be int32 (B,N) matching x")
+    K = int(clusters)
+    dt = fk_dtype(x.dtype)
+    if sums is None:
+        sums = torch.empty((B, K, d), dtype=torch.float64, device=dev)
+    if counts is None:
+        counts = torch.empty((B, K), dtype=torch.int64, device=dev)
+    L = N.lib()
+    need = L.fk_update_workspace(dt, B, n, K, d)
+    ws = _ws.get(dev, need, "update")
+    st = L.fk_update(dt, x.data_ptr(), ids.data_ptr(), B, n, K, d, int(chunk or n),
+                     1 if accumulate else 0, sums.data_ptr(), counts.data_ptr(),
+                     None if merges is None else merges.data_ptr(), ws.data_ptr(), ws.numel(),
+                     _stream(dev))
+    N.check(st, "fk_update")
+    return sums, counts
+
+
+def normalize(sums: torch.Tensor, counts: torch.Tensor, prev: torch.Tensor,
+              out: torch.Tensor | None = None, operand_dtype: torch.dtype | None = None,
+              operand_out: torch.Tensor | None = None, empty: torch.Tensor | None = None,
+              shift2: torch.Tensor | None = None):
+    """c = sums/counts (empty clusters keep ``prev`` bitwise).
+
+    ``prev``/``out`` are float32 or float64 masters; ``operand_out`` gets the
+    rounded copy in ``operand_dtype`` (the next MMA operand).  ``shift2``
+    (f64 device scalar, pre-zeroed) receives max_k ||out_k - prev_k||^2.
+    Returns (out, operand_out, empty_mask uint8 (B,K)).
+    """
+    dev = _require_cuda(sums, counts, prev)
+    B, K, d = prev.shape
+    mdt = fk_dtype(prev.dtype)
+    if prev.dtype not in (torch.float32, torch.float64):
+        raise ValueError("centroid masters are float32 or float64")
+    if out is None:
+        out = torch.empty_like(prev)
+    if operand_dtype is not None and operand_out is None:
+        operand_out = torch.empty((B, K, d), dtype=operand_dtype, device=dev)
+    if empty is None:
+        empty = torch.empty((B, K), dtype=torch.uint8, device=dev)
+    odt = fk_dtype(operand_out.dtype) if operand_out is not None else 0
+    st = N.lib().fk_normalize(mdt, sums.data_ptr(), counts.data_ptr(), prev.data_ptr(),
+                              out.data_ptr(), odt,
+                              None if operand_out is None else operand_out.data_ptr(),
+                              empty.data_ptr(), None if shift2 is None else shift2.data_ptr(),
+                              B, K, d, _stream(dev))
+    N.check(st, "fk_normalize")
+    return out, operand_out, empty
+
+
+def objective(mind: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Per-batch float64 sum of min_dists (pipeline._objective_row)."""
+    dev = _require_cuda(mind)
+    B, n = mind.shape
+    if out is None:
+        out = torch.empty((B,), dtype=torch.float64, device=dev)
+    L = N.lib()
+    need = L.fk_objective_workspace(B, n)
+    ws = _ws.get(dev, need, "objective")
+    st = L.fk_objective(fk_dtype(mind.dtype), mind.data_ptr(), B, n, out.data_ptr(),
+                        ws.data_ptr(), ws.numel(), _stream(dev))
+    N.check(st, "fk_objective")
+    return out
+
+
+def row_norms(m: torch.Tensor) -> torch.Tensor:
+    """Exact row norms of a (rows, d) float32/float64 CUDA matrix (core.row_norms)."""
+    dev = _require_cuda(m)
+    m = m.contiguous()
+    out = torch.empty((m.shape[0],), dtype=m.dtype, device=dev)
+    st = N.lib().fk_row_norms(fk_dtype(m.dtype), m.data_ptr(), m.shape[0], m.shape[1],
+                              out.data_ptr(), _stream(dev))
+    N.check(st, "fk_row_norms")
+    return out
+
+
+def scatter(x: torch.Tensor, ids: torch.Tensor, clusters: int):
+    """Contended atomic scatter (baseline.scatter_update foil, ncu comparisons only)."""
+    dev = _require_cuda(x, ids)
+    B, n, d = x.shape
+    sums = torch.empty((B, clusters, d), dtype=torch.float64, device=dev)
+    counts = torch.empty((B, clusters), dtype=torch.int64, device=dev)
+    st = N.lib().fk_scatter(fk_dtype(x.dtype), x.contiguous().data_ptr(), ids.contiguous().data_ptr(),
+                            B, n, clusters, d, sums.data_ptr(), counts.data_ptr(), _stream(dev))
+    N.check(st, "fk_scatter")
+    return sums, counts
