@@ -1,0 +1,553 @@
+"""Run drivers: the in-core Lloyd loop and the chunked out-of-core variant.
+
+Drop-in for reference pipeline.py:1-530 with the same termination semantics
+(pipeline.py:110-147): stop when assignments repeat, when the largest
+centroid shift falls to shift_tol, or at max_iters.  B200 design:
+
+* ``LloydEngine`` keeps everything device-resident: X, two assignment
+  buffers (ping-pong, so the repeat test is a device flag raised by the assign
+  kernel), the f64/int64 statistics, a float32/float64 centroid master and the
+  bf16/fp16 MMA operand, the objective history.  One iteration is four
+  launches (assign, objective, update, normalize) and ONE 16-byte
+  device->host read (changed flag + max shift) -- the only host sync.
+* ``_streaming_pass`` streams pinned host chunks over a dedicated copy stream
+  into two device buffers (event-gated ping-pong), overlapping H2D of chunk
+  t+1 with assign+update of chunk t, accumulating statistics on the device
+  and normalizing once per pass (pipeline.py:312-373).
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .baseline import argmin_rows, compute_distance_matrix, gather_assigned_distances, scatter_update
+from .core import (INIT_METHODS, LOW_PRECISION, Assignments, Centroids, ClusterStats, Counters,
+                   DataFormatError, DataMatrix, KMeansConfig, KMeansResult, device_of, init_indices,
+                   master_dtype, to_device)
+from .flash_assign import TilingConfig
+from .tuner import CacheModel, ProblemShape, heuristic_config
+
+__all__ = ["LloydEngine", "HostStream", "PartialStats", "DeviceAssignmentStore", "lloyd_run",
+           "out_of_core_iteration", "chunked_stream_run", "ENGINES"]
+
+ENGINES = ("flash", "baseline")
+
+
+def _resolve_tiling(cfg: KMeansConfig, points: int, dims: int, batch: int, elem: int,
+                    workers: int) -> TilingConfig:
+    if cfg.tiling is not None:
+        return cfg.tiling
+    shape = ProblemShape(points=points, clusters=cfg.clusters, dims=dims, batch=batch)
+    return heuristic_config(shape, CacheModel(elem_bytes=elem, workers=workers))
+
+
+def _workers(workers):
+    from .core import worker_count
+
+    return worker_count(workers)
+
+
+class LloydEngine:
+    """Device-resident Lloyd state for one (B, N, K, d) problem.
+
+    ``x`` is a CUDA tensor (B, N, d).  ``update_chunk`` only defines the
+    reference-compatible merge count.  ``allreduce`` (optional) is called
+    once per iteration with a packed float64 device buffer
+    [sums | counts | objective | changed] to combine point shards
+    (distributed.py); it must sum in place.
+    """
+
+    def __init__(self, x: torch.Tensor, clusters: int, update_chunk: int | None = None,
+                 allreduce=None, backend=None):
+        # ``backend`` provides assign/objective/update/normalize with the
+        # signatures of ``ops``; the product always uses ``ops`` (CUDA).  Tests
+        # substitute a CPU checker to exercise the orchestration under gloo.
+        self.be = ops if backend is None else backend
+        if backend is None and not x.is_cuda:
+            raise ValueError("LloydEngine needs the data on a CUDA device")
+        self.x = x.contiguous()
+        self.B, self.N, self.d = self.x.shape
+        self.K = int(clusters)
+        self.chunk = int(update_chunk or self.N)
+        self.dev = self.x.device
+        self.allreduce = allreduce
+        B, N, K, d, dev = self.B, self.N, self.K, self.d, self.dev
+        self.dtype = self.x.dtype
+        self.mdtype = master_dtype(self.dtype)
+        self.ids = [torch.empty((B, N), dtype=torch.int32, device=dev) for _ in range(2)]
+        self.mind = torch.empty((B, N), dtype=torch.float32 if self.dtype in LOW_PRECISION
+                                else self.dtype, device=dev)
+        nred = B * K * d + B * K + B + 1
+        self.red = torch.empty((nred,), dtype=torch.float64, device=dev)
+        self.sums = self.red[: B * K * d].view(B, K, d)
+        self.counts_f = self.red[B * K * d: B * K * d + B * K].view(B, K)
+        self.obj_red = self.red[B * K * d + B * K: B * K * d + B * K + B]
+        self.changed_f = self.red[-1:]
+        self.counts = torch.empty((B, K), dtype=torch.int64, device=dev)
+        self.master = [torch.empty((B, K, d), dtype=self.mdtype, device=dev) for _ in range(2)]
+        if self.dtype in LOW_PRECISION:
+            self.operand = [torch.empty((B, K, d), dtype=self.dtype, device=dev) for _ in range(2)]
+        else:
+            self.operand = self.master
+        self.empty = torch.empty((B, K), dtype=torch.uint8, device=dev)
+        # scalars: [changed(int32) | pad] and [shift2 (f64)] and merges (int64)
+        self.changed = torch.zeros((), dtype=torch.int32, device=dev)
+        self.shift2 = torch.zeros((), dtype=torch.float64, device=dev)
+        self.merges = torch.zeros((), dtype=torch.int64, device=dev)      # committed updates
+        self.merges_it = torch.zeros((), dtype=torch.int64, device=dev)   # this iteration
+        self.obj = torch.empty((B,), dtype=torch.float64, device=dev)
+        self.cur = 0
+        self.it = 0
+
+    # -------------------------------------------------------------- state
+    def set_centroids(self, c: torch.Tensor) -> None:
+        c = to_device(c, self.dev)
+        self.master[self.cur].copy_(c.to(self.mdtype))
+        if self.operand is not self.master:
+            self.operand[self.cur].copy_(self.master[self.cur].to(self.dtype))
+        self.it = 0
+
+    @property
+    def centroids(self) -> torch.Tensor:
+        return self.master[self.cur]
+
+    @property
+    def operand_centroids(self) -> torch.Tensor:
+        return self.operand[self.cur]
+
+    # -------------------------------------------------------------- phases
+    def assign(self, out_slot: int, compare: bool):
+        self.be.assign(self.x, self.operand[self.cur], idx_prev=self.ids[out_slot ^ 1] if compare else None,
+                   changed=self.changed if compare else None, idx_out=self.ids[out_slot],
+                   mind_out=self.mind)
+
+    def iterate(self, history_row: torch.Tensor | None = None):
+        """One Lloyd iteration, fully on the device.
+
+        Writes: ids[slot] (this iteration's assignment), objective, the next
+        master/operand into the other centroid slot, the changed flag and
+        max squared shift.  Returns the assignment slot used."""
+        slot = self.it & 1
+        compare = self.it > 0
+        self.changed.zero_()
+        self.shift2.zero_()
+        self.merges_it.zero_()
+        self.assign(slot, compare)
+        self.be.objective(self.mind, out=self.obj)
+        self.be.update(self.x, self.ids[slot], self.K, self.chunk, sums=self.sums, counts=self.counts,
+                   merges=self.merges_it)
+        if self.allreduce is not None:
+            self.counts_f.copy_(self.counts)
+            self.obj_red.copy_(self.obj)
+            self.changed_f.copy_(self.changed)
+            self.allreduce(self.red)
+            self.counts.copy_(self.counts_f)
+            self.obj.copy_(self.obj_red)
+            self.changed.copy_((self.changed_f[0] > 0).to(torch.int32))
+        if history_row is not None:
+            history_row.copy_(self.obj)
+        nxt = self.cur ^ 1
+        self.be.normalize(self.sums, self.counts, self.master[self.cur], out=self.master[nxt],
+                      operand_out=None if self.operand is self.master else self.operand[nxt],
+                      empty=self.empty, shift2=self.shift2)
+        self.it += 1
+        return slot
+
+    def poll(self):
+        """(changed: bool, shift: float) -- the one device->host read per iteration."""
+        v = torch.stack([self.changed.to(torch.float64), self.shift2]).cpu()
+        return bool(v[0] != 0), math.sqrt(float(v[1]))
+
+    def commit(self) -> None:
+        """Adopt the normalized centroids (the swap `c = new_c`); the update ran for real."""
+        self.cur ^= 1
+        self.merges += self.merges_it
+
+    def reseed_farthest(self, slot: int) -> None:
+        """reseed_farthest policy (pipeline.py:76-89): each empty cluster takes the
+        next-farthest point (distance desc, index asc), in id order."""
+        nxt = self.cur ^ 1
+        em = self.empty.cpu().numpy()
+        for b in range(self.B):
+            empties = np.flatnonzero(em[b])
+            if empties.size == 0:
+                continue
+            order = torch.sort(-self.mind[b].double(), stable=True).indices
+            rows = order[: empties.size]
+            cid = torch.from_numpy(empties).to(self.dev)
+            self.master[nxt][b, cid] = self.x[b, rows].to(self.mdtype)
+            if self.operand is not self.master:
+                self.operand[nxt][b, cid] = self.x[b, rows]
+        diff = self.master[nxt].double() - self.master[self.cur].double()
+        self.shift2.copy_((diff * diff).sum(-1).max())
+
+
+def lloyd_run(x: DataMatrix, cfg: KMeansConfig, engine: str = "flash", workers: int | None = None,
+              counters: Counters | None = None) -> KMeansResult:
+    """Full in-core run (pipeline.py:110-147); device-resident, one host sync per iteration.
+
+    objective_history[i, b] is the float64 sum of assigned squared distances
+    observed by iteration i's assignment step."""
+    if engine not in ENGINES:
+        raise ValueError(f"engine must be one of {ENGINES}")
+    counters = counters if counters is not None else Counters()
+    n_workers = _workers(workers)
+    tiling = _resolve_tiling(cfg, x.points, x.dims, x.batch, x.elem_bytes, n_workers)
+    dev = device_of(x.data)
+    xd = to_device(x.data, dev)
+    if engine == "baseline":
+        return _lloyd_baseline(DataMatrix(xd, check_finite=False), cfg, counters)
+    idx = init_indices(x.points, cfg.clusters, cfg.seed, x.batch, cfg.init, x.data)
+    it_ = torch.from_numpy(idx).to(dev)
+    c0 = torch.stack([xd[b].index_select(0, it_[b]) for b in range(x.batch)])
+    eng = LloydEngine(xd, cfg.clusters, tiling.update_chunk)
+    eng.set_centroids(c0)
+    history = torch.empty((cfg.max_iters, x.batch), dtype=torch.float64, device=dev)
+    iterations = 0
+    slot = 0
+    for it in range(1, cfg.max_iters + 1):
+        iterations = it
+        slot = eng.iterate(history[it - 1])
+        changed, shift = eng.poll()
+        if it > 1 and not changed:
+            break  # assignments repeated: the update reproduces c bitwise
+        if cfg.empty_cluster_policy == "reseed_farthest":
+            eng.reseed_farthest(slot)
+            _, shift = eng.poll()
+        eng.commit()
+        if shift <= cfg.shift_tol:
+            break
+    counters.synchronized_merges += int(eng.merges.item())
+    return KMeansResult(Centroids(eng.centroids.clone(), check_finite=False),
+                        Assignments(eng.ids[slot].clone(), validate=False),
+                        history[:iterations].cpu().numpy(), iterations, counters)
+
+
+def _lloyd_baseline(x: DataMatrix, cfg: KMeansConfig, counters: Counters) -> KMeansResult:
+    """engine="baseline": the materializing foil (baseline.py), same decisions."""
+    from .baseline import normalize
+    from .core import init_centroids
+
+    c = init_centroids(x, cfg.clusters, cfg.seed, cfg.init)
+    if c.data.dtype in LOW_PRECISION:
+        c = Centroids(c.data.float(), check_finite=False)
+    history, prev, a = [], None, None
+    iterations = 0
+    for it in range(1, cfg.max_iters + 1):
+        iterations = it
+        xc = x if c.data.dtype == x.data.dtype else DataMatrix(x.data.float(), check_finite=False)
+        d = compute_distance_matrix(xc, c, counters)
+        a = argmin_rows(d)
+        mind = gather_assigned_distances(d, a)
+        history.append(mind.double().sum(dim=1).cpu().numpy())
+        if prev is not None and torch.equal(prev.values, a.values):
+            break
+        stats = scatter_update(xc, a, cfg.clusters, counters)
+        new_c, _ = normalize(stats, c, cfg.empty_cluster_policy)
+        diff = new_c.data.double() - c.data.double()
+        shift = float((diff * diff).sum(-1).max().sqrt())
+        prev, c = a, new_c
+        if shift <= cfg.shift_tol:
+            break
+    return KMeansResult(c, a, np.array(history), iterations, counters)
+
+
+# ============================================================== streaming
+class HostStream:
+    """Chunk-granular source over a host-resident (B, N, d) array.
+
+    Stands in for the reference's file-backed ChunkStream (pipeline.py:150-234)
+    with the same surface (batch, total_points, dims, precision, chunk_points,
+    n_chunks, bounds, read_rows).  The array is pinned once so every chunk is a
+    true async DMA (cudaMemcpyAsync from page-locked memory)."""
+
+    def __init__(self, data, chunk_points: int, pin: bool = True):
+        if int(chunk_points) < 1:
+            raise ValueError("chunk_points must be >= 1")
+        t = data.data if isinstance(data, DataMatrix) else (
+            torch.from_numpy(np.ascontiguousarray(data)) if isinstance(data, np.ndarray) else data)
+        if t.dim() != 3:
+            raise DataFormatError("stream payload must be (batch, points, dims)")
+        if t.is_cuda:
+            raise ValueError("HostStream wraps host memory; use lloyd_run for device data")
+        self.host = t.contiguous()
+        if pin and not self.host.is_pinned():
+            self.host = self.host.pin_memory()
+        self.batch, self.total_points, self.dims = self.host.shape
+        self.chunk_points = min(int(chunk_points), self.total_points)
+        self.path = None
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self.host.dtype
+
+    @property
+    def precision(self) -> str:
+        from .core import precision_for
+
+        return precision_for(self.host.dtype)
+
+    @property
+    def elem_bytes(self) -> int:
+        return self.host.element_size()
+
+    @property
+    def n_chunks(self) -> int:
+        return -(-self.total_points // self.chunk_points)
+
+    def bounds(self, t: int) -> tuple[int, int]:
+        if not 0 <= t < self.n_chunks:
+            raise ValueError(f"chunk index {t} out of range")
+        lo = t * self.chunk_points
+        return lo, min(self.total_points, lo + self.chunk_points)
+
+    def view(self, b: int, lo: int, hi: int) -> torch.Tensor:
+        if not 0 <= b < self.batch or not 0 <= lo < hi <= self.total_points:
+            raise ValueError("row range outside the stream bounds")
+        return self.host[b, lo:hi]
+
+    def read_rows(self, b: int, lo: int, hi: int) -> torch.Tensor:
+        return self.view(b, lo, hi).clone()
+
+    def close(self) -> None:
+        pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+@dataclass
+class PartialStats:
+    """One chunk's cluster sums/counts; combined in ascending chunk order (pipeline.py:237-258)."""
+
+    chunk_index: int
+    sums: torch.Tensor
+    counts: torch.Tensor
+
+    def __post_init__(self):
+        if self.sums.dim() != 2 or self.sums.dtype != torch.float64:
+            raise ValueError("PartialStats.sums must be (clusters, dims) float64")
+        if tuple(self.counts.shape) != tuple(self.sums.shape[:1]) or self.counts.dtype != torch.int64:
+            raise ValueError("PartialStats.counts must be (clusters,) int64")
+
+    def combine(self, other: "PartialStats") -> "PartialStats":
+        if self.sums.shape != other.sums.shape:
+            raise ValueError("cannot combine partials of different shapes")
+        return PartialStats(min(self.chunk_index, other.chunk_index), self.sums + other.sums,
+                            self.counts + other.counts)
+
+
+class DeviceAssignmentStore:
+    """Device-resident stand-in for the reference's FKA1 AssignmentStore
+    (fileio.py:189-247): holds this pass's and the previous pass's ids and
+    raises a device changed flag; starts from the 0xFFFFFFFF sentinel."""
+
+    def __init__(self, batch: int, points: int, device):
+        self.batch, self.points = batch, points
+        self.ids = [torch.full((batch, points), -1, dtype=torch.int32, device=device) for _ in range(2)]
+        self.cur = 0
+        self.changed = torch.zeros((), dtype=torch.int32, device=device)
+
+    def begin_pass(self):
+        self.cur ^= 1
+        self.changed.zero_()
+
+    @property
+    def new(self) -> torch.Tensor:
+        return self.ids[self.cur]
+
+    @property
+    def old(self) -> torch.Tensor:
+        return self.ids[self.cur ^ 1]
+
+    def read_all(self) -> Assignments:
+        return Assignments(self.new.clone(), validate=False)
+
+    def finalize(self) -> None:
+        pass
+
+    def abort(self) -> None:
+        pass
+
+
+class _StreamState:
+    """Device buffers and streams for the chunk pipeline of one stream shape."""
+
+    def __init__(self, stream: HostStream, clusters: int, device):
+        self.dev = device
+        cp, d = stream.chunk_points, stream.dims
+        self.buf = [torch.empty((1, cp, d), dtype=stream.dtype, device=device) for _ in range(2)]
+        self.mind = torch.empty((1, cp), dtype=torch.float32 if stream.dtype in LOW_PRECISION
+                                else stream.dtype, device=device)
+        self.copy_stream = torch.cuda.Stream(device=device)
+        self.ready = [torch.cuda.Event() for _ in range(2)]
+        self.free = [torch.cuda.Event() for _ in range(2)]
+        B = stream.batch
+        self.sums = torch.zeros((B, clusters, d), dtype=torch.float64, device=device)
+        self.counts = torch.zeros((B, clusters), dtype=torch.int64, device=device)
+        self.obj = torch.zeros((B,), dtype=torch.float64, device=device)
+        self.obj_chunk = torch.empty((1,), dtype=torch.float64, device=device)
+        self.merges = torch.zeros((), dtype=torch.int64, device=device)
+
+
+def _streaming_pass(stream: HostStream, master: torch.Tensor, operand: torch.Tensor, clusters: int,
+                    chunk: int, counters: Counters, store: DeviceAssignmentStore, st: _StreamState,
+                    new_master: torch.Tensor, new_operand: torch.Tensor | None,
+                    shift2: torch.Tensor, empty: torch.Tensor, allreduce=None):
+    """One pass (pipeline.py:312-373): per-chunk assign + update, then normalize.
+
+    With ``allreduce`` (multi-GPU, each rank streaming its own row shard) the
+    pass statistics, objective and changed flag are summed across ranks with
+    one packed float64 all-reduce before the (replicated) normalize."""
+    st.sums.zero_()
+    st.counts.zero_()
+    st.obj.zero_()
+    shift2.zero_()
+    store.begin_pass()
+    compute = torch.cuda.current_stream(st.dev)
+    tasks = [(b, t) for b in range(stream.batch) for t in range(stream.n_chunks)]
+
+    def issue_copy(i):
+        b, t = tasks[i]
+        lo, hi = stream.bounds(t)
+        k = i & 1
+        with torch.cuda.stream(st.copy_stream):
+            st.copy_stream.wait_event(st.free[k])
+            st.buf[k][0, : hi - lo].copy_(stream.view(b, lo, hi), non_blocking=True)
+            st.ready[k].record(st.copy_stream)
+
+    for k in range(2):  # both buffers start free
+        st.free[k].record(compute)
+    if tasks:
+        issue_copy(0)
+    for i, (b, t) in enumerate(tasks):
+        if i + 1 < len(tasks):
+            issue_copy(i + 1)
+        lo, hi = stream.bounds(t)
+        rows = hi - lo
+        k = i & 1
+        compute.wait_event(st.ready[k])
+        xb = st.buf[k][:, :rows]
+        ids_new = store.new[b: b + 1, lo:hi]   # contiguous: one row segment of (B, N)
+        ids_old = store.old[b: b + 1, lo:hi]
+        ops.assign(xb, operand[b: b + 1], idx_prev=ids_old, changed=store.changed,
+                   idx_out=ids_new, mind_out=st.mind[:, :rows])
+        ops.objective(st.mind[:, :rows], out=st.obj_chunk)
+        st.obj[b: b + 1] += st.obj_chunk
+        ops.update(xb, ids_new, clusters, chunk, accumulate=True, sums=st.sums[b: b + 1],
+                   counts=st.counts[b: b + 1], merges=st.merges)
+        st.free[k].record(compute)
+        counters.elements_streamed += rows
+    if allreduce is not None:
+        red = torch.cat([st.sums.reshape(-1), st.counts.reshape(-1).double(), st.obj,
+                         store.changed.reshape(1).double()])
+        allreduce(red)
+        n1, n2 = st.sums.numel(), st.counts.numel()
+        st.sums.copy_(red[:n1].view_as(st.sums))
+        st.counts.copy_(red[n1:n1 + n2].view_as(st.counts).to(torch.int64))
+        st.obj.copy_(red[n1 + n2:n1 + n2 + st.obj.numel()])
+        store.changed.copy_((red[-1] > 0).to(torch.int32))
+    ops.normalize(st.sums, st.counts, master, out=new_master, operand_out=new_operand, empty=empty,
+                  shift2=shift2)
+
+
+def _init_from_stream(stream: HostStream, clusters: int, seed: int, method: str) -> torch.Tensor:
+    """Same row draws as the in-core initializer (pipeline.py:456-479)."""
+    if method not in INIT_METHODS:
+        raise ValueError(f"init method must be one of {INIT_METHODS}")
+    if clusters > stream.total_points:
+        raise ValueError(f"cannot place {clusters} clusters with only {stream.total_points} points")
+    idx = init_indices(stream.total_points, clusters, seed, stream.batch, method,
+                       stream.host if method == "kmeanspp" else None)
+    out = torch.stack([stream.host[b][torch.from_numpy(idx[b])] for b in range(stream.batch)])
+    return out.contiguous()
+
+
+class _StreamRunner:
+    def __init__(self, stream: HostStream, clusters: int, device, chunk: int, allreduce=None):
+        self.allreduce = allreduce
+        self.stream = stream
+        self.K = clusters
+        self.chunk = chunk
+        self.dev = device
+        self.st = _StreamState(stream, clusters, device)
+        B, K, d = stream.batch, clusters, stream.dims
+        self.mdt = master_dtype(stream.dtype)
+        self.master = [torch.empty((B, K, d), dtype=self.mdt, device=device) for _ in range(2)]
+        self.lowp = stream.dtype in LOW_PRECISION
+        self.operand = ([torch.empty((B, K, d), dtype=stream.dtype, device=device) for _ in range(2)]
+                        if self.lowp else self.master)
+        self.shift2 = torch.zeros((), dtype=torch.float64, device=device)
+        self.empty = torch.empty((B, K), dtype=torch.uint8, device=device)
+        self.store = DeviceAssignmentStore(B, stream.total_points, device)
+        self.cur = 0
+
+    def set(self, c: torch.Tensor):
+        self.master[self.cur].copy_(to_device(c, self.dev).to(self.mdt))
+        if self.lowp:
+            self.operand[self.cur].copy_(self.master[self.cur].to(self.stream.dtype))
+
+    def one_pass(self, counters: Counters):
+        nxt = self.cur ^ 1
+        _streaming_pass(self.stream, self.master[self.cur], self.operand[self.cur], self.K,
+                        self.chunk, counters, self.store, self.st, self.master[nxt],
+                        self.operand[nxt] if self.lowp else None, self.shift2, self.empty,
+                        self.allreduce)
+        v = torch.stack([self.store.changed.to(torch.float64), self.shift2]).cpu()
+        return bool(v[0] != 0), math.sqrt(float(v[1]))
+
+
+def out_of_core_iteration(stream: HostStream, c: Centroids, cfg: KMeansConfig, counters: Counters,
+                          store=None, workers: int | None = None, device=None):
+    """One streaming Lloyd iteration (pipeline.py:385-417): returns (new centroids,
+    assignment store, counters)."""
+    if c.batch != stream.batch or c.dims != stream.dims:
+        raise ValueError("centroids do not match the stream shape")
+    if c.clusters != cfg.clusters:
+        raise ValueError("centroid count does not match the configuration")
+    dev = device or device_of(c.data)
+    tiling = _resolve_tiling(cfg, stream.total_points, stream.dims, stream.batch, stream.elem_bytes,
+                             _workers(workers))
+    run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk)
+    if store is not None:
+        run.store = store
+    run.set(c.data)
+    run.one_pass(counters)
+    counters.synchronized_merges += int(run.st.merges.item())
+    return Centroids(run.master[run.cur ^ 1].clone(), check_finite=False), run.store, counters
+
+
+def chunked_stream_run(stream: HostStream, cfg: KMeansConfig, assign_path: str | None = None,
+                       workers: int | None = None, counters: Counters | None = None,
+                       device=None) -> KMeansResult:
+    """Full out-of-core run (pipeline.py:482-530) with the in-core run's decisions."""
+    counters = counters if counters is not None else Counters()
+    if cfg.clusters > stream.total_points:
+        raise ValueError("more clusters than points in the stream")
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    tiling = _resolve_tiling(cfg, stream.total_points, stream.dims, stream.batch, stream.elem_bytes,
+                             _workers(workers))
+    run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk)
+    run.set(_init_from_stream(stream, cfg.clusters, cfg.seed, cfg.init))
+    history = []
+    iterations = 0
+    for it in range(1, cfg.max_iters + 1):
+        iterations = it
+        changed, shift = run.one_pass(counters)
+        history.append(run.st.obj.cpu().numpy().copy())
+        if not changed:
+            break
+        run.cur ^= 1
+        if shift <= cfg.shift_tol:
+            break
+    counters.synchronized_merges += int(run.st.merges.item())
+    return KMeansResult(Centroids(run.master[run.cur].clone(), check_finite=False),
+                        run.store.read_all(), np.array(history), iterations, counters)

@@ -1,0 +1,70 @@
+"""World-size-2 gloo test of the point-sharded Lloyd path (CPU).
+
+Each rank owns a contiguous row range; the per-iteration exchange is the
+packed float64 all-reduce of LloydEngine.  With float32 data every partial
+sum is exact in float64, so the sharded run must reproduce the single-process
+oracle's lloyd_run bit for bit (assignments, centroids, iteration count).
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _worker(rank, world, port, result_q, prec):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle_backend
+        from oracle import oracle as O
+        from paper_2603_09229_b200 import KMeansConfig
+        from paper_2603_09229_b200.distributed import lloyd_run_sharded, shard_bounds
+
+        dt = np.float32 if prec == "single" else np.float64
+        x = O.generate_dataset(2, 901, 6, 5, 1.3, 17, dt)
+        lo, hi = shard_bounds(x.shape[1], world, rank)
+        cfg = KMeansConfig(6, max_iters=25, seed=3, precision=prec)
+        r = lloyd_run_sharded(torch.from_numpy(np.ascontiguousarray(x[:, lo:hi])), x.shape[1], lo,
+                              cfg, update_chunk=x.shape[1], backend=oracle_backend)
+        result_q.put((rank, lo, hi, r.centroids.data.numpy(), r.assignments.values.numpy(),
+                      r.objective_history, r.iterations_run))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("prec", ["single", "double"])
+def test_sharded_lloyd_matches_single_process(oracle, prec):
+    world = 2
+    port = 29500 + (os.getpid() % 2000)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, prec)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    dt = np.float32 if prec == "single" else np.float64
+    x = oracle.generate_dataset(2, 901, 6, 5, 1.3, 17, dt)
+    c_ref, a_ref, h_ref, it_ref, _ = oracle.lloyd_run(x, 6, max_iters=25, seed=3)
+    a = np.concatenate([r[4] for r in res], axis=1)
+    assert res[0][6] == res[1][6] == it_ref
+    assert np.array_equal(a, a_ref)
+    np.testing.assert_allclose(res[0][5], h_ref, rtol=1e-12)
+    for r in res:
+        if prec == "single":
+            assert np.array_equal(r[3], c_ref)
+        else:
+            np.testing.assert_allclose(r[3], c_ref, rtol=1e-12)
+    assert np.array_equal(res[0][3], res[1][3])  # replicas never diverge
