@@ -75,7 +75,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -245,6 +245,7 @@ def run_ours(args):
     timers = [[ev() for _ in range(4)] for _ in range(args.steps)]
     t0, t1 = ev(), ev()
     with ClockSampler(local) as clk:
+        time.sleep(0.6)  # let the sampler start before the timed region
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -386,12 +387,14 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-sample", type=int, default=65536)
+    ap.add_argument("--cpu-sample", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-chunk", type=int, default=1 << 21)
     args = ap.parse_args()
+    if args.cpu_sample is None:  # ~8 s of host work for cpu_baseline, ~2 s per reference step
+        args.cpu_sample = 131072 if args.impl == "reference" else 524288
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":
