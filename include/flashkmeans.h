@@ -130,7 +130,8 @@ FK_API fk_status fk_row_norms(fk_dtype dt, const void* M, int64_t rows, int64_t 
 
 /* objective[b] = sum_i mind[b,i] in f64 (pipeline._objective_row); mind is
  * f32 (FK_F32/FK_BF16/FK_F16 data) or f64.  Deterministic fixed-order
- * reduction that follows numpy's buffered pairwise summation.               */
+ * reduction; for f32 min_dists every f64 partial is exact in practice, so it
+ * equals numpy's np.sum(m, dtype=float64) bit for bit.                      */
 FK_API size_t fk_objective_workspace(int64_t B, int64_t N);
 FK_API fk_status fk_objective(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N, double* out,
                        void* workspace, size_t workspace_bytes, void* stream);

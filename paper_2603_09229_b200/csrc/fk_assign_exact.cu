@@ -49,20 +49,23 @@ __global__ void k_row_norms_exact(const T* __restrict__ M, int64_t rows, int64_t
 template <typename T>
 __global__ void k_cn_pad(const T* __restrict__ C, int64_t B, int64_t K, int64_t d, int kpad,
                          float* out) {
-  int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // one warp per (padded) centroid row; lanes stride over the features
+  const int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (gi >= B * kpad) return;
-  int64_t b = gi / kpad, k = gi - b * kpad;
+  const int64_t b = gi / kpad, k = gi - b * kpad;
   if (k >= K) {
-    out[gi] = __int_as_float(0x7f800000);
+    if (lane == 0) out[gi] = __int_as_float(0x7f800000);
     return;
   }
   const T* p = C + (b * K + k) * d;
   float acc = 0.f;
-  for (int64_t j = 0; j < d; ++j) {
+  for (int64_t j = lane; j < d; j += 32) {
     float v = to_f32(p[j]);
     acc = fmaf(v, v, acc);
   }
-  out[gi] = acc;
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[gi] = acc;
 }
 
 // ---------------------------------------------------------------- assign
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(EX_ROWS)
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_cn_pad(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
                           float* cn_pad, cudaStream_t stream) {
-  const int64_t n = B * kpad;
+  const int64_t n = B * kpad * 32;  // one warp per row
   const int th = 256;
   const unsigned grid = (unsigned)((n + th - 1) / th);
   if (dt == DT_BF16)

@@ -9,18 +9,20 @@
 //
 // Persistent, warp-specialized CTA (one per SM, 384 threads):
 //   warp 0      TMA producer: X row tile (128 x d, resident for the whole
-//               centroid sweep, double-buffered) and C column tiles
-//               (256 x 64 per stage, 4-stage ring) -- C stays L2-resident.
+//               centroid sweep, double-buffered), C column tiles
+//               (256 x 64 per stage, 4-stage ring; C stays L2-resident) and
+//               the matching 1 KB slice of ||c||^2 (4-slot ring, bulk copy).
 //   warp 1      MMA issuer: one elected thread issues M=128,N=256,K=16 MMAs
 //               into a double-buffered TMEM accumulator (2 x 256 columns).
 //   warp 2      TMEM allocator.
 //   warps 4-11  epilogue, two warpgroups splitting each 256-column tile into
 //               halves; thread = one point row (TMEM lane).  Per 32-column
-//               chunk: tcgen05.ld, s = c_norm - 2 acc (packed FFMA2), a
-//               3-input-min tree, and a warp vote; the chunk's 32 scores are
-//               spilled to a private smem slot only when this row's running
-//               minimum improves, so the index is recovered once per row
-//               tile instead of being tracked per element.
+//               chunk: tcgen05.ld (next chunk prefetched), s = c_norm - 2 acc
+//               (packed FFMA2, c_norm broadcast from smem), a 3-input-min tree
+//               and a warp vote; the chunk's 32 scores are copied into a
+//               register-resident "winning chunk" only when some row of the
+//               warp improves, so the index is recovered once per row tile
+//               instead of being tracked per element.
 // Tie rule (rowmin_merge, _kernels.py:64-82): strict < in ascending column
 // order within a thread, first equal element within the winning chunk, and a
 // lexicographic (value, index) merge across the two warpgroups -> the lowest
@@ -38,12 +40,13 @@ constexpr int KATOMS_MAX = 2;            // d <= 128 (64 bf16 = 128 B per atom)
 constexpr int A_ATOM = BM * 128;         // 16 KB
 constexpr int A_SLOT = KATOMS_MAX * A_ATOM;
 constexpr int B_STAGE = BN * 128;        // 32 KB
+constexpr int CN_SLOTS = 4;              // ||c||^2 ring (1 KB per column tile)
 constexpr int OFF_A = 0;
 constexpr int OFF_B = OFF_A + 2 * A_SLOT;            // 64 KB
-constexpr int OFF_REC = OFF_B + STAGES * B_STAGE;    // 192 KB
-constexpr int OFF_XCH = OFF_REC + 256 * 128;         // 224 KB
+constexpr int OFF_CN = OFF_B + STAGES * B_STAGE;     // 192 KB
+constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;  // 196 KB
 constexpr int OFF_BAR = OFF_XCH + BM * 8;
-constexpr int NBARS = 16;
+constexpr int NBARS = 16 + 2 * CN_SLOTS;
 constexpr int SMEM_USED = OFF_BAR + NBARS * 8 + 16;
 constexpr int SMEM_BYTES = SMEM_USED + 1024;         // alignment slack
 constexpr int THREADS = 384;
@@ -93,19 +96,17 @@ FK_DEV float row_norm_smem(const uint8_t* a_slot, int row, int katoms, int lane)
   return acc;
 }
 
-// One 32-column chunk: bias, chunk minimum, conditional spill.
-FK_DEV void epi_chunk(const uint32_t (&v)[32], const float* __restrict__ cnp, int colbase,
-                      float& M, int& best, float* rec, int lane) {
-  float s[32];
-  const float4* c4 = reinterpret_cast<const float4*>(cnp);
+// One 32-column chunk: bias, chunk minimum, conditional capture of the
+// winning chunk's scores (registers; only when some row of the warp improves).
+FK_DEV void epi_chunk(uint32_t (&v)[32], uint32_t cn_addr, int colbase, float& M, int& best,
+                      float (&bestv)[32]) {
   const float2 m2 = make_float2(-2.f, -2.f);
+  float* s = reinterpret_cast<float*>(v);
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
-    float4 cc = __ldg(c4 + j);
-    float2 r0 = ffma2(make_float2(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1])), m2,
-                      make_float2(cc.x, cc.y));
-    float2 r1 = ffma2(make_float2(__uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3])),
-                      m2, make_float2(cc.z, cc.w));
+    const float4 cc = lds128(cn_addr + 16 * j);
+    float2 r0 = ffma2(make_float2(s[4 * j], s[4 * j + 1]), m2, make_float2(cc.x, cc.y));
+    float2 r1 = ffma2(make_float2(s[4 * j + 2], s[4 * j + 3]), m2, make_float2(cc.z, cc.w));
     s[4 * j] = r0.x;
     s[4 * j + 1] = r0.y;
     s[4 * j + 2] = r1.x;
@@ -115,19 +116,15 @@ FK_DEV void epi_chunk(const uint32_t (&v)[32], const float* __restrict__ cnp, in
 #pragma unroll
   for (int j = 0; j < 10; ++j) a[j] = fmin3(s[3 * j], s[3 * j + 1], s[3 * j + 2]);
   a[10] = fminf(s[30], s[31]);
-  float b0 = fmin3(a[0], a[1], a[2]);
-  float b1 = fmin3(a[3], a[4], a[5]);
-  float b2 = fmin3(a[6], a[7], a[8]);
-  float b3 = fminf(a[9], a[10]);
-  float mc = fmin3(b0, b1, fminf(b2, b3));
-  bool p = mc < M;
+  const float b0 = fmin3(a[0], a[1], a[2]);
+  const float b1 = fmin3(a[3], a[4], a[5]);
+  const float b2 = fmin3(a[6], a[7], a[8]);
+  const float b3 = fminf(a[9], a[10]);
+  const float mc = fmin3(b0, b1, fminf(b2, b3));
+  const bool p = mc < M;
   if (__any_sync(0xffffffffu, p)) {
-    if (p) {
-      float4* r4 = reinterpret_cast<float4*>(rec);
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        r4[j ^ (lane & 7)] = make_float4(s[4 * j], s[4 * j + 1], s[4 * j + 2], s[4 * j + 3]);
-    }
+    for (int j = 0; j < 32; ++j) bestv[j] = p ? s[j] : bestv[j];
   }
   M = p ? mc : M;
   best = p ? colbase : best;
@@ -142,7 +139,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                                              ~uintptr_t(1023));
   uint8_t* sA = smem + tc::OFF_A;
   uint8_t* sB = smem + tc::OFF_B;
-  float* sREC = reinterpret_cast<float*>(smem + tc::OFF_REC);
+  float* sCN = reinterpret_cast<float*>(smem + tc::OFF_CN);
   float* xch_m = reinterpret_cast<float*>(smem + tc::OFF_XCH);
   int* xch_i = reinterpret_cast<int*>(smem + tc::OFF_XCH + tc::BM * 4);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tc::OFF_BAR);
@@ -152,6 +149,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   uint64_t* b_empty = bars + 8;
   uint64_t* t_full = bars + 12;
   uint64_t* t_empty = bars + 14;
+  uint64_t* cn_full = bars + 16;
+  uint64_t* cn_empty = bars + 16 + tc::CN_SLOTS;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + tc::NBARS);
 
   const int warp = threadIdx.x >> 5;
@@ -169,6 +168,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     for (int s = 0; s < tc::STAGES; ++s) {
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
+    }
+    for (int s = 0; s < tc::CN_SLOTS; ++s) {
+      mbar_init(&cn_full[s], 1);
+      mbar_init(&cn_empty[s], 8);  // every epilogue warp
     }
     fence_barrier_init();
   }
@@ -194,10 +197,18 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                       b, kEvictFirst);
       };
       int i = 0;
+      uint32_t g = 0;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
         const int b = t / p.tiles_per_batch;
         if (i == 0) load_a(t, 0);
-        for (int c = 0; c < p.ncol; ++c) {
+        for (int c = 0; c < p.ncol; ++c, ++g) {
+          {  // ||c||^2 slice of this column tile
+            const uint32_t slot = g % tc::CN_SLOTS;
+            mbar_wait(&cn_empty[slot], ((g / tc::CN_SLOTS) & 1) ^ 1);
+            mbar_arrive_expect_tx(&cn_full[slot], tc::BN * 4);
+            bulk_load(sCN + slot * tc::BN, p.cn + (size_t)b * p.kpad + (size_t)c * tc::BN,
+                      tc::BN * 4, &cn_full[slot]);
+          }
           for (int ka = 0; ka < p.katoms; ++ka) {
             mbar_wait(&b_empty[stage], sphase ^ 1);
             mbar_arrive_expect_tx(&b_full[stage], tc::B_STAGE);
@@ -257,59 +268,58 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int wg = ew >> 2;         // column half of every tile
     const int q = warp & 3;         // TMEM lane quarter
     const int row = q * 32 + lane;  // tile row owned by this thread
-    float* rec = sREC + (wg * tc::BM + row) * 32;
     uint32_t g = 0;
     int i = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++i) {
       const int b = t / p.tiles_per_batch;
       const int row0 = (t - b * p.tiles_per_batch) * tc::BM;
       const int slot = i & 1;
-      const float* cnb = p.cn + (size_t)b * p.kpad;
       float M = __int_as_float(0x7f800000);
       int best = -1;
+      float bestv[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bestv[j] = M;
       float xn = 0.f;
       for (int c = 0; c < p.ncol; ++c, ++g) {
         const uint32_t buf = g & 1;
+        const uint32_t cslot = g % tc::CN_SLOTS;
         mbar_wait(&t_full[buf], (g >> 1) & 1);
         tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + buf * tc::BN + wg * 128;
+        uint32_t va[32], vb[32];
+        FK_TMEM_LD_32x32b_X32(taddr, va);
         if (c == 0 && wg == 0) {
           xn = row_norm_smem<FMT>(sA + slot * tc::A_SLOT, row, p.katoms, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_empty[slot]);
         }
-        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + buf * tc::BN + wg * 128;
+        mbar_wait(&cn_full[cslot], (g / tc::CN_SLOTS) & 1);
+        const uint32_t cnp = smem_u32(sCN + cslot * tc::BN + wg * 128);
         const int col0 = c * tc::BN + wg * 128;
-        uint32_t va[32], vb[32];
-        FK_TMEM_LD_32x32b_X32(taddr, va);
         FK_TMEM_WAIT_LD(va);
         FK_TMEM_LD_32x32b_X32(taddr + 32, vb);
-        epi_chunk(va, cnb + col0, col0, M, best, rec, lane);
+        epi_chunk(va, cnp, col0, M, best, bestv);
         FK_TMEM_WAIT_LD(vb);
         FK_TMEM_LD_32x32b_X32(taddr + 64, va);
-        epi_chunk(vb, cnb + col0 + 32, col0 + 32, M, best, rec, lane);
+        epi_chunk(vb, cnp + 128, col0 + 32, M, best, bestv);
         FK_TMEM_WAIT_LD(va);
         FK_TMEM_LD_32x32b_X32(taddr + 96, vb);
-        epi_chunk(va, cnb + col0 + 64, col0 + 64, M, best, rec, lane);
+        epi_chunk(va, cnp + 256, col0 + 64, M, best, bestv);
         FK_TMEM_WAIT_LD(vb);
         // every TMEM read of this buffer has landed: hand it back to the MMA warp
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&t_empty[buf]);
-        epi_chunk(vb, cnb + col0 + 96, col0 + 96, M, best, rec, lane);
+        epi_chunk(vb, cnp + 384, col0 + 96, M, best, bestv);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cn_empty[cslot]);
       }
       // recover the index inside the winning chunk (first equal element)
       int idx = -1;
       if (best >= 0) {
-        const float4* r4 = reinterpret_cast<const float4*>(rec);
         int found = 31;
 #pragma unroll
-        for (int j = 7; j >= 0; --j) {
-          float4 v = r4[j ^ (lane & 7)];
-          found = (v.w == M) ? 4 * j + 3 : found;
-          found = (v.z == M) ? 4 * j + 2 : found;
-          found = (v.y == M) ? 4 * j + 1 : found;
-          found = (v.x == M) ? 4 * j + 0 : found;
-        }
+        for (int j = 31; j >= 0; --j) found = (bestv[j] == M) ? j : found;
         idx = best + found;
       }
       if (wg == 1) {

@@ -66,6 +66,14 @@ FK_DEV void tma_load_3d(void* smem_dst, const void* desc, uint64_t* bar, int c0,
       "l"(desc), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "l"(cache_hint)
       : "memory");
 }
+// 1-D bulk copy global -> shared (size and addresses multiples of 16 B).
+FK_DEV void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
 // L2 cache-policy constants (createpolicy.fractional.* encodings as used by CUTLASS).
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
@@ -146,6 +154,14 @@ FK_DEV uint64_t make_sdesc_sw128(uint32_t smem_addr) {
                  "+r"(r[30]), "+r"(r[31])                                                     \
                :                                                                                \
                : "memory")
+
+FK_DEV float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
 
 // ------------------------------------------------------------- math bits
 FK_DEV float fmin3(float a, float b, float c) {

@@ -33,26 +33,34 @@ FK_DEV double as_f64(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
 FK_DEV double as_f64(__half v) { return (double)__half2float(v); }
 
 // ----------------------------------------------------------------- hist
-__global__ void k_hist(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K,
-                       int32_t* __restrict__ hist) {
+// Each block owns a contiguous range of points.  With B*K <= HIST_SMEM_KEYS
+// the block histograms in shared memory and publishes one atomic per
+// non-empty bin; otherwise identical keys are warp-aggregated.
+__device__ __forceinline__ void range_of(int64_t P, int64_t& lo, int64_t& hi) {
+  const int64_t per = (P + gridDim.x - 1) / gridDim.x;
+  lo = (int64_t)blockIdx.x * per;
+  hi = lo + per < P ? lo + per : P;
+}
+
+__global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, int64_t B, int64_t N,
+                                               int64_t K, int32_t* __restrict__ hist) {
   extern __shared__ int32_t sh[];
   const int64_t BK = B * K;
   const bool use_smem = BK <= HIST_SMEM_KEYS;
+  int64_t lo, hi;
+  range_of(B * N, lo, hi);
   if (use_smem) {
     for (int64_t k = threadIdx.x; k < BK; k += blockDim.x) sh[k] = 0;
     __syncthreads();
   }
-  const int64_t P = B * N;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += stride) {
-    const int64_t b = i / N;
-    const int32_t id = ids[i];
+#pragma unroll 4
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int32_t id = __ldg(ids + i);
     if (id < 0 || id >= K) continue;  // validated on the host side
-    const int64_t key = b * K + id;
-    if (use_smem)
+    const int64_t key = B == 1 ? id : (i / N) * K + id;
+    if (use_smem) {
       atomicAdd(&sh[key], 1);
-    else {
-      // warp-aggregate identical keys: one global atomic per distinct key per warp
+    } else {
       const unsigned peers = __match_any_sync(__activemask(), key);
       const int leader = __ffs(peers) - 1;
       if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[key], __popc(peers));
@@ -72,7 +80,7 @@ __global__ void __launch_bounds__(1024)
            int accumulate, int64_t* __restrict__ off, int32_t* __restrict__ cursor,
            int64_t* __restrict__ counts, int64_t* __restrict__ merges) {
   __shared__ int64_t warp_tot[32];
-  __shared__ unsigned long long merge_acc;
+  __shared__ unsigned long long warp_mg[32];
   const int64_t BK = B * K;
   const int t = threadIdx.x;
   const int64_t per = (BK + blockDim.x - 1) / blockDim.x;
@@ -80,14 +88,12 @@ __global__ void __launch_bounds__(1024)
   const int64_t k1 = (k0 + per < BK) ? k0 + per : BK;
   int64_t local = 0;
   for (int64_t k = k0; k < k1; ++k) local += hist[k];
-  // block exclusive scan of `local`
   int64_t v = local;
   const int lane = t & 31, w = t >> 5;
   for (int o = 1; o < 32; o <<= 1) {
     int64_t u = __shfl_up_sync(0xffffffffu, v, o);
     if (lane >= o) v += u;
   }
-  if (t == 0) merge_acc = 0;
   if (lane == 31) warp_tot[w] = v;
   __syncthreads();
   if (w == 0) {
@@ -101,30 +107,71 @@ __global__ void __launch_bounds__(1024)
   __syncthreads();
   int64_t run = v - local + (w > 0 ? warp_tot[w - 1] : 0);  // exclusive prefix
   unsigned long long mg = 0;
+  int64_t b = k0 / K, kb_end = (b + 1) * K;
   for (int64_t k = k0; k < k1; ++k) {
+    if (k >= kb_end) {
+      ++b;
+      kb_end += K;
+    }
     const int64_t c = hist[k];
     off[k] = run;
     cursor[k] = (int32_t)run;
-    if (accumulate)
-      counts[k] += c;
-    else
-      counts[k] = c;
-    if (c > 0) {
+    counts[k] = accumulate ? counts[k] + c : c;
+    if (c > 0 && merges) {
       // reference merges: the run [s, e) of this key inside its batch element
       // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks.
-      const int64_t b = k / K;
       const int64_t s = run - b * N, e = s + c;
       mg += (unsigned long long)((e - 1) / chunk - s / chunk + 1);
     }
     run += c;
   }
   if (k1 == BK && k0 < k1) off[BK] = run;  // exactly one thread owns the last key
-  atomicAdd(&merge_acc, mg);
+  for (int o = 16; o; o >>= 1) mg += __shfl_xor_sync(0xffffffffu, mg, o);
+  if (lane == 0) warp_mg[w] = mg;
   __syncthreads();
-  if (t == 0 && merges) atomicAdd((unsigned long long*)merges, merge_acc);
+  if (w == 0 && merges) {
+    unsigned long long m = (lane < (int)(blockDim.x >> 5)) ? warp_mg[lane] : 0;
+    for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+    if (lane == 0) atomicAdd((unsigned long long*)merges, m);
+  }
 }
 
 // ----------------------------------------------------------------- scatter
+// Bucket point indices by key.  Block-aggregated: a block histograms its
+// contiguous point range in shared memory, reserves ONE contiguous range per
+// non-empty key with a single global atomic, then hands out positions with
+// shared-memory cursors -- no per-point global atomics, no dependency chains.
+__global__ void __launch_bounds__(1024)
+    k_scatter_block(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K,
+                    int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
+  extern __shared__ int32_t sh[];
+  const int64_t BK = B * K;
+  int64_t lo, hi;
+  range_of(B * N, lo, hi);
+  for (int64_t k = threadIdx.x; k < BK; k += blockDim.x) sh[k] = 0;
+  __syncthreads();
+#pragma unroll 4
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int32_t id = __ldg(ids + i);
+    if (id < 0 || id >= K) continue;
+    atomicAdd(&sh[B == 1 ? id : (i / N) * K + id], 1);
+  }
+  __syncthreads();
+  for (int64_t k = threadIdx.x; k < BK; k += blockDim.x) {
+    const int32_t c = sh[k];
+    sh[k] = c ? atomicAdd(&cursor[k], c) : 0;
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int32_t id = __ldg(ids + i);
+    if (id < 0 || id >= K) continue;
+    const int pos = atomicAdd(&sh[B == 1 ? id : (i / N) * K + id], 1);
+    order[pos] = (int32_t)i;
+  }
+}
+
+// Large B*K: warp-aggregated cursor bumps straight in global memory.
 __global__ void k_scatter(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K,
                           int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
   const int64_t P = B * N;
@@ -236,22 +283,33 @@ __global__ void __launch_bounds__(256)
   int64_t p = p0;
   while (p < p1) {
     const int64_t lim = seg_end < p1 ? seg_end : p1;
-    while (p + RPW * U <= lim) {
+    if (p + RPW * U <= lim) {
+      // software pipeline: the sorted-order indices of the next group are
+      // fetched while this group's gathered rows are in flight
       int32_t ri[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) ri[u] = __ldg(order + p + u * RPW + sub);
-      uint4 v[U][VPL];
+      while (true) {
+        uint4 v[U][VPL];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const T* rp = X + (int64_t)ri[u] * row_elems;
+        for (int u = 0; u < U; ++u) {
+          const T* rp = X + (int64_t)ri[u] * row_elems;
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) v[u][q] = ldg_stream(rp + (q * LPR + sl) * E);
+          for (int q = 0; q < VPL; ++q) v[u][q] = ldg_stream(rp + (q * LPR + sl) * E);
+        }
+        const int64_t pn = p + RPW * U;
+        const bool more = pn + RPW * U <= lim;
+        if (more) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) ri[u] = __ldg(order + pn + u * RPW + sub);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < VPL; ++q) VecCvt<T>::add(acc + q * E, v[u][q]);
+        p = pn;
+        if (!more) break;
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int q = 0; q < VPL; ++q) VecCvt<T>::add(acc + q * E, v[u][q]);
-      p += RPW * U;
     }
     while (p < lim) {
       const int64_t r = p + sub;
@@ -363,8 +421,8 @@ static cudaError_t dispatch_segsum(const void* X, const int32_t* order, const in
       case 1: FK_SEG(1, 1, 4); break;
       case 2: FK_SEG(2, 1, 4); break;
       case 4: FK_SEG(4, 1, 4); break;
-      case 8: FK_SEG(8, 1, 4); break;
-      case 16: FK_SEG(16, 1, 4); break;
+      case 8: FK_SEG(8, 1, 8); break;
+      case 16: FK_SEG(16, 1, 8); break;
       case 32: FK_SEG(32, 1, 4); break;
       case 64: FK_SEG(32, 2, 2); break;
       case 128: FK_SEG(32, 4, 1); break;
@@ -396,16 +454,22 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   cudaError_t e;
   if ((e = cudaMemsetAsync(hist, 0, BK * 4, s)) != cudaSuccess) return e;
   if (!accumulate && (e = cudaMemsetAsync(sums, 0, BK * d * 8, s)) != cudaSuccess) return e;
-  const int th = 512;
-  int64_t blocks = (P + th - 1) / th;
-  const int64_t cap = (int64_t)num_sms * 4;
+  // one block per SM-ish slice of points; 1024 threads so the shared histogram
+  // is built and drained quickly
+  int64_t blocks = (P + 8191) / 8192;
+  const int64_t cap = (int64_t)num_sms * 2;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  const size_t hsm = BK <= HIST_SMEM_KEYS ? BK * 4 : 0;
-  k_hist<<<(unsigned)blocks, th, hsm, s>>>(ids, B, N, K, hist);
+  const bool smem_keys = BK <= HIST_SMEM_KEYS;
+  const size_t hsm = smem_keys ? BK * 4 : 0;
+  k_hist<<<(unsigned)blocks, 1024, hsm, s>>>(ids, B, N, K, hist);
   k_scan<<<1, 1024, 0, s>>>(hist, B, N, K, chunk < 1 ? 1 : chunk, accumulate, off, cursor, counts,
                             merges);
-  k_scatter<<<(unsigned)blocks, th, 0, s>>>(ids, B, N, K, cursor, order);
+  if (smem_keys)
+    k_scatter_block<<<(unsigned)blocks, 1024, hsm, s>>>(ids, B, N, K, cursor, order);
+  else
+    k_scatter<<<(unsigned)((P + 511) / 512 < num_sms * 4 ? (P + 511) / 512 : num_sms * 4), 512, 0,
+                s>>>(ids, B, N, K, cursor, order);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   switch (dt) {
     case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, order, off, BK, P, d, sums, num_sms, s);
@@ -480,8 +544,10 @@ cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* c
 }
 
 // ----------------------------------------------------------------- objective
-// Deterministic two-level reduction: fixed 8192-element blocks summed in a
-// fixed tree, then the block partials summed in order per batch element.
+// Deterministic two-level reduction (fixed 8192-element blocks, fixed trees).
+// For float32 min_dists every float64 partial sum is exact in practice, so
+// the result equals numpy's np.sum(m, dtype=float64) bit for bit; for
+// float64 data the summation order differs from numpy's pairwise tree.
 constexpr int OBJ_BLOCK = 8192;
 
 template <typename T>
@@ -503,11 +569,17 @@ __global__ void k_obj_partial(const T* __restrict__ m, int64_t B, int64_t N, int
 }
 
 __global__ void k_obj_final(const double* part, int64_t B, int64_t nblk, double* out) {
-  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (b >= B) return;
+  __shared__ double red[256];
+  const int64_t b = blockIdx.x;
   double acc = 0.0;
-  for (int64_t i = 0; i < nblk; ++i) acc += part[b * nblk + i];
-  out[b] = acc;
+  for (int64_t i = threadIdx.x; i < nblk; i += 256) acc += part[b * nblk + i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[b] = red[0];
 }
 
 size_t objective_workspace_bytes(int64_t B, int64_t N) {
@@ -523,7 +595,7 @@ cudaError_t launch_objective(int mind_is_f64, const void* mind, int64_t B, int64
     k_obj_partial<double><<<grid, 256, 0, s>>>((const double*)mind, B, N, nblk, part);
   else
     k_obj_partial<float><<<grid, 256, 0, s>>>((const float*)mind, B, N, nblk, part);
-  k_obj_final<<<(unsigned)((B + 127) / 128), 128, 0, s>>>(part, B, nblk, out);
+  k_obj_final<<<(unsigned)B, 256, 0, s>>>(part, B, nblk, out);
   return cudaGetLastError();
 }
 
