@@ -29,6 +29,7 @@
 // centroid id among equal minima.
 #include "fk_common.cuh"
 #include "fk_kernels.h"
+#include <cstdlib>
 
 namespace fk {
 
@@ -65,6 +66,7 @@ struct TcArgs {
   float* mind_out;      // (B, N)
   const int32_t* idx_prev;
   int32_t* changed;
+  int debug_mode;  // 0 normal; 1 epilogue skips math (MMA/TMA bound); 2 MMA skipped (epilogue bound)
 };
 
 template <int FMT>
@@ -247,10 +249,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             tc_fence_after();
             const uint32_t aa = a_base + ka * tc::A_ATOM;
             const uint32_t bb = smem_u32(sB + stage * tc::B_STAGE);
+            if (p.debug_mode != 2) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc_mma_f16(d_tmem, make_sdesc_sw128(aa + k * 32), make_sdesc_sw128(bb + k * 32),
-                         idesc, (ka | k) != 0);
+              for (int k = 0; k < 4; ++k)
+                tc_mma_f16(d_tmem, make_sdesc_sw128(aa + k * 32), make_sdesc_sw128(bb + k * 32),
+                           idesc, (ka | k) != 0);
+            }
             tc_commit(&b_empty[stage]);
             if (++stage == tc::STAGES) {
               stage = 0;
@@ -296,6 +300,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         mbar_wait(&cn_full[cslot], (g / tc::CN_SLOTS) & 1);
         const uint32_t cnp = smem_u32(sCN + cslot * tc::BN + wg * 128);
         const int col0 = c * tc::BN + wg * 128;
+        if (p.debug_mode == 1) {
+          FK_TMEM_WAIT_LD(va);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&t_empty[buf]);
+            mbar_arrive(&cn_empty[cslot]);
+          }
+          M = fminf(M, __uint_as_float(va[0]));
+          continue;
+        }
         FK_TMEM_WAIT_LD(va);
         FK_TMEM_LD_32x32b_X32(taddr + 32, vb);
         epi_chunk(va, cnp, col0, M, best, bestv);
@@ -355,6 +370,283 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
   }
 }
 
+// ====================================================================
+// CTA-pair variant (cta_group::2): the two CTAs of a cluster own 128 rows
+// each and compute a 256 x 256 tile with one MMA stream issued by the leader
+// CTA.  Each CTA stages only HALF of every C tile (128 centroids), so the
+// L2 -> SM traffic and the shared-memory footprint of C halve; the per-SM
+// epilogue work is unchanged.
+// ====================================================================
+namespace tc2 {
+constexpr int BM = 128;                  // rows per CTA (TMEM lanes)
+constexpr int BN = 256;                  // centroids per pair tile
+constexpr int BNH = 128;                 // centroids staged per CTA
+constexpr int STAGES = 6;                // C ring depth (16 KB per CTA each)
+constexpr int A_ATOM = BM * 128;         // 16 KB
+constexpr int A_SLOT = 2 * A_ATOM;       // d <= 128
+constexpr int B_STAGE = BNH * 128;       // 16 KB
+constexpr int CN_SLOTS = 4;
+constexpr int OFF_A = 0;
+constexpr int OFF_B = OFF_A + 2 * A_SLOT;
+constexpr int OFF_CN = OFF_B + STAGES * B_STAGE;
+constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;
+constexpr int OFF_BAR = OFF_XCH + BM * 8;
+constexpr int NBARS = 8 + 2 * STAGES + 2 * CN_SLOTS;
+constexpr int SMEM_USED = OFF_BAR + NBARS * 8 + 16;
+constexpr int SMEM_BYTES = SMEM_USED + 1024;
+constexpr int THREADS = 384;
+static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB dynamic shared memory");
+}  // namespace tc2
+
+template <int FMT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
+    fk_assign_tc2_kernel(const __grid_constant__ CUtensorMap tmx,
+                         const __grid_constant__ CUtensorMap tmc, const TcArgs p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem + tc2::OFF_A;
+  uint8_t* sB = smem + tc2::OFF_B;
+  float* sCN = reinterpret_cast<float*>(smem + tc2::OFF_CN);
+  float* xch_m = reinterpret_cast<float*>(smem + tc2::OFF_XCH);
+  int* xch_i = reinterpret_cast<int*>(smem + tc2::OFF_XCH + tc2::BM * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tc2::OFF_BAR);
+  uint64_t* a_full = bars + 0;
+  uint64_t* a_empty = bars + 2;
+  uint64_t* t_full = bars + 4;
+  uint64_t* t_empty = bars + 6;
+  uint64_t* b_full = bars + 8;
+  uint64_t* b_empty = bars + 8 + tc2::STAGES;
+  uint64_t* cn_full = bars + 8 + 2 * tc2::STAGES;
+  uint64_t* cn_empty = cn_full + tc2::CN_SLOTS;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + tc2::NBARS);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1;
+  const int npairs = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmx);
+    tma_prefetch_desc(&tmc);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&a_full[s], 1);       // leader's expect_tx (both CTAs' bytes)
+      mbar_init(&a_empty[s], 1 + 4);  // pair-MMA commit + 4 warps of this CTA's WG0
+      mbar_init(&t_full[s], 1);
+      mbar_init(&t_empty[s], 16);     // every epilogue warp of both CTAs
+    }
+    for (int s = 0; s < tc2::STAGES; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_empty[s], 1);
+    }
+    for (int s = 0; s < tc2::CN_SLOTS; ++s) {
+      mbar_init(&cn_full[s], 1);
+      mbar_init(&cn_empty[s], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc_cg2<512>(tmem_holder);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer (both CTAs)
+    if (lane == 0) {
+      uint32_t stage = 0, sphase = 0;
+      const uint32_t a_bytes = p.katoms * tc2::A_ATOM;
+      auto load_a = [&](int t, int j) {
+        const int slot = j & 1;
+        const int b = t / p.tiles_per_batch;
+        const int row0 = (t - b * p.tiles_per_batch) * (2 * tc2::BM) + rank * tc2::BM;
+        mbar_wait(&a_empty[slot], ((j >> 1) & 1) ^ 1);
+        if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
+        const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
+        for (int ka = 0; ka < p.katoms; ++ka)
+          tma_load_3d_cg2(sA + slot * tc2::A_SLOT + ka * tc2::A_ATOM, &tmx, bar, ka * 64, row0, b,
+                          kEvictFirst);
+      };
+      int i = 0;
+      uint32_t g = 0;
+      for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
+        const int b = t / p.tiles_per_batch;
+        if (i == 0) load_a(t, 0);
+        for (int c = 0; c < p.ncol; ++c, ++g) {
+          {
+            const uint32_t slot = g % tc2::CN_SLOTS;
+            mbar_wait(&cn_empty[slot], ((g / tc2::CN_SLOTS) & 1) ^ 1);
+            mbar_arrive_expect_tx(&cn_full[slot], tc2::BN * 4);
+            bulk_load(sCN + slot * tc2::BN, p.cn + (size_t)b * p.kpad + (size_t)c * tc2::BN,
+                      tc2::BN * 4, &cn_full[slot]);
+          }
+          for (int ka = 0; ka < p.katoms; ++ka) {
+            mbar_wait(&b_empty[stage], sphase ^ 1);
+            if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * tc2::B_STAGE);
+            tma_load_3d_cg2(sB + stage * tc2::B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
+                            ka * 64, c * tc2::BN + rank * tc2::BNH, b, kEvictLast);
+            if (++stage == tc2::STAGES) {
+              stage = 0;
+              sphase ^= 1;
+            }
+          }
+          if (c == 0) {
+            const int t2 = t + npairs;
+            if (t2 < p.total_tiles) load_a(t2, i + 1);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ pair MMA (leader only)
+    if (lane == 0 && leader) {
+      const uint32_t idesc = make_idesc_f16(FMT, 2 * tc2::BM, tc2::BN);
+      uint32_t stage = 0, sphase = 0, g = 0;
+      int i = 0;
+      for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
+        const int slot = i & 1;
+        mbar_wait(&a_full[slot], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t a_base = smem_u32(sA + slot * tc2::A_SLOT);
+        for (int c = 0; c < p.ncol; ++c, ++g) {
+          const uint32_t buf = g & 1;
+          mbar_wait(&t_empty[buf], ((g >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d_tmem = tmem_base + buf * tc2::BN;
+          for (int ka = 0; ka < p.katoms; ++ka) {
+            mbar_wait(&b_full[stage], sphase);
+            tc_fence_after();
+            const uint32_t aa = a_base + ka * tc2::A_ATOM;
+            const uint32_t bb = smem_u32(sB + stage * tc2::B_STAGE);
+            if (p.debug_mode != 2) {
+#pragma unroll
+              for (int k = 0; k < 4; ++k)
+                tc_mma_f16_cg2(d_tmem, make_sdesc_sw128(aa + k * 32), make_sdesc_sw128(bb + k * 32),
+                               idesc, (ka | k) != 0);
+            }
+            tc_commit_cg2_mc(&b_empty[stage], 0x3);
+            if (++stage == tc2::STAGES) {
+              stage = 0;
+              sphase ^= 1;
+            }
+          }
+          tc_commit_cg2_mc(&t_full[buf], 0x3);
+        }
+        tc_commit_cg2_mc(&a_empty[slot], 0x3);
+      }
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue (both CTAs)
+    const int ew = warp - 4;
+    const int wg = ew >> 2;
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    uint32_t g = 0;
+    int i = 0;
+    for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
+      const int b = t / p.tiles_per_batch;
+      const int row0 = (t - b * p.tiles_per_batch) * (2 * tc2::BM) + rank * tc2::BM;
+      const int slot = i & 1;
+      float M = __int_as_float(0x7f800000);
+      int best = -1;
+      float bestv[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) bestv[j] = M;
+      float xn = 0.f;
+      for (int c = 0; c < p.ncol; ++c, ++g) {
+        const uint32_t buf = g & 1;
+        const uint32_t cslot = g % tc2::CN_SLOTS;
+        mbar_wait(&t_full[buf], (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + buf * tc2::BN + wg * 128;
+        uint32_t va[32], vb[32];
+        FK_TMEM_LD_32x32b_X32(taddr, va);
+        if (c == 0 && wg == 0) {
+          xn = row_norm_smem<FMT>(sA + slot * tc2::A_SLOT, row, p.katoms, lane);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&a_empty[slot]);
+        }
+        mbar_wait(&cn_full[cslot], (g / tc2::CN_SLOTS) & 1);
+        const uint32_t cnp = smem_u32(sCN + cslot * tc2::BN + wg * 128);
+        const int col0 = c * tc2::BN + wg * 128;
+        if (p.debug_mode == 1) {
+          FK_TMEM_WAIT_LD(va);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if (leader)
+              mbar_arrive(&t_empty[buf]);
+            else
+              mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[buf]), 0));
+            mbar_arrive(&cn_empty[cslot]);
+          }
+          M = fminf(M, __uint_as_float(va[0]));
+          continue;
+        }
+        FK_TMEM_WAIT_LD(va);
+        FK_TMEM_LD_32x32b_X32(taddr + 32, vb);
+        epi_chunk(va, cnp, col0, M, best, bestv);
+        FK_TMEM_WAIT_LD(vb);
+        FK_TMEM_LD_32x32b_X32(taddr + 64, va);
+        epi_chunk(vb, cnp + 128, col0 + 32, M, best, bestv);
+        FK_TMEM_WAIT_LD(va);
+        FK_TMEM_LD_32x32b_X32(taddr + 96, vb);
+        epi_chunk(va, cnp + 256, col0 + 64, M, best, bestv);
+        FK_TMEM_WAIT_LD(vb);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader)
+            mbar_arrive(&t_empty[buf]);
+          else
+            mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[buf]), 0));
+        }
+        epi_chunk(vb, cnp + 384, col0 + 96, M, best, bestv);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cn_empty[cslot]);
+      }
+      int idx = -1;
+      if (best >= 0) {
+        int found = 31;
+#pragma unroll
+        for (int j = 31; j >= 0; --j) found = (bestv[j] == M) ? j : found;
+        idx = best + found;
+      }
+      if (wg == 1) {
+        xch_m[row] = M;
+        xch_i[row] = idx;
+      }
+      named_bar_sync(1, 256);
+      if (wg == 0) {
+        const float M1 = xch_m[row];
+        const int i1 = xch_i[row];
+        if (M1 < M || (M1 == M && i1 >= 0 && (idx < 0 || i1 < idx))) {
+          M = M1;
+          idx = i1;
+        }
+        const int grow = row0 + row;
+        bool ch = false;
+        if (grow < p.N) {
+          const size_t o = (size_t)b * p.N + grow;
+          p.idx_out[o] = idx;
+          p.mind_out[o] = fmaxf(0.f, xn + M);
+          if (p.idx_prev) ch = p.idx_prev[o] != idx;
+        }
+        if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
+      }
+      named_bar_sync(2, 256);
+    }
+    tc_fence_before();
+  }
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_cg2<512>(tmem_base);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -391,9 +683,11 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
                              int64_t B, int64_t N, int64_t K, int64_t d, int32_t* idx_out,
                              float* mind_out, const int32_t* idx_prev, int32_t* changed,
                              int num_sms, cudaStream_t stream) {
-  CUtensorMap tmx, tmc;
+  CUtensorMap tmx, tmc, tmx2, tmc2;
   if (!make_map(&tmx, X, fmt, d, N, B, tc::BM)) return cudaErrorInvalidValue;
   if (!make_map(&tmc, C, fmt, d, K, B, tc::BN)) return cudaErrorInvalidValue;
+  if (!make_map(&tmx2, X, fmt, d, N, B, tc2::BM)) return cudaErrorInvalidValue;
+  if (!make_map(&tmc2, C, fmt, d, K, B, tc2::BNH)) return cudaErrorInvalidValue;
   TcArgs a;
   a.B = (int)B;
   a.N = (int)N;
@@ -409,23 +703,40 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
   a.mind_out = mind_out;
   a.idx_prev = idx_prev;
   a.changed = changed;
+  {
+    const char* dm = getenv("FK_ASSIGN_DEBUG_MODE");
+    a.debug_mode = dm ? atoi(dm) : 0;
+  }
+  const char* cta = getenv("FK_ASSIGN_CTA");
+  const bool pair = !(cta && atoi(cta) == 1);
+  if (pair) {
+    // pair tiles of 256 rows; one cluster of 2 CTAs per TPC
+    a.tiles_per_batch = (int)((N + 2 * tc2::BM - 1) / (2 * tc2::BM));
+    a.total_tiles = (int)(B * a.tiles_per_batch);
+    int pairs = num_sms / 2;
+    if (a.total_tiles < pairs) pairs = a.total_tiles;
+    if (pairs <= 0) return cudaSuccess;
+    const int grid = 2 * pairs;
+    if (fmt == 1) {
+      cudaFuncSetAttribute(fk_assign_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tc2::SMEM_BYTES);
+      fk_assign_tc2_kernel<1><<<grid, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(tmx2, tmc2, a);
+    } else {
+      cudaFuncSetAttribute(fk_assign_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           tc2::SMEM_BYTES);
+      fk_assign_tc2_kernel<0><<<grid, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(tmx2, tmc2, a);
+    }
+    return cudaGetLastError();
+  }
   const int grid = a.total_tiles < num_sms ? a.total_tiles : num_sms;
   if (grid <= 0) return cudaSuccess;
   if (fmt == 1) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(fk_assign_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           tc::SMEM_BYTES);
-      attr = true;
-    }
+    cudaFuncSetAttribute(fk_assign_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         tc::SMEM_BYTES);
     fk_assign_tc_kernel<1><<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(tmx, tmc, a);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(fk_assign_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           tc::SMEM_BYTES);
-      attr = true;
-    }
+    cudaFuncSetAttribute(fk_assign_tc_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         tc::SMEM_BYTES);
     fk_assign_tc_kernel<0><<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(tmx, tmc, a);
   }
   return cudaGetLastError();
