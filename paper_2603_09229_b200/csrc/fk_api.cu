@@ -92,7 +92,8 @@ int fk_device_supported(int device) {
 size_t fk_assign_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d) {
   (void)d;
   if (!valid_dt(dt) || B < 1 || N < 1 || K < 1) return 0;
-  if (is_lowp(dt)) return al256((size_t)B * fk::assign_tc_kpad(K) * 4);
+  if (is_lowp(dt))  // ||c||^2 (fp32) + the bias-in-GEMM operand (16 x 16-bit per centroid)
+    return al256((size_t)B * fk::assign_tc_kpad(K) * 4) + al256((size_t)B * fk::assign_tc_kpad(K) * 32);
   const size_t es = elem_size(dt);
   return al256((size_t)B * N * es) + al256((size_t)B * K * es);
 }
@@ -112,9 +113,17 @@ fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B, int64_
     float* cn = reinterpret_cast<float*>(ws);
     if (tc_path(dt, d, X, C)) {
       const int kpad = fk::assign_tc_kpad(K);
-      fk_status st = cuda_status(fk::launch_cn_pad(dt, C, B, K, d, kpad, cn, s));
+      const int fmt = dt == FK_BF16 ? 1 : 0;
+      void* ext = nullptr;
+      fk_status st;
+      if (fk::assign_tc_uses_ext(fmt)) {
+        ext = reinterpret_cast<uint8_t*>(ws) + al256((size_t)B * kpad * 4);
+        st = cuda_status(fk::launch_cn_ext(dt, C, B, K, d, kpad, ext, s));
+      } else {
+        st = cuda_status(fk::launch_cn_pad(dt, C, B, K, d, kpad, cn, s));
+      }
       if (st != FK_OK) return st;
-      return cuda_status(fk::launch_assign_tc(dt == FK_BF16 ? 1 : 0, X, C, cn, B, N, K, d, idx_out,
+      return cuda_status(fk::launch_assign_tc(fmt, X, C, cn, ext, B, N, K, d, idx_out,
                                               reinterpret_cast<float*>(mind_out), idx_prev,
                                               changed_flag, di.sms, s));
     }

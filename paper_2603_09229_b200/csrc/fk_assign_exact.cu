@@ -68,6 +68,45 @@ __global__ void k_cn_pad(const T* __restrict__ C, int64_t B, int64_t K, int64_t 
   if (lane == 0) out[gi] = acc;
 }
 
+// Bias operand for the bias-in-GEMM FlashAssign: ||c||^2 / 2 split into three
+// bf16 terms (24 significant bits) so that one extra K=16 MMA step against a
+// constant ones operand adds it to the accumulator exactly enough.
+__global__ void k_cn_ext_bf16(const __nv_bfloat16* __restrict__ C, int64_t B, int64_t K, int64_t d,
+                              int kpad, __nv_bfloat16* out) {
+  const int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gi >= B * kpad) return;
+  const int64_t b = gi / kpad, k = gi - b * kpad;
+  __nv_bfloat16* o = out + gi * 16;
+  if (k >= K) {
+    if (lane < 16) o[lane] = lane == 0 ? __float2bfloat16(__int_as_float(0x7f800000)) : __float2bfloat16(0.f);
+    return;
+  }
+  const __nv_bfloat16* p = C + (b * K + k) * d;
+  float acc = 0.f;
+  for (int64_t j = lane; j < d; j += 32) {
+    const float v = __bfloat162float(p[j]);
+    acc = fmaf(v, v, acc);
+  }
+  for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+  const float v = 0.5f * acc;
+  const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+  const float r1 = v - __bfloat162float(hi);
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+  if (lane < 16) o[lane] = lane == 0 ? hi : lane == 1 ? mid : lane == 2 ? lo : __float2bfloat16(0.f);
+}
+
+cudaError_t launch_cn_ext(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
+                          void* out, cudaStream_t stream) {
+  if (dt != DT_BF16) return cudaErrorInvalidValue;
+  const int64_t n = B * kpad * 32;
+  const int th = 256;
+  k_cn_ext_bf16<<<(unsigned)((n + th - 1) / th), th, 0, stream>>>(
+      (const __nv_bfloat16*)C, B, K, d, kpad, (__nv_bfloat16*)out);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------- assign
 constexpr int EX_ROWS = 128;  // points per block (one per thread)
 constexpr int EX_KT = 16;     // centroids per register tile

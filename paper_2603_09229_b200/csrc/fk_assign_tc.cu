@@ -381,45 +381,83 @@ namespace tc2 {
 constexpr int BM = 128;                  // rows per CTA (TMEM lanes)
 constexpr int BN = 256;                  // centroids per pair tile
 constexpr int BNH = 128;                 // centroids staged per CTA
-constexpr int STAGES = 6;                // C ring depth (16 KB per CTA each)
+constexpr int NBUF = 2;                  // TMEM accumulators (2 x 256 columns)
 constexpr int A_ATOM = BM * 128;         // 16 KB
 constexpr int A_SLOT = 2 * A_ATOM;       // d <= 128
-constexpr int B_STAGE = BNH * 128;       // 16 KB
-constexpr int CN_SLOTS = 4;
+constexpr int B_STAGE = BNH * 128;       // 16 KB per CTA
+constexpr int STAGES = 6;
+constexpr int CN_SLOTS = 6;              // ||c||^2 ring (bias in the epilogue)
+constexpr int EXT_ROW = 32;              // 16 bf16: [hi, mid, lo, 0...] of ||c||^2 / 2
+constexpr int EXT_SLOT = BNH * EXT_ROW;  // 4 KB per CTA per column tile
+constexpr int EXT_SLOTS = 4;             // bias-in-GEMM operand ring
 constexpr int OFF_A = 0;
 constexpr int OFF_B = OFF_A + 2 * A_SLOT;
-constexpr int OFF_CN = OFF_B + STAGES * B_STAGE;
+constexpr int OFF_AEXT = OFF_B + STAGES * B_STAGE;         // constant ones operand (4 KB)
+constexpr int OFF_EXT = OFF_AEXT + BM * EXT_ROW;
+constexpr int OFF_CN = OFF_EXT + EXT_SLOTS * EXT_SLOT;
 constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;
 constexpr int OFF_BAR = OFF_XCH + BM * 8;
-constexpr int NBARS = 8 + 2 * STAGES + 2 * CN_SLOTS;
+constexpr int NBARS = 4 + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
 constexpr int SMEM_USED = OFF_BAR + NBARS * 8 + 16;
 constexpr int SMEM_BYTES = SMEM_USED + 1024;
 constexpr int THREADS = 384;
 static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB dynamic shared memory");
 }  // namespace tc2
 
-template <int FMT>
+// Epilogue chunk when the bias is already in the accumulator (s = ||c||^2/2 - x.c).
+FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, float (&bestv)[32]) {
+  const float* s = reinterpret_cast<const float*>(v);
+  float a[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) a[j] = fmin3(s[3 * j], s[3 * j + 1], s[3 * j + 2]);
+  a[10] = fminf(s[30], s[31]);
+  const float b0 = fmin3(a[0], a[1], a[2]);
+  const float b1 = fmin3(a[3], a[4], a[5]);
+  const float b2 = fmin3(a[6], a[7], a[8]);
+  const float b3 = fminf(a[9], a[10]);
+  const float mc = fmin3(b0, b1, fminf(b2, b3));
+  const bool p = mc < M;
+  if (__any_sync(0xffffffffu, p)) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bestv[j] = p ? s[j] : bestv[j];
+  }
+  M = p ? mc : M;
+  best = p ? colbase : best;
+}
+
+// AUG = true : the ||c||^2 bias rides in the GEMM as one extra K=16 step
+//              (A_ext = ones, B_ext = 3-way bf16 split of ||c||^2/2, main
+//              MMAs negate A), so the epilogue is a pure min-reduction.
+// AUG = false: bias applied in the epilogue from a smem ring (fp16 data,
+//              whose range cannot hold ||c||^2 safely).
+template <int FMT, bool AUG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     fk_assign_tc2_kernel(const __grid_constant__ CUtensorMap tmx,
-                         const __grid_constant__ CUtensorMap tmc, const TcArgs p) {
+                         const __grid_constant__ CUtensorMap tmc,
+                         const __grid_constant__ CUtensorMap tmext, const TcArgs p) {
+  using namespace tc2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sA = smem + tc2::OFF_A;
-  uint8_t* sB = smem + tc2::OFF_B;
-  float* sCN = reinterpret_cast<float*>(smem + tc2::OFF_CN);
-  float* xch_m = reinterpret_cast<float*>(smem + tc2::OFF_XCH);
-  int* xch_i = reinterpret_cast<int*>(smem + tc2::OFF_XCH + tc2::BM * 4);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + tc2::OFF_BAR);
+  uint8_t* sA = smem + OFF_A;
+  uint8_t* sB = smem + OFF_B;
+  uint8_t* sAext = smem + OFF_AEXT;
+  uint8_t* sExt = smem + OFF_EXT;
+  float* sCN = reinterpret_cast<float*>(smem + OFF_CN);
+  float* xch_m = reinterpret_cast<float*>(smem + OFF_XCH);
+  int* xch_i = reinterpret_cast<int*>(smem + OFF_XCH + BM * 4);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* a_full = bars + 0;
   uint64_t* a_empty = bars + 2;
   uint64_t* t_full = bars + 4;
-  uint64_t* t_empty = bars + 6;
-  uint64_t* b_full = bars + 8;
-  uint64_t* b_empty = bars + 8 + tc2::STAGES;
-  uint64_t* cn_full = bars + 8 + 2 * tc2::STAGES;
-  uint64_t* cn_empty = cn_full + tc2::CN_SLOTS;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + tc2::NBARS);
+  uint64_t* t_empty = t_full + NBUF;
+  uint64_t* b_full = t_empty + NBUF;
+  uint64_t* b_empty = b_full + STAGES;
+  uint64_t* cn_full = b_empty + STAGES;
+  uint64_t* cn_empty = cn_full + CN_SLOTS;
+  uint64_t* ext_full = cn_empty + CN_SLOTS;
+  uint64_t* ext_empty = ext_full + EXT_SLOTS;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + NBARS);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -431,21 +469,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmc);
+    if (AUG) tma_prefetch_desc(&tmext);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&a_full[s], 1);       // leader's expect_tx (both CTAs' bytes)
       mbar_init(&a_empty[s], 1 + 4);  // pair-MMA commit + 4 warps of this CTA's WG0
+    }
+    for (int s = 0; s < NBUF; ++s) {
       mbar_init(&t_full[s], 1);
       mbar_init(&t_empty[s], 16);     // every epilogue warp of both CTAs
     }
-    for (int s = 0; s < tc2::STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(&b_full[s], 1);
       mbar_init(&b_empty[s], 1);
     }
-    for (int s = 0; s < tc2::CN_SLOTS; ++s) {
+    for (int s = 0; s < CN_SLOTS; ++s) {
       mbar_init(&cn_full[s], 1);
       mbar_init(&cn_empty[s], 8);
     }
+    for (int s = 0; s < EXT_SLOTS; ++s) {
+      mbar_init(&ext_full[s], 1);
+      mbar_init(&ext_empty[s], 1);
+    }
     fence_barrier_init();
+  }
+  if (AUG && warp == 3) {
+    // A_ext rows = [1,1,1,0,0,0,0,0] in BOTH 16-byte halves: invariant under
+    // the 32-byte swizzle, and only columns 0-2 of B_ext are non-zero.
+    const uint32_t one = FMT == 1 ? 0x3F80u : 0x3C00u;
+    const uint4 v = make_uint4(one | (one << 16), one, 0u, 0u);
+    uint4* dst = reinterpret_cast<uint4*>(sAext);
+    for (int i = lane; i < BM * 2; i += 32) dst[i] = v;
+    fence_proxy_async_smem();
   }
   if (warp == 2) tmem_alloc_cg2<512>(tmem_holder);
   tc_fence_before();
@@ -457,16 +511,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     // ------------------------------------------------------------ producer (both CTAs)
     if (lane == 0) {
       uint32_t stage = 0, sphase = 0;
-      const uint32_t a_bytes = p.katoms * tc2::A_ATOM;
+      const uint32_t a_bytes = p.katoms * A_ATOM;
       auto load_a = [&](int t, int j) {
         const int slot = j & 1;
         const int b = t / p.tiles_per_batch;
-        const int row0 = (t - b * p.tiles_per_batch) * (2 * tc2::BM) + rank * tc2::BM;
+        const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
         mbar_wait(&a_empty[slot], ((j >> 1) & 1) ^ 1);
         if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
         const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
         for (int ka = 0; ka < p.katoms; ++ka)
-          tma_load_3d_cg2(sA + slot * tc2::A_SLOT + ka * tc2::A_ATOM, &tmx, bar, ka * 64, row0, b,
+          tma_load_3d_cg2(sA + slot * A_SLOT + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
                           kEvictFirst);
       };
       int i = 0;
@@ -475,19 +529,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         const int b = t / p.tiles_per_batch;
         if (i == 0) load_a(t, 0);
         for (int c = 0; c < p.ncol; ++c, ++g) {
-          {
-            const uint32_t slot = g % tc2::CN_SLOTS;
-            mbar_wait(&cn_empty[slot], ((g / tc2::CN_SLOTS) & 1) ^ 1);
-            mbar_arrive_expect_tx(&cn_full[slot], tc2::BN * 4);
-            bulk_load(sCN + slot * tc2::BN, p.cn + (size_t)b * p.kpad + (size_t)c * tc2::BN,
-                      tc2::BN * 4, &cn_full[slot]);
+          if (AUG) {
+            const uint32_t slot = g % EXT_SLOTS;
+            mbar_wait(&ext_empty[slot], ((g / EXT_SLOTS) & 1) ^ 1);
+            if (leader) mbar_arrive_expect_tx(&ext_full[slot], 2 * EXT_SLOT);
+            tma_load_3d_cg2(sExt + slot * EXT_SLOT, &tmext, mapa_shared(smem_u32(&ext_full[slot]), 0),
+                            0, c * BN + rank * BNH, b, kEvictLast);
+          } else {
+            const uint32_t slot = g % CN_SLOTS;
+            mbar_wait(&cn_empty[slot], ((g / CN_SLOTS) & 1) ^ 1);
+            mbar_arrive_expect_tx(&cn_full[slot], BN * 4);
+            bulk_load(sCN + slot * BN, p.cn + (size_t)b * p.kpad + (size_t)c * BN, BN * 4,
+                      &cn_full[slot]);
           }
           for (int ka = 0; ka < p.katoms; ++ka) {
             mbar_wait(&b_empty[stage], sphase ^ 1);
-            if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * tc2::B_STAGE);
-            tma_load_3d_cg2(sB + stage * tc2::B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
-                            ka * 64, c * tc2::BN + rank * tc2::BNH, b, kEvictLast);
-            if (++stage == tc2::STAGES) {
+            if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * B_STAGE);
+            tma_load_3d_cg2(sB + stage * B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
+                            ka * 64, c * BN + rank * BNH, b, kEvictLast);
+            if (++stage == STAGES) {
               stage = 0;
               sphase ^= 1;
             }
@@ -502,35 +562,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   } else if (warp == 1) {
     // ------------------------------------------------------------ pair MMA (leader only)
     if (lane == 0 && leader) {
-      const uint32_t idesc = make_idesc_f16(FMT, 2 * tc2::BM, tc2::BN);
+      const uint32_t idesc = make_idesc_f16(FMT, 2 * BM, BN);
+      const uint32_t idesc_main = AUG ? (idesc | kIdescNegateA) : idesc;
+      const uint64_t aext_desc = make_sdesc_sw32(smem_u32(sAext));
       uint32_t stage = 0, sphase = 0, g = 0;
       int i = 0;
       for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
         const int slot = i & 1;
         mbar_wait(&a_full[slot], (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(sA + slot * tc2::A_SLOT);
+        const uint32_t a_base = smem_u32(sA + slot * A_SLOT);
         for (int c = 0; c < p.ncol; ++c, ++g) {
-          const uint32_t buf = g & 1;
-          mbar_wait(&t_empty[buf], ((g >> 1) & 1) ^ 1);
+          const uint32_t buf = g % NBUF;
+          mbar_wait(&t_empty[buf], ((g / NBUF) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t d_tmem = tmem_base + buf * tc2::BN;
+          const uint32_t d_tmem = tmem_base + buf * BN;
           for (int ka = 0; ka < p.katoms; ++ka) {
             mbar_wait(&b_full[stage], sphase);
             tc_fence_after();
-            const uint32_t aa = a_base + ka * tc2::A_ATOM;
-            const uint32_t bb = smem_u32(sB + stage * tc2::B_STAGE);
+            const uint32_t aa = a_base + ka * A_ATOM;
+            const uint32_t bb = smem_u32(sB + stage * B_STAGE);
             if (p.debug_mode != 2) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 tc_mma_f16_cg2(d_tmem, make_sdesc_sw128(aa + k * 32), make_sdesc_sw128(bb + k * 32),
-                               idesc, (ka | k) != 0);
+                               idesc_main, (ka | k) != 0);
             }
             tc_commit_cg2_mc(&b_empty[stage], 0x3);
-            if (++stage == tc2::STAGES) {
+            if (++stage == STAGES) {
               stage = 0;
               sphase ^= 1;
             }
+          }
+          if (AUG) {
+            const uint32_t es = g % EXT_SLOTS;
+            mbar_wait(&ext_full[es], (g / EXT_SLOTS) & 1);
+            tc_fence_after();
+            tc_mma_f16_cg2(d_tmem, aext_desc, make_sdesc_sw32(smem_u32(sExt + es * EXT_SLOT)), idesc,
+                           p.debug_mode != 2 ? 1u : 0u);
+            tc_commit_cg2_mc(&ext_empty[es], 0x3);
           }
           tc_commit_cg2_mc(&t_full[buf], 0x3);
         }
@@ -540,14 +610,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue (both CTAs)
     const int ew = warp - 4;
-    const int wg = ew >> 2;
-    const int q = warp & 3;
+    const int wg = ew >> 2;          // column half of every tile
+    const int q = warp & 3;          // TMEM lane quarter
     const int row = q * 32 + lane;
     uint32_t g = 0;
     int i = 0;
     for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
       const int b = t / p.tiles_per_batch;
-      const int row0 = (t - b * p.tiles_per_batch) * (2 * tc2::BM) + rank * tc2::BM;
+      const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
       const int slot = i & 1;
       float M = __int_as_float(0x7f800000);
       int best = -1;
@@ -556,23 +626,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       for (int j = 0; j < 32; ++j) bestv[j] = M;
       float xn = 0.f;
       for (int c = 0; c < p.ncol; ++c, ++g) {
-        const uint32_t buf = g & 1;
-        const uint32_t cslot = g % tc2::CN_SLOTS;
-        mbar_wait(&t_full[buf], (g >> 1) & 1);
+        const uint32_t buf = g % NBUF;
+        const uint32_t cslot = g % CN_SLOTS;
+        mbar_wait(&t_full[buf], (g / NBUF) & 1);
         tc_fence_after();
-        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + buf * tc2::BN + wg * 128;
+        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + buf * BN + wg * (BN / 2);
         uint32_t va[32], vb[32];
         FK_TMEM_LD_32x32b_X32(taddr, va);
         if (c == 0 && wg == 0) {
-          xn = row_norm_smem<FMT>(sA + slot * tc2::A_SLOT, row, p.katoms, lane);
+          xn = row_norm_smem<FMT>(sA + slot * A_SLOT, row, p.katoms, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_empty[slot]);
         }
-        mbar_wait(&cn_full[cslot], (g / tc2::CN_SLOTS) & 1);
-        const uint32_t cnp = smem_u32(sCN + cslot * tc2::BN + wg * 128);
-        const int col0 = c * tc2::BN + wg * 128;
-        if (p.debug_mode == 1) {
-          FK_TMEM_WAIT_LD(va);
+        uint32_t cnp = 0;
+        if (!AUG) {
+          mbar_wait(&cn_full[cslot], (g / CN_SLOTS) & 1);
+          cnp = smem_u32(sCN + cslot * BN + wg * (BN / 2));
+        }
+        const int col0 = c * BN + wg * (BN / 2);
+        auto release_tmem = [&]() {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) {
@@ -580,32 +652,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               mbar_arrive(&t_empty[buf]);
             else
               mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[buf]), 0));
-            mbar_arrive(&cn_empty[cslot]);
           }
+        };
+        auto chunk = [&](uint32_t (&v)[32], int ch) {
+          if (AUG)
+            epi_chunk_aug(v, col0 + 32 * ch, M, best, bestv);
+          else
+            epi_chunk(v, cnp + 128 * ch, col0 + 32 * ch, M, best, bestv);
+        };
+        if (p.debug_mode == 1) {
+          FK_TMEM_WAIT_LD(va);
+          release_tmem();
+          if (!AUG && lane == 0) mbar_arrive(&cn_empty[cslot]);
           M = fminf(M, __uint_as_float(va[0]));
           continue;
         }
         FK_TMEM_WAIT_LD(va);
         FK_TMEM_LD_32x32b_X32(taddr + 32, vb);
-        epi_chunk(va, cnp, col0, M, best, bestv);
+        chunk(va, 0);
         FK_TMEM_WAIT_LD(vb);
         FK_TMEM_LD_32x32b_X32(taddr + 64, va);
-        epi_chunk(vb, cnp + 128, col0 + 32, M, best, bestv);
+        chunk(vb, 1);
         FK_TMEM_WAIT_LD(va);
         FK_TMEM_LD_32x32b_X32(taddr + 96, vb);
-        epi_chunk(va, cnp + 256, col0 + 64, M, best, bestv);
+        chunk(va, 2);
         FK_TMEM_WAIT_LD(vb);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if (leader)
-            mbar_arrive(&t_empty[buf]);
-          else
-            mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[buf]), 0));
+        release_tmem();  // every TMEM read of this buffer has landed
+        chunk(vb, 3);
+        if (!AUG) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&cn_empty[cslot]);
         }
-        epi_chunk(vb, cnp + 384, col0 + 96, M, best, bestv);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&cn_empty[cslot]);
       }
       int idx = -1;
       if (best >= 0) {
@@ -631,7 +708,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         if (grow < p.N) {
           const size_t o = (size_t)b * p.N + grow;
           p.idx_out[o] = idx;
-          p.mind_out[o] = fmaxf(0.f, xn + M);
+          p.mind_out[o] = fmaxf(0.f, AUG ? fmaf(2.f, M, xn) : xn + M);
           if (p.idx_prev) ch = p.idx_prev[o] != idx;
         }
         if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
@@ -645,6 +722,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     tc_fence_after();
     tmem_dealloc_cg2<512>(tmem_base);
   }
+}
+
+template <int FMT, bool AUG>
+static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
+                               const CUtensorMap& tmext, TcArgs a, int num_sms,
+                               cudaStream_t stream) {
+  a.tiles_per_batch = (a.N + 2 * tc2::BM - 1) / (2 * tc2::BM);
+  a.total_tiles = a.B * a.tiles_per_batch;
+  a.ncol = (a.K + tc2::BN - 1) / tc2::BN;
+  int pairs = num_sms / 2;
+  if (a.total_tiles < pairs) pairs = a.total_tiles;
+  if (pairs <= 0) return cudaSuccess;
+  cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, AUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       tc2::SMEM_BYTES);
+  fk_assign_tc2_kernel<FMT, AUG><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(tmx, tmc,
+                                                                                      tmext, a);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- host side
@@ -661,33 +755,37 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-// 3-D map over (d, rows, B) with a {64, box_rows, 1} box and 128-B swizzle.
-static bool make_map(CUtensorMap* m, const void* base, int fmt, int64_t d, int64_t rows,
-                     int64_t B, int box_rows) {
+// 3-D map over (inner, rows, B): box {box_inner, box_rows, 1}; 128-B swizzle
+// for the 64-wide K atoms of X / C, 32-B swizzle for the 16-wide bias operand.
+static bool make_map(CUtensorMap* m, const void* base, int fmt, int64_t inner, int64_t rows,
+                     int64_t B, int box_rows, int box_inner = 64,
+                     CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode_fn();
   if (!enc) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)B};
-  cuuint64_t strides[2] = {(cuuint64_t)(d * 2), (cuuint64_t)(rows * d * 2)};
-  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)rows, (cuuint64_t)B};
+  cuuint64_t strides[2] = {(cuuint64_t)(inner * 2), (cuuint64_t)(rows * inner * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, fmt == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
 bool assign_tc_supported(int64_t d) { return d >= 8 && d <= 128 && (d % 8) == 0; }
 
+// Bias-in-GEMM is used for bf16 data (fp16 cannot hold ||c||^2/2 safely);
+// FK_ASSIGN_AUG=0 forces the epilogue-bias variant (A/B comparisons).
+bool assign_tc_uses_ext(int fmt) {
+  const char* e = getenv("FK_ASSIGN_AUG");
+  return fmt == 1 && !(e && atoi(e) == 0);
+}
+
 cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
-                             int64_t B, int64_t N, int64_t K, int64_t d, int32_t* idx_out,
-                             float* mind_out, const int32_t* idx_prev, int32_t* changed,
-                             int num_sms, cudaStream_t stream) {
-  CUtensorMap tmx, tmc, tmx2, tmc2;
-  if (!make_map(&tmx, X, fmt, d, N, B, tc::BM)) return cudaErrorInvalidValue;
-  if (!make_map(&tmc, C, fmt, d, K, B, tc::BN)) return cudaErrorInvalidValue;
-  if (!make_map(&tmx2, X, fmt, d, N, B, tc2::BM)) return cudaErrorInvalidValue;
-  if (!make_map(&tmc2, C, fmt, d, K, B, tc2::BNH)) return cudaErrorInvalidValue;
+                             const void* cn_ext, int64_t B, int64_t N, int64_t K, int64_t d,
+                             int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
+                             int32_t* changed, int num_sms, cudaStream_t stream) {
   TcArgs a;
   a.B = (int)B;
   a.N = (int)N;
@@ -708,26 +806,25 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     a.debug_mode = dm ? atoi(dm) : 0;
   }
   const char* cta = getenv("FK_ASSIGN_CTA");
-  const bool pair = !(cta && atoi(cta) == 1);
-  if (pair) {
-    // pair tiles of 256 rows; one cluster of 2 CTAs per TPC
-    a.tiles_per_batch = (int)((N + 2 * tc2::BM - 1) / (2 * tc2::BM));
-    a.total_tiles = (int)(B * a.tiles_per_batch);
-    int pairs = num_sms / 2;
-    if (a.total_tiles < pairs) pairs = a.total_tiles;
-    if (pairs <= 0) return cudaSuccess;
-    const int grid = 2 * pairs;
-    if (fmt == 1) {
-      cudaFuncSetAttribute(fk_assign_tc2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           tc2::SMEM_BYTES);
-      fk_assign_tc2_kernel<1><<<grid, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(tmx2, tmc2, a);
+  if (!(cta && atoi(cta) == 1)) {
+    CUtensorMap tmx2, tmc2, tmext;
+    if (!make_map(&tmx2, X, fmt, d, N, B, tc2::BM)) return cudaErrorInvalidValue;
+    if (!make_map(&tmc2, C, fmt, d, K, B, tc2::BNH)) return cudaErrorInvalidValue;
+    const bool aug = cn_ext != nullptr && assign_tc_uses_ext(fmt);
+    if (aug) {
+      if (!make_map(&tmext, cn_ext, fmt, 16, a.kpad, B, tc2::BNH, 16, CU_TENSOR_MAP_SWIZZLE_32B))
+        return cudaErrorInvalidValue;
     } else {
-      cudaFuncSetAttribute(fk_assign_tc2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           tc2::SMEM_BYTES);
-      fk_assign_tc2_kernel<0><<<grid, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(tmx2, tmc2, a);
+      tmext = tmc2;  // unused
     }
-    return cudaGetLastError();
+    if (fmt == 1)
+      return aug ? launch_pair<1, true>(tmx2, tmc2, tmext, a, num_sms, stream)
+                 : launch_pair<1, false>(tmx2, tmc2, tmext, a, num_sms, stream);
+    return launch_pair<0, false>(tmx2, tmc2, tmext, a, num_sms, stream);
   }
+  CUtensorMap tmx, tmc;
+  if (!make_map(&tmx, X, fmt, d, N, B, tc::BM)) return cudaErrorInvalidValue;
+  if (!make_map(&tmc, C, fmt, d, K, B, tc::BN)) return cudaErrorInvalidValue;
   const int grid = a.total_tiles < num_sms ? a.total_tiles : num_sms;
   if (grid <= 0) return cudaSuccess;
   if (fmt == 1) {

@@ -129,6 +129,14 @@ FK_DEV uint64_t make_sdesc_sw128(uint32_t smem_addr) {
          (uint64_t(1) << 46) | (uint64_t(2) << 61);
 }
 
+// Same for a K-major operand whose rows are 32 B (16 bf16) wide, stored with
+// SWIZZLE_32B (8-row / 256 B atoms): layout type 6, SBO = 256 B.
+FK_DEV uint64_t make_sdesc_sw32(uint32_t smem_addr) {
+  return uint64_t((smem_addr >> 4) & 0x3FFFu) | (uint64_t(1) << 16) | (uint64_t(256 >> 4) << 32) |
+         (uint64_t(1) << 46) | (uint64_t(6) << 61);
+}
+constexpr uint32_t kIdescNegateA = 1u << 13;
+
 // 32 lanes x 32 consecutive 32-bit columns -> 32 registers per thread.
 #define FK_TMEM_LD_32x32b_X32(taddr, r)                                                          \
   asm volatile(                                                                                  \
@@ -180,7 +188,7 @@ FK_DEV uint32_t mapa_shared(uint32_t local_addr, uint32_t rank) {
   return r;
 }
 FK_DEV void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
 // 2-SM TMA: the bytes land in this CTA's smem; completion is counted on the

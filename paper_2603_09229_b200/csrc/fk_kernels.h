@@ -11,14 +11,18 @@ enum Dt { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2, DT_F64 = 3 };
 // fk_assign_tc.cu
 bool assign_tc_supported(int64_t d);
 int assign_tc_kpad(int64_t K);
+bool assign_tc_uses_ext(int fmt);
 cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
-                             int64_t B, int64_t N, int64_t K, int64_t d, int32_t* idx_out,
-                             float* mind_out, const int32_t* idx_prev, int32_t* changed,
-                             int num_sms, cudaStream_t stream);
+                             const void* cn_ext, int64_t B, int64_t N, int64_t K, int64_t d,
+                             int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
+                             int32_t* changed, int num_sms, cudaStream_t stream);
 
 // fk_assign_exact.cu
 cudaError_t launch_cn_pad(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
                           float* cn_pad, cudaStream_t stream);
+// (B, kpad, 16) operand [hi, mid, lo, 0...] of ||c||^2 / 2 (+inf beyond K)
+cudaError_t launch_cn_ext(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
+                          void* out, cudaStream_t stream);
 cudaError_t launch_row_norms_exact(int dt, const void* M, int64_t rows, int64_t d, void* out,
                                    cudaStream_t stream);
 cudaError_t launch_assign_exact(int dt, const void* X, const void* C, const void* xn,
