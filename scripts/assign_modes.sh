@@ -1,4 +1,4 @@
-for m in 0 1 2; do FK_ASSIGN_DEBUG_MODE=$m python - <<'PY'
+for m in ${MODES:-0 1 2}; do FK_ASSIGN_DEBUG_MODE=$m python - <<'PY'
 import os, sys, torch
 sys.path.insert(0, ".")
 from paper_2603_09229_b200 import ops
