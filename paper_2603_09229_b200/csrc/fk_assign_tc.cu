@@ -69,62 +69,7 @@ struct TcArgs {
   int32_t* changed;
   int debug_mode;  // 0 normal; 1 epilogue skips math (MMA/TMA bound); 2 MMA skipped (epilogue bound)
   unsigned long long* trace;  // debug timeline (FK_ASSIGN_TRACE), nullptr normally
-  const void* C;              // (B, K, d) MMA operand (warm start reads the previous centroid)
-  const uint16_t* ext;        // (B, kpad, 16) [hi, mid, lo] of ||c||^2 / 2 (bias-in-GEMM)
-  int warm;                   // 1: seed each row's minimum with its previous centroid's score
 };
-
-// Warm start (Lloyd iterations >= 2): s(prev) = ||c_prev||^2/2 - x . c_prev on
-// CUDA cores from the resident X row, so the running minimum starts near its
-// final value and the epilogue's chunk capture almost never fires once
-// assignments stabilize.  Also returns ||x||^2.
-template <int FMT>
-FK_DEV void warm_row(const uint8_t* a_slot, int row, int katoms, int lane, int d,
-                     const uint16_t* __restrict__ crow, const uint16_t* __restrict__ erow,
-                     float& xn, float& s_prev) {
-  float acc_xx = 0.f, acc_xc = 0.f;
-  for (int ka = 0; ka < katoms; ++ka) {
-    const uint4* r = reinterpret_cast<const uint4*>(a_slot + ka * tc::A_ATOM + row * 128);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      // SWIZZLE_128B: physical 16-B chunk pj of a row holds logical chunk pj ^ (row & 7)
-      const int pj = (j + lane) & 7;
-      const int col = ka * 64 + ((pj ^ (row & 7)) << 3);
-      const uint4 w = r[pj];
-      uint4 cw = make_uint4(0u, 0u, 0u, 0u);
-      if (crow != nullptr && col < d) cw = __ldg(reinterpret_cast<const uint4*>(crow + col));
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-      const uint32_t cs[4] = {cw.x, cw.y, cw.z, cw.w};
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        float xl, xh, cl, ch;
-        if (FMT == 1) {
-          xl = __uint_as_float(ws[e] << 16);
-          xh = __uint_as_float(ws[e] & 0xffff0000u);
-          cl = __uint_as_float(cs[e] << 16);
-          ch = __uint_as_float(cs[e] & 0xffff0000u);
-        } else {
-          const float2 fx = __half22float2(*reinterpret_cast<const __half2*>(&ws[e]));
-          const float2 fc = __half22float2(*reinterpret_cast<const __half2*>(&cs[e]));
-          xl = fx.x; xh = fx.y; cl = fc.x; ch = fc.y;
-        }
-        acc_xx = fmaf(xl, xl, acc_xx);
-        acc_xx = fmaf(xh, xh, acc_xx);
-        acc_xc = fmaf(xl, cl, acc_xc);
-        acc_xc = fmaf(xh, ch, acc_xc);
-      }
-    }
-  }
-  xn = acc_xx;
-  s_prev = __int_as_float(0x7f800000);
-  if (crow != nullptr) {
-    // the bias operand holds ||c||^2/2 as hi + mid + lo (bf16)
-    const float hi = __uint_as_float(uint32_t(erow[0]) << 16);
-    const float mid = __uint_as_float(uint32_t(erow[1]) << 16);
-    const float lo = __uint_as_float(uint32_t(erow[2]) << 16);
-    s_prev = ((hi + mid) + lo) - acc_xc;
-  }
-}
 
 // Debug timeline: events of pair 0 / tile window [TR_G0, TR_G0 + TR_N) only.
 constexpr int TR_G0 = 64, TR_N = 64, TR_EV = 8;
@@ -468,11 +413,7 @@ static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB dynamic shared memory");
 }  // namespace tc2
 
 // Epilogue chunk when the bias is already in the accumulator (s = ||c||^2/2 - x.c).
-// best == -2 means "warm start, still at the previous centroid `prev`": a chunk
-// holding an exactly equal score at an index <= prev is captured as well, so
-// the lowest-index tie rule survives the warm start.
-FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, float (&bestv)[32],
-                          int prev) {
+FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, float (&bestv)[32]) {
   const float* s = reinterpret_cast<const float*>(v);
   float a[11];
 #pragma unroll
@@ -483,7 +424,7 @@ FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, f
   const float b2 = fmin3(a[6], a[7], a[8]);
   const float b3 = fminf(a[9], a[10]);
   const float mc = fmin3(b0, b1, fminf(b2, b3));
-  const bool p = mc < M || (best == -2 && mc == M && colbase <= prev);
+  const bool p = mc < M;
   if (__any_sync(0xffffffffu, p)) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) bestv[j] = p ? s[j] : bestv[j];
@@ -543,7 +484,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     if (AUG) tma_prefetch_desc(&tmext);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&a_full[s], 1);       // leader's expect_tx (both CTAs' bytes)
-      mbar_init(&a_empty[s], 1 + 8);  // pair-MMA commit + the 8 epilogue warps of this CTA
+      mbar_init(&a_empty[s], 1 + 4);  // pair-MMA commit + 4 warps of this CTA's WG0
     }
     for (int s = 0; s < NBUF; ++s) {
       mbar_init(&t_full[s], 1);
@@ -708,12 +649,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
 #pragma unroll
       for (int j = 0; j < 32; ++j) bestv[j] = M;
       float xn = 0.f;
-      int prev = -1;
-      if (AUG && p.warm && p.idx_prev) {
-        const int grow = row0 + row;
-        if (grow < p.N) prev = p.idx_prev[(size_t)b * p.N + grow];
-        if (prev >= p.K) prev = -1;
-      }
       for (int c = 0; c < p.ncol; ++c, ++g) {
         const uint32_t buf = g % NBUF;
         const uint32_t cslot = g % CN_SLOTS;
@@ -724,21 +659,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + buf * BN + wg * (BN / 2);
         uint32_t va[32], vb[32];
         FK_TMEM_LD_32x32b_X32(taddr, va);
-        if (c == 0) {
-          // every epilogue warp reads its rows of the resident X tile once per
-          // row tile: ||x||^2 and, with a warm start, the previous centroid's score
-          const uint16_t* crow = nullptr;
-          const uint16_t* erow = nullptr;
-          if (prev >= 0) {
-            crow = reinterpret_cast<const uint16_t*>(p.C) + ((size_t)b * p.K + prev) * p.d;
-            erow = p.ext + ((size_t)b * p.kpad + prev) * 16;
-          }
-          float s_prev;
-          warm_row<FMT>(sA + slot * A_SLOT, row, p.katoms, lane, p.d, crow, erow, xn, s_prev);
-          if (prev >= 0) {
-            M = s_prev;
-            best = -2;
-          }
+        if (c == 0 && wg == 0) {
+          xn = row_norm_smem<FMT>(sA + slot * A_SLOT, row, p.katoms, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_empty[slot]);
         }
@@ -760,7 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         };
         auto chunk = [&](uint32_t (&v)[32], int ch) {
           if (AUG)
-            epi_chunk_aug(v, col0 + 32 * ch, M, best, bestv, prev);
+            epi_chunk_aug(v, col0 + 32 * ch, M, best, bestv);
           else
             epi_chunk(v, cnp + 128 * ch, col0 + 32 * ch, M, best, bestv);
         };
@@ -805,7 +727,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           if (lane == 0) mbar_arrive(&cn_empty[cslot]);
         }
       }
-      int idx = best == -2 ? prev : -1;
+      int idx = -1;
       if (best >= 0) {
         int found = 31;
 #pragma unroll
@@ -925,12 +847,6 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
   {
     const char* dm = getenv("FK_ASSIGN_DEBUG_MODE");
     a.debug_mode = dm ? atoi(dm) : 0;
-  }
-  a.C = C;
-  a.ext = reinterpret_cast<const uint16_t*>(cn_ext);
-  {
-    const char* w = getenv("FK_ASSIGN_WARM");
-    a.warm = (idx_prev != nullptr && cn_ext != nullptr && !(w && atoi(w) == 0)) ? 1 : 0;
   }
   a.trace = nullptr;
   static unsigned long long* trace_buf = nullptr;
