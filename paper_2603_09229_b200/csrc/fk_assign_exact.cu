@@ -71,7 +71,8 @@ __global__ void k_cn_pad(const T* __restrict__ C, int64_t B, int64_t K, int64_t 
 // Bias operand for the bias-in-GEMM FlashAssign: ||c||^2 / 2 split into three
 // bf16 terms (24 significant bits) so that one extra K=16 MMA step against a
 // constant ones operand adds it to the accumulator exactly enough.
-__global__ void k_cn_ext_bf16(const __nv_bfloat16* __restrict__ C, int64_t B, int64_t K, int64_t d,
+template <typename T>
+__global__ void k_cn_ext_bf16(const T* __restrict__ C, int64_t B, int64_t K, int64_t d,
                               int kpad, __nv_bfloat16* out) {
   const int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -82,10 +83,10 @@ __global__ void k_cn_ext_bf16(const __nv_bfloat16* __restrict__ C, int64_t B, in
     if (lane < 16) o[lane] = lane == 0 ? __float2bfloat16(__int_as_float(0x7f800000)) : __float2bfloat16(0.f);
     return;
   }
-  const __nv_bfloat16* p = C + (b * K + k) * d;
+  const T* p = C + (b * K + k) * d;
   float acc = 0.f;
   for (int64_t j = lane; j < d; j += 32) {
-    const float v = __bfloat162float(p[j]);
+    const float v = to_f32(p[j]);
     acc = fmaf(v, v, acc);
   }
   for (int s = 16; s; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
@@ -99,11 +100,16 @@ __global__ void k_cn_ext_bf16(const __nv_bfloat16* __restrict__ C, int64_t B, in
 
 cudaError_t launch_cn_ext(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
                           void* out, cudaStream_t stream) {
-  if (dt != DT_BF16) return cudaErrorInvalidValue;
   const int64_t n = B * kpad * 32;
   const int th = 256;
-  k_cn_ext_bf16<<<(unsigned)((n + th - 1) / th), th, 0, stream>>>(
-      (const __nv_bfloat16*)C, B, K, d, kpad, (__nv_bfloat16*)out);
+  if (dt == DT_BF16)
+    k_cn_ext_bf16<__nv_bfloat16><<<(unsigned)((n + th - 1) / th), th, 0, stream>>>(
+        (const __nv_bfloat16*)C, B, K, d, kpad, (__nv_bfloat16*)out);
+  else if (dt == DT_F16)
+    k_cn_ext_bf16<__half><<<(unsigned)((n + th - 1) / th), th, 0, stream>>>(
+        (const __half*)C, B, K, d, kpad, (__nv_bfloat16*)out);
+  else
+    return cudaErrorInvalidValue;
   return cudaGetLastError();
 }
 

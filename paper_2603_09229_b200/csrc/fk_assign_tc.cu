@@ -72,7 +72,7 @@ struct TcArgs {
 };
 
 // Debug timeline: events of pair 0 / tile window [TR_G0, TR_G0 + TR_N) only.
-constexpr int TR_G0 = 64, TR_N = 64, TR_EV = 8;
+constexpr int TR_G0 = 16, TR_N = 32, TR_EV = 8;
 FK_DEV void trace_ev(const TcArgs& p, uint32_t g, int ev) {
   if (p.trace && g >= TR_G0 && g < TR_G0 + TR_N) p.trace[(g - TR_G0) * TR_EV + ev] = clock64();
 }
@@ -405,7 +405,7 @@ constexpr int OFF_EXT = OFF_AEXT + BM * EXT_ROW;
 constexpr int OFF_CN = OFF_EXT + EXT_SLOTS * EXT_SLOT;
 constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;
 constexpr int OFF_BAR = OFF_XCH + BM * 8;
-constexpr int NBARS = 4 + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
+constexpr int NBARS = 8 + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
 constexpr int SMEM_USED = OFF_BAR + NBARS * 8 + 16;
 constexpr int SMEM_BYTES = SMEM_USED + 1024;
 constexpr int THREADS = 384;
@@ -456,8 +456,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   int* xch_i = reinterpret_cast<int*>(smem + OFF_XCH + BM * 4);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* a_full = bars + 0;
-  uint64_t* a_empty = bars + 2;
-  uint64_t* t_full = bars + 4;
+  uint64_t* a_empty = bars + 4;
+  uint64_t* t_full = bars + 8;
   uint64_t* t_empty = t_full + NBUF;
   uint64_t* b_full = t_empty + NBUF;
   uint64_t* b_empty = b_full + STAGES;
@@ -477,18 +477,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
+  // X row-tile ring: the 64 KB A region holds 2 slots of 2 K-atoms (d <= 128)
+  // or 4 slots of 1 atom (d <= 64): deeper prefetch when a row tile is short.
+  const int a_slots = p.katoms == 1 ? 4 : 2;
+  const int a_slot_bytes = p.katoms * A_ATOM;
+  // Single-column-tile rows (K <= 256): the two epilogue warpgroups take
+  // alternate tiles (whole rows each, two tiles in flight, no merge) instead
+  // of splitting every tile's columns.
+  const bool alt = p.ncol == 1;
+  const int epi_warps_per_buf = alt ? 4 : 8;
 
   if (warp == W_PRODUCER && lane == 0) {
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmc);
     if (AUG) tma_prefetch_desc(&tmext);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < 4; ++s) {
       mbar_init(&a_full[s], 1);       // leader's expect_tx (both CTAs' bytes)
       mbar_init(&a_empty[s], 1 + 4);  // pair-MMA commit + 4 warps of this CTA's WG0
     }
     for (int s = 0; s < NBUF; ++s) {
       mbar_init(&t_full[s], 1);
-      mbar_init(&t_empty[s], 16);     // every epilogue warp of both CTAs
+      mbar_init(&t_empty[s], 2 * epi_warps_per_buf);  // epilogue warps of both CTAs
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&b_full[s], 1);
@@ -496,7 +505,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     }
     for (int s = 0; s < CN_SLOTS; ++s) {
       mbar_init(&cn_full[s], 1);
-      mbar_init(&cn_empty[s], 8);
+      mbar_init(&cn_empty[s], epi_warps_per_buf);
     }
     for (int s = 0; s < EXT_SLOTS; ++s) {
       mbar_init(&ext_full[s], 1);
@@ -507,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   if (AUG && warp == W_INIT) {
     // A_ext rows = [1,1,1,0,0,0,0,0] in BOTH 16-byte halves: invariant under
     // the 32-byte swizzle, and only columns 0-2 of B_ext are non-zero.
-    const uint32_t one = FMT == 1 ? 0x3F80u : 0x3C00u;
+    const uint32_t one = 0x3F80u;  // bf16 1.0 (bias MMA is bf16 x bf16 for any data type)
     const uint4 v = make_uint4(one | (one << 16), one, 0u, 0u);
     uint4* dst = reinterpret_cast<uint4*>(sAext);
     for (int i = lane; i < BM * 2; i += 32) dst[i] = v;
@@ -525,21 +534,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       uint32_t stage = 0, sphase = 0;
       const uint32_t a_bytes = p.katoms * A_ATOM;
       auto load_a = [&](int t, int j) {
-        const int slot = j & 1;
+        const int slot = j % a_slots;
         const int b = t / p.tiles_per_batch;
         const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
-        mbar_wait(&a_empty[slot], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&a_empty[slot], ((j / a_slots) & 1) ^ 1);
         if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
         const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
         for (int ka = 0; ka < p.katoms; ++ka)
-          tma_load_3d_cg2(sA + slot * A_SLOT + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
+          tma_load_3d_cg2(sA + slot * a_slot_bytes + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
                           kEvictFirst);
       };
       int i = 0;
       uint32_t g = 0;
       for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
         const int b = t / p.tiles_per_batch;
-        if (i == 0) load_a(t, 0);
+        if (i == 0)  // prime the ring: this tile and the next a_slots - 2
+          for (int j = 0; j < a_slots - 1 && t + j * npairs < p.total_tiles; ++j)
+            load_a(t + j * npairs, j);
         for (int c = 0; c < p.ncol; ++c, ++g) {
           if (AUG) {
             const uint32_t slot = g % EXT_SLOTS;
@@ -566,8 +577,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           }
           if (pair == 0 && leader) trace_ev(p, g, 5);
           if (c == 0) {
-            const int t2 = t + npairs;
-            if (t2 < p.total_tiles) load_a(t2, i + 1);
+            const int t2 = t + (a_slots - 1) * npairs;
+            if (t2 < p.total_tiles) load_a(t2, i + a_slots - 1);
           }
         }
       }
@@ -579,14 +590,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     if (leader) {
       const uint32_t idesc = make_idesc_f16(FMT, 2 * BM, BN);
       const uint32_t idesc_main = AUG ? (idesc | kIdescNegateA) : idesc;
+      const uint32_t idesc_ext = make_idesc_f16(1, 2 * BM, BN);
       const uint64_t aext_desc = make_sdesc_sw32(smem_u32(sAext));
       uint32_t stage = 0, sphase = 0, g = 0;
       int i = 0;
       for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
-        const int slot = i & 1;
-        mbar_wait(&a_full[slot], (i >> 1) & 1);
+        const int slot = i % a_slots;
+        mbar_wait(&a_full[slot], (i / a_slots) & 1);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(sA + slot * A_SLOT);
+        const uint32_t a_base = smem_u32(sA + slot * a_slot_bytes);
         for (int c = 0; c < p.ncol; ++c, ++g) {
           const uint32_t buf = g % NBUF;
           if (pair == 0 && lane == 0) trace_ev(p, g, 6);
@@ -619,7 +631,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             tc_fence_after();
             const uint64_t edesc = make_sdesc_sw32(smem_u32(sExt + es * EXT_SLOT));
             if (elect_one()) {
-              tc_mma_f16_cg2(d_tmem, aext_desc, edesc, idesc, p.debug_mode != 2 ? 1u : 0u);
+              tc_mma_f16_cg2(d_tmem, aext_desc, edesc, idesc_ext, p.debug_mode != 2 ? 1u : 0u);
               tc_commit_cg2_mc(&ext_empty[es], 0x3);
             }
             __syncwarp();
@@ -634,15 +646,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ epilogue (both CTAs)
-    const int wg = warp >> 2;        // column half of every tile
+    const int wg = warp >> 2;        // column half of every tile (alt: tile parity)
     const int q = warp & 3;          // TMEM lane quarter
     const int row = q * 32 + lane;
+    const int ncols = alt ? BN : BN / 2;  // columns this warp reads per tile
     uint32_t g = 0;
     int i = 0;
     for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
+      if (alt && (i & 1) != wg) {  // the other warpgroup owns this tile
+        ++g;
+        continue;
+      }
       const int b = t / p.tiles_per_batch;
       const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
-      const int slot = i & 1;
+      const int slot = i % a_slots;
       float M = __int_as_float(0x7f800000);
       int best = -1;
       float bestv[32];
@@ -656,20 +673,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         mbar_wait(&t_full[buf], (g / NBUF) & 1);
         tc_fence_after();
         if (tr) trace_ev(p, g, 2);
-        const uint32_t taddr = tmem_base + (uint32_t(q * 32) << 16) + buf * BN + wg * (BN / 2);
+        const uint32_t taddr =
+            tmem_base + (uint32_t(q * 32) << 16) + buf * BN + (alt ? 0 : wg * (BN / 2));
         uint32_t va[32], vb[32];
         FK_TMEM_LD_32x32b_X32(taddr, va);
-        if (c == 0 && wg == 0) {
-          xn = row_norm_smem<FMT>(sA + slot * A_SLOT, row, p.katoms, lane);
+        if (c == 0 && (alt || wg == 0)) {
+          xn = row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane);
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_empty[slot]);
         }
         uint32_t cnp = 0;
         if (!AUG) {
           mbar_wait(&cn_full[cslot], (g / CN_SLOTS) & 1);
-          cnp = smem_u32(sCN + cslot * BN + wg * (BN / 2));
+          cnp = smem_u32(sCN + cslot * BN + (alt ? 0 : wg * (BN / 2)));
         }
-        const int col0 = c * BN + wg * (BN / 2);
+        const int col0 = c * BN + (alt ? 0 : wg * (BN / 2));
         auto release_tmem = [&]() {
           tc_fence_before();
           __syncwarp();
@@ -693,34 +711,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           M = fminf(M, __uint_as_float(va[0]));
           continue;
         }
-        if (p.debug_mode == 4) {  // every TMEM read, no math
+        const int nch = ncols / 32;  // 4 (column split) or 8 (alternate tiles)
+        for (int ch = 0; ch < nch; ch += 2) {
           FK_TMEM_WAIT_LD(va);
-          FK_TMEM_LD_32x32b_X32(taddr + 32, vb);
+          FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 1), vb);
+          chunk(va, ch);
           FK_TMEM_WAIT_LD(vb);
-          M = fminf(M, __uint_as_float(va[0]));
-          FK_TMEM_LD_32x32b_X32(taddr + 64, va);
-          FK_TMEM_WAIT_LD(va);
-          M = fminf(M, __uint_as_float(vb[0]));
-          FK_TMEM_LD_32x32b_X32(taddr + 96, vb);
-          FK_TMEM_WAIT_LD(vb);
-          M = fminf(M, __uint_as_float(va[0]) + __uint_as_float(vb[0]));
-          release_tmem();
-          if (!AUG && lane == 0) mbar_arrive(&cn_empty[cslot]);
-          continue;
+          if (ch + 2 < nch) {
+            FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 2), va);
+          } else {
+            release_tmem();  // every TMEM read of this buffer has landed
+            if (tr) trace_ev(p, g, 3);
+          }
+          chunk(vb, ch + 1);
         }
-        FK_TMEM_WAIT_LD(va);
-        FK_TMEM_LD_32x32b_X32(taddr + 32, vb);
-        chunk(va, 0);
-        FK_TMEM_WAIT_LD(vb);
-        FK_TMEM_LD_32x32b_X32(taddr + 64, va);
-        chunk(vb, 1);
-        FK_TMEM_WAIT_LD(va);
-        FK_TMEM_LD_32x32b_X32(taddr + 96, vb);
-        chunk(va, 2);
-        FK_TMEM_WAIT_LD(vb);
-        release_tmem();  // every TMEM read of this buffer has landed
-        if (tr) trace_ev(p, g, 3);
-        chunk(vb, 3);
         if (tr) trace_ev(p, g, 4);
         if (!AUG) {
           __syncwarp();
@@ -734,18 +738,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         for (int j = 31; j >= 0; --j) found = (bestv[j] == M) ? j : found;
         idx = best + found;
       }
-      if (wg == 1) {
-        xch_m[row] = M;
-        xch_i[row] = idx;
-      }
-      named_bar_sync(1, 256);
-      if (wg == 0) {
-        const float M1 = xch_m[row];
-        const int i1 = xch_i[row];
-        if (M1 < M || (M1 == M && i1 >= 0 && (idx < 0 || i1 < idx))) {
-          M = M1;
-          idx = i1;
+      if (!alt) {
+        if (wg == 1) {
+          xch_m[row] = M;
+          xch_i[row] = idx;
         }
+        named_bar_sync(1, 256);
+        if (wg == 0) {
+          const float M1 = xch_m[row];
+          const int i1 = xch_i[row];
+          if (M1 < M || (M1 == M && i1 >= 0 && (idx < 0 || i1 < idx))) {
+            M = M1;
+            idx = i1;
+          }
+        }
+      }
+      if (alt || wg == 0) {
         const int grow = row0 + row;
         bool ch = false;
         if (grow < p.N) {
@@ -756,7 +764,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         }
         if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
       }
-      named_bar_sync(2, 256);
+      if (!alt) named_bar_sync(2, 256);
     }
     tc_fence_before();
   }
@@ -777,8 +785,14 @@ static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
   int pairs = num_sms / 2;
   if (a.total_tiles < pairs) pairs = a.total_tiles;
   if (pairs <= 0) return cudaSuccess;
-  cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, AUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       tc2::SMEM_BYTES);
+  static int attr_dev_mask = 0;  // one-time per device (keeps graph capture free of it)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_dev_mask & (1 << (dev & 31)))) {
+    cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, AUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         tc2::SMEM_BYTES);
+    attr_dev_mask |= 1 << (dev & 31);
+  }
   fk_assign_tc2_kernel<FMT, AUG><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(tmx, tmc,
                                                                                       tmext, a);
   return cudaGetLastError();
@@ -821,8 +835,9 @@ bool assign_tc_supported(int64_t d) { return d >= 8 && d <= 128 && (d % 8) == 0;
 // Bias-in-GEMM is used for bf16 data (fp16 cannot hold ||c||^2/2 safely);
 // FK_ASSIGN_AUG=0 forces the epilogue-bias variant (A/B comparisons).
 bool assign_tc_uses_ext(int fmt) {
+  (void)fmt;
   const char* e = getenv("FK_ASSIGN_AUG");
-  return fmt == 1 && !(e && atoi(e) == 0);
+  return !(e && atoi(e) == 0);
 }
 
 cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
@@ -863,14 +878,15 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     if (!make_map(&tmc2, C, fmt, d, K, B, tc2::BNH)) return cudaErrorInvalidValue;
     const bool aug = cn_ext != nullptr && assign_tc_uses_ext(fmt);
     if (aug) {
-      if (!make_map(&tmext, cn_ext, fmt, 16, a.kpad, B, tc2::BNH, 16, CU_TENSOR_MAP_SWIZZLE_32B))
+      if (!make_map(&tmext, cn_ext, 1, 16, a.kpad, B, tc2::BNH, 16, CU_TENSOR_MAP_SWIZZLE_32B))
         return cudaErrorInvalidValue;
     } else {
       tmext = tmc2;  // unused
     }
     cudaError_t e = fmt == 1 ? (aug ? launch_pair<1, true>(tmx2, tmc2, tmext, a, num_sms, stream)
                                     : launch_pair<1, false>(tmx2, tmc2, tmext, a, num_sms, stream))
-                             : launch_pair<0, false>(tmx2, tmc2, tmext, a, num_sms, stream);
+                             : (aug ? launch_pair<0, true>(tmx2, tmc2, tmext, a, num_sms, stream)
+                                    : launch_pair<0, false>(tmx2, tmc2, tmext, a, num_sms, stream));
     if (trace_path && e == cudaSuccess) {  // debug only: synchronous dump
       unsigned long long h[TR_N * TR_EV];
       cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, stream);

@@ -33,34 +33,40 @@ FK_DEV double as_f64(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
 FK_DEV double as_f64(__half v) { return (double)__half2float(v); }
 
 // ----------------------------------------------------------------- hist
-// Each block owns a contiguous range of points.  With B*K <= HIST_SMEM_KEYS
-// the block histograms in shared memory and publishes one atomic per
-// non-empty bin; otherwise identical keys are warp-aggregated.
-__device__ __forceinline__ void range_of(int64_t P, int64_t& lo, int64_t& hi) {
-  const int64_t per = (P + gridDim.x - 1) / gridDim.x;
-  lo = (int64_t)blockIdx.x * per;
-  hi = lo + per < P ? lo + per : P;
+// Each block owns a contiguous range of one batch element's points.  With
+// K <= HIST_SMEM_KEYS the block histograms in shared memory and publishes one
+// atomic per non-empty bin; otherwise identical keys are warp-aggregated.
+// Blocks are laid out per batch element (gridDim.x = B * bpb): block j of
+// element b owns a contiguous slice of that element's points, so a shared
+// histogram needs only K bins, whatever B is.
+__device__ __forceinline__ void range_of(int64_t N, int bpb, int64_t& b, int64_t& lo,
+                                         int64_t& hi) {
+  b = blockIdx.x / bpb;
+  const int j = blockIdx.x - (int)b * bpb;
+  const int64_t per = (N + bpb - 1) / bpb;
+  lo = b * N + (int64_t)j * per;
+  const int64_t end = (int64_t)j * per + per < N ? (int64_t)j * per + per : N;
+  hi = b * N + end;
 }
 
 __global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, int64_t B, int64_t N,
-                                               int64_t K, int32_t* __restrict__ hist) {
+                                               int64_t K, int bpb, int32_t* __restrict__ hist) {
   extern __shared__ int32_t sh[];
-  const int64_t BK = B * K;
-  const bool use_smem = BK <= HIST_SMEM_KEYS;
-  int64_t lo, hi;
-  range_of(B * N, lo, hi);
+  const bool use_smem = K <= HIST_SMEM_KEYS;
+  int64_t b, lo, hi;
+  range_of(N, bpb, b, lo, hi);
   if (use_smem) {
-    for (int64_t k = threadIdx.x; k < BK; k += blockDim.x) sh[k] = 0;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sh[k] = 0;
     __syncthreads();
   }
 #pragma unroll 4
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const int32_t id = __ldg(ids + i);
     if (id < 0 || id >= K) continue;  // validated on the host side
-    const int64_t key = B == 1 ? id : (i / N) * K + id;
     if (use_smem) {
-      atomicAdd(&sh[key], 1);
+      atomicAdd(&sh[id], 1);
     } else {
+      const int64_t key = b * K + id;
       const unsigned peers = __match_any_sync(__activemask(), key);
       const int leader = __ffs(peers) - 1;
       if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[key], __popc(peers));
@@ -68,13 +74,15 @@ __global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, 
   }
   if (use_smem) {
     __syncthreads();
-    for (int64_t k = threadIdx.x; k < BK; k += blockDim.x)
-      if (sh[k]) atomicAdd(&hist[k], sh[k]);
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
+      if (sh[k]) atomicAdd(&hist[b * K + k], sh[k]);
   }
 }
 
 // ----------------------------------------------------------------- scan
-// Single block of 1024 threads; each thread owns a contiguous key range.
+// One block of 1024 threads walks the keys in coalesced tiles of 1024:
+// block-wide exclusive scan per tile plus a running carry.  Also produces the
+// int64 counts and the reference's synchronized_merges count.
 __global__ void __launch_bounds__(1024)
     k_scan(const int32_t* __restrict__ hist, int64_t B, int64_t N, int64_t K, int64_t chunk,
            int accumulate, int64_t* __restrict__ off, int32_t* __restrict__ cursor,
@@ -83,54 +91,50 @@ __global__ void __launch_bounds__(1024)
   __shared__ unsigned long long warp_mg[32];
   const int64_t BK = B * K;
   const int t = threadIdx.x;
-  const int64_t per = (BK + blockDim.x - 1) / blockDim.x;
-  const int64_t k0 = t * per;
-  const int64_t k1 = (k0 + per < BK) ? k0 + per : BK;
-  int64_t local = 0;
-  for (int64_t k = k0; k < k1; ++k) local += hist[k];
-  int64_t v = local;
   const int lane = t & 31, w = t >> 5;
-  for (int o = 1; o < 32; o <<= 1) {
-    int64_t u = __shfl_up_sync(0xffffffffu, v, o);
-    if (lane >= o) v += u;
-  }
-  if (lane == 31) warp_tot[w] = v;
-  __syncthreads();
-  if (w == 0) {
-    int64_t x = (lane < (int)(blockDim.x >> 5)) ? warp_tot[lane] : 0;
-    for (int o = 1; o < 32; o <<= 1) {
-      int64_t u = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += u;
-    }
-    warp_tot[lane] = x;  // inclusive over warps
-  }
-  __syncthreads();
-  int64_t run = v - local + (w > 0 ? warp_tot[w - 1] : 0);  // exclusive prefix
+  int64_t carry = 0;
   unsigned long long mg = 0;
-  int64_t b = k0 / K, kb_end = (b + 1) * K;
-  for (int64_t k = k0; k < k1; ++k) {
-    if (k >= kb_end) {
-      ++b;
-      kb_end += K;
+  for (int64_t base = 0; base < BK; base += 1024) {
+    const int64_t k = base + t;
+    const int64_t c = k < BK ? hist[k] : 0;
+    int64_t v = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += u;
     }
-    const int64_t c = hist[k];
-    off[k] = run;
-    cursor[k] = (int32_t)run;
-    counts[k] = accumulate ? counts[k] + c : c;
-    if (c > 0 && merges) {
-      // reference merges: the run [s, e) of this key inside its batch element
-      // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks.
-      const int64_t s = run - b * N, e = s + c;
-      mg += (unsigned long long)((e - 1) / chunk - s / chunk + 1);
+    if (lane == 31) warp_tot[w] = v;
+    __syncthreads();
+    if (w == 0) {
+      int64_t x = warp_tot[lane];
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += u;
+      }
+      warp_tot[lane] = x;  // inclusive over warps
     }
-    run += c;
+    __syncthreads();
+    const int64_t run = carry + v - c + (w > 0 ? warp_tot[w - 1] : 0);  // exclusive prefix
+    if (k < BK) {
+      off[k] = run;
+      cursor[k] = (int32_t)run;
+      counts[k] = accumulate ? counts[k] + c : c;
+      if (c > 0 && merges) {
+        // reference merges: the run [s, e) of this key inside its batch element
+        // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks.
+        const int64_t b = k / K;
+        const int64_t s0 = run - b * N, e = s0 + c;
+        mg += (unsigned long long)((e - 1) / chunk - s0 / chunk + 1);
+      }
+    }
+    carry += warp_tot[31];
+    __syncthreads();
   }
-  if (k1 == BK && k0 < k1) off[BK] = run;  // exactly one thread owns the last key
+  if (t == 0) off[BK] = carry;
   for (int o = 16; o; o >>= 1) mg += __shfl_xor_sync(0xffffffffu, mg, o);
   if (lane == 0) warp_mg[w] = mg;
   __syncthreads();
   if (w == 0 && merges) {
-    unsigned long long m = (lane < (int)(blockDim.x >> 5)) ? warp_mg[lane] : 0;
+    unsigned long long m = warp_mg[lane];
     for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
     if (lane == 0) atomicAdd((unsigned long long*)merges, m);
   }
@@ -142,31 +146,30 @@ __global__ void __launch_bounds__(1024)
 // non-empty key with a single global atomic, then hands out positions with
 // shared-memory cursors -- no per-point global atomics, no dependency chains.
 __global__ void __launch_bounds__(1024)
-    k_scatter_block(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K,
+    k_scatter_block(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K, int bpb,
                     int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
   extern __shared__ int32_t sh[];
-  const int64_t BK = B * K;
-  int64_t lo, hi;
-  range_of(B * N, lo, hi);
-  for (int64_t k = threadIdx.x; k < BK; k += blockDim.x) sh[k] = 0;
+  int64_t b, lo, hi;
+  range_of(N, bpb, b, lo, hi);
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sh[k] = 0;
   __syncthreads();
 #pragma unroll 4
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const int32_t id = __ldg(ids + i);
     if (id < 0 || id >= K) continue;
-    atomicAdd(&sh[B == 1 ? id : (i / N) * K + id], 1);
+    atomicAdd(&sh[id], 1);
   }
   __syncthreads();
-  for (int64_t k = threadIdx.x; k < BK; k += blockDim.x) {
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
     const int32_t c = sh[k];
-    sh[k] = c ? atomicAdd(&cursor[k], c) : 0;
+    sh[k] = c ? atomicAdd(&cursor[b * K + k], c) : 0;
   }
   __syncthreads();
 #pragma unroll 4
   for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
     const int32_t id = __ldg(ids + i);
     if (id < 0 || id >= K) continue;
-    const int pos = atomicAdd(&sh[B == 1 ? id : (i / N) * K + id], 1);
+    const int pos = atomicAdd(&sh[id], 1);
     order[pos] = (int32_t)i;
   }
 }
@@ -311,14 +314,26 @@ __global__ void __launch_bounds__(256)
         if (!more) break;
       }
     }
-    while (p < lim) {
-      const int64_t r = p + sub;
-      if (r < lim) {
-        const T* rp = X + (int64_t)__ldg(order + r) * row_elems;
+    // tail of the segment (< RPW*U rows): same batched gathers, masked per row
+    if (p < lim) {
+      int32_t ri[U];
 #pragma unroll
-        for (int q = 0; q < VPL; ++q) VecCvt<T>::add(acc + q * E, ldg_stream(rp + (q * LPR + sl) * E));
+      for (int u = 0; u < U; ++u) {
+        const int64_t r = p + u * RPW + sub;
+        ri[u] = r < lim ? __ldg(order + r) : -1;
       }
-      p += RPW;
+      uint4 v[U][VPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const T* rp = X + (int64_t)(ri[u] < 0 ? 0 : ri[u]) * row_elems;
+#pragma unroll
+        for (int q = 0; q < VPL; ++q)
+          v[u][q] = ri[u] >= 0 ? ldg_stream(rp + (q * LPR + sl) * E) : make_uint4(0u, 0u, 0u, 0u);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < VPL; ++q) VecCvt<T>::add(acc + q * E, v[u][q]);
     }
     p = lim;
     // flush this segment's partial (one merge per segment)
@@ -454,19 +469,20 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   cudaError_t e;
   if ((e = cudaMemsetAsync(hist, 0, BK * 4, s)) != cudaSuccess) return e;
   if (!accumulate && (e = cudaMemsetAsync(sums, 0, BK * d * 8, s)) != cudaSuccess) return e;
-  // one block per SM-ish slice of points; 1024 threads so the shared histogram
-  // is built and drained quickly
-  int64_t blocks = (P + 8191) / 8192;
-  const int64_t cap = (int64_t)num_sms * 2;
-  if (blocks > cap) blocks = cap;
-  if (blocks < 1) blocks = 1;
-  const bool smem_keys = BK <= HIST_SMEM_KEYS;
-  const size_t hsm = smem_keys ? BK * 4 : 0;
-  k_hist<<<(unsigned)blocks, 1024, hsm, s>>>(ids, B, N, K, hist);
+  // blocks per batch element: ~2 waves of SMs in total, each block owning
+  // >= 2048 points so the shared histogram amortizes
+  int64_t bpb = ((int64_t)num_sms * 2 + B - 1) / B;
+  const int64_t max_bpb = (N + 2047) / 2048;
+  if (bpb > max_bpb) bpb = max_bpb;
+  if (bpb < 1) bpb = 1;
+  const unsigned blocks = (unsigned)(B * bpb);
+  const bool smem_keys = K <= HIST_SMEM_KEYS;
+  const size_t hsm = smem_keys ? K * 4 : 0;
+  k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist);
   k_scan<<<1, 1024, 0, s>>>(hist, B, N, K, chunk < 1 ? 1 : chunk, accumulate, off, cursor, counts,
                             merges);
   if (smem_keys)
-    k_scatter_block<<<(unsigned)blocks, 1024, hsm, s>>>(ids, B, N, K, cursor, order);
+    k_scatter_block<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, cursor, order);
   else
     k_scatter<<<(unsigned)((P + 511) / 512 < num_sms * 4 ? (P + 511) / 512 : num_sms * 4), 512, 0,
                 s>>>(ids, B, N, K, cursor, order);

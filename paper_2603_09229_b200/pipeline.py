@@ -103,6 +103,10 @@ class LloydEngine:
         self.obj = torch.empty((B,), dtype=torch.float64, device=dev)
         self.cur = 0
         self.it = 0
+        # CUDA graphs of one iteration, keyed by (assignment slot, centroid slot);
+        # only for the single-device CUDA path (the NCCL all-reduce stays eager)
+        self.use_graphs = backend is None and allreduce is None and self.x.is_cuda
+        self._graphs: dict = {}
 
     # -------------------------------------------------------------- state
     def set_centroids(self, c: torch.Tensor) -> None:
@@ -131,9 +135,31 @@ class LloydEngine:
 
         Writes: ids[slot] (this iteration's assignment), objective, the next
         master/operand into the other centroid slot, the changed flag and
-        max squared shift.  Returns the assignment slot used."""
+        max squared shift.  Returns the assignment slot used.  From the second
+        iteration on, the launch sequence is replayed from a CUDA graph (two
+        graphs alternate with the ping-pong buffers)."""
         slot = self.it & 1
-        compare = self.it > 0
+        if self.use_graphs and self.it > 0:
+            key = (slot, self.cur)
+            gr = self._graphs.get(key)
+            if gr is None:
+                gr = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gr):
+                    self._body(slot, True)
+                self._graphs[key] = gr
+            gr.replay()
+            if history_row is not None:
+                history_row.copy_(self.obj)
+            self.it += 1
+            return slot
+        self._body(slot, self.it > 0)
+        if history_row is not None:
+            history_row.copy_(self.obj)
+        self.it += 1
+        return slot
+
+    def _body(self, slot: int, compare: bool) -> None:
+        """The device work of one iteration (eager or under graph capture)."""
         self.changed.zero_()
         self.shift2.zero_()
         self.merges_it.zero_()
@@ -149,14 +175,10 @@ class LloydEngine:
             self.counts.copy_(self.counts_f)
             self.obj.copy_(self.obj_red)
             self.changed.copy_((self.changed_f[0] > 0).to(torch.int32))
-        if history_row is not None:
-            history_row.copy_(self.obj)
         nxt = self.cur ^ 1
         self.be.normalize(self.sums, self.counts, self.master[self.cur], out=self.master[nxt],
-                      operand_out=None if self.operand is self.master else self.operand[nxt],
-                      empty=self.empty, shift2=self.shift2)
-        self.it += 1
-        return slot
+                          operand_out=None if self.operand is self.master else self.operand[nxt],
+                          empty=self.empty, shift2=self.shift2)
 
     def poll(self):
         """(changed: bool, shift: float) -- the one device->host read per iteration."""
