@@ -120,10 +120,12 @@ __global__ void __launch_bounds__(1024)
       counts[k] = accumulate ? counts[k] + c : c;
       if (c > 0 && merges) {
         // reference merges: the run [s, e) of this key inside its batch element
-        // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks.
-        const int64_t b = k / K;
-        const int64_t s0 = run - b * N, e = s0 + c;
-        mg += (unsigned long long)((e - 1) / chunk - s0 / chunk + 1);
+        // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks
+        // (all quantities < 2^31: 32-bit divisions)
+        const uint32_t b = (uint32_t)k / (uint32_t)K;
+        const uint32_t s0 = (uint32_t)(run - (int64_t)b * N), e = s0 + (uint32_t)c;
+        const uint32_t ch = (uint32_t)chunk;
+        mg += (unsigned long long)((e - 1) / ch - s0 / ch + 1);
       }
     }
     carry += warp_tot[31];
@@ -479,8 +481,8 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   const bool smem_keys = K <= HIST_SMEM_KEYS;
   const size_t hsm = smem_keys ? K * 4 : 0;
   k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist);
-  k_scan<<<1, 1024, 0, s>>>(hist, B, N, K, chunk < 1 ? 1 : chunk, accumulate, off, cursor, counts,
-                            merges);
+  const int64_t ch = chunk < 1 ? 1 : (chunk > N ? N : chunk);
+  k_scan<<<1, 1024, 0, s>>>(hist, B, N, K, ch, accumulate, off, cursor, counts, merges);
   if (smem_keys)
     k_scatter_block<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, cursor, order);
   else
@@ -497,29 +499,38 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
 
 // ----------------------------------------------------------------- normalize
 template <typename TM, typename TO>
-__global__ void k_normalize(const double* __restrict__ sums, const int64_t* __restrict__ counts,
-                            const TM* prev, TM* out, TO* operand, uint8_t* empty,
-                            double* max_shift2, int64_t BK, int64_t d) {
+__global__ void __launch_bounds__(256)
+    k_normalize(const double* __restrict__ sums, const int64_t* __restrict__ counts,
+                const TM* prev, TM* out, TO* operand, uint8_t* empty, double* max_shift2,
+                int64_t BK, int64_t d) {
+  __shared__ double wmax[8];
   const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (row >= BK) return;
-  const int64_t cnt = counts[row];
   double sh = 0.0;
-  for (int64_t j = lane; j < d; j += 32) {
-    const int64_t o = row * d + j;
-    const TM old = prev[o];
-    TM nv = old;
-    if (cnt > 0) nv = (TM)(sums[o] / (double)cnt);
-    out[o] = nv;
-    if (operand) operand[o] = (TO)(float)nv;
-    const double df = (double)nv - (double)old;
-    sh += df * df;
+  if (row < BK) {
+    const int64_t cnt = counts[row];
+    for (int64_t j = lane; j < d; j += 32) {
+      const int64_t o = row * d + j;
+      const TM old = prev[o];
+      TM nv = old;
+      if (cnt > 0) nv = (TM)(sums[o] / (double)cnt);  // correctly rounded, as numpy
+      out[o] = nv;
+      if (operand) operand[o] = (TO)(float)nv;
+      const double df = (double)nv - (double)old;
+      sh += df * df;
+    }
+    if (lane == 0 && empty) empty[row] = cnt > 0 ? 0 : 1;
   }
-  if (lane == 0 && empty) empty[row] = cnt > 0 ? 0 : 1;
   if (max_shift2) {
     for (int o = 16; o; o >>= 1) sh += __shfl_xor_sync(0xffffffffu, sh, o);
-    if (lane == 0)
-      atomicMax((unsigned long long*)max_shift2, (unsigned long long)__double_as_longlong(sh));
+    if (lane == 0) wmax[threadIdx.x >> 5] = sh;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wmax[w]);
+      // non-negative doubles order like their bit patterns
+      atomicMax((unsigned long long*)max_shift2, (unsigned long long)__double_as_longlong(m));
+    }
   }
 }
 
