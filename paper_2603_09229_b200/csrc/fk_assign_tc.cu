@@ -433,6 +433,20 @@ FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, f
   best = p ? colbase : best;
 }
 
+// Debug (mode 5): min tree without the capture, to time the capture's share.
+FK_DEV void epi_chunk_nocapture(uint32_t (&v)[32], int colbase, float& M, int& best) {
+  const float* s = reinterpret_cast<const float*>(v);
+  float a[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) a[j] = fmin3(s[3 * j], s[3 * j + 1], s[3 * j + 2]);
+  a[10] = fminf(s[30], s[31]);
+  const float mc = fmin3(fmin3(a[0], a[1], a[2]), fmin3(a[3], a[4], a[5]),
+                         fmin3(fmin3(a[6], a[7], a[8]), a[9], a[10]));
+  const bool p = mc < M;
+  M = p ? mc : M;
+  best = p ? colbase : best;
+}
+
 // AUG = true : the ||c||^2 bias rides in the GEMM as one extra K=16 step
 //              (A_ext = ones, B_ext = 3-way bf16 split of ||c||^2/2, main
 //              MMAs negate A), so the epilogue is a pure min-reduction.
@@ -699,7 +713,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           }
         };
         auto chunk = [&](uint32_t (&v)[32], int ch) {
-          if (AUG)
+          if (AUG && p.debug_mode == 5)
+            epi_chunk_nocapture(v, col0 + 32 * ch, M, best);
+          else if (AUG)
             epi_chunk_aug(v, col0 + 32 * ch, M, best, bestv);
           else
             epi_chunk(v, cnp + 128 * ch, col0 + 32 * ch, M, best, bestv);
