@@ -50,7 +50,8 @@ __device__ __forceinline__ void range_of(int64_t N, int bpb, int64_t& b, int64_t
 }
 
 __global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, int64_t B, int64_t N,
-                                               int64_t K, int bpb, int32_t* __restrict__ hist) {
+                                               int64_t K, int bpb, int32_t* __restrict__ hist,
+                                               int32_t* __restrict__ table) {
   extern __shared__ int32_t sh[];
   const bool use_smem = K <= HIST_SMEM_KEYS;
   int64_t b, lo, hi;
@@ -74,8 +75,12 @@ __global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, 
   }
   if (use_smem) {
     __syncthreads();
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x)
-      if (sh[k]) atomicAdd(&hist[b * K + k], sh[k]);
+    int32_t* trow = table + (int64_t)blockIdx.x * K;  // this block's histogram, reused by the scatter
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+      const int32_t c = sh[k];
+      trow[k] = c;
+      if (c) atomicAdd(&hist[b * K + k], c);
+    }
   }
 }
 
@@ -149,21 +154,16 @@ __global__ void __launch_bounds__(1024)
 // shared-memory cursors -- no per-point global atomics, no dependency chains.
 __global__ void __launch_bounds__(1024)
     k_scatter_block(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K, int bpb,
-                    int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
+                    const int32_t* __restrict__ table, int32_t* __restrict__ cursor,
+                    int32_t* __restrict__ order) {
   extern __shared__ int32_t sh[];
   int64_t b, lo, hi;
   range_of(N, bpb, b, lo, hi);
-  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sh[k] = 0;
-  __syncthreads();
-#pragma unroll 4
-  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-    const int32_t id = __ldg(ids + i);
-    if (id < 0 || id >= K) continue;
-    atomicAdd(&sh[id], 1);
-  }
-  __syncthreads();
+  // this block's histogram (built by k_hist over the same point range):
+  // reserve one contiguous range per non-empty key
+  const int32_t* trow = table + (int64_t)blockIdx.x * K;
   for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
-    const int32_t c = sh[k];
+    const int32_t c = trow[k];
     sh[k] = c ? atomicAdd(&cursor[b * K + k], c) : 0;
   }
   __syncthreads();
@@ -410,10 +410,21 @@ __global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restr
   }
 }
 
+// Blocks per batch element for the histogram / scatter passes: ~2 waves in
+// total, each block owning >= 2048 points so the shared histogram amortizes.
+static int64_t update_bpb(int64_t B, int64_t N, int num_sms) {
+  int64_t bpb = ((int64_t)num_sms * 2 + B - 1) / B;
+  const int64_t max_bpb = (N + 2047) / 2048;
+  if (bpb > max_bpb) bpb = max_bpb;
+  return bpb < 1 ? 1 : bpb;
+}
+constexpr int kMaxSms = 256;  // workspace bound for any sm_100 part
+
 size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K) {
   const int64_t BK = B * K, P = B * N;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  return al(BK * 4) + al(BK * 4) + al((BK + 1) * 8) + al(P * 4);
+  const int64_t table = K <= HIST_SMEM_KEYS ? B * update_bpb(B, N, kMaxSms) * K : 0;
+  return al(BK * 4) + al(BK * 4) + al((BK + 1) * 8) + al(P * 4) + al(table * 4);
 }
 
 template <typename T, typename A>
@@ -468,23 +479,20 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   int64_t* off = (int64_t*)w;
   w += al((BK + 1) * 8);
   int32_t* order = (int32_t*)w;
+  w += al(P * 4);
+  int32_t* table = (int32_t*)w;  // per-block histograms (shared-histogram path)
   cudaError_t e;
   if ((e = cudaMemsetAsync(hist, 0, BK * 4, s)) != cudaSuccess) return e;
   if (!accumulate && (e = cudaMemsetAsync(sums, 0, BK * d * 8, s)) != cudaSuccess) return e;
-  // blocks per batch element: ~2 waves of SMs in total, each block owning
-  // >= 2048 points so the shared histogram amortizes
-  int64_t bpb = ((int64_t)num_sms * 2 + B - 1) / B;
-  const int64_t max_bpb = (N + 2047) / 2048;
-  if (bpb > max_bpb) bpb = max_bpb;
-  if (bpb < 1) bpb = 1;
+  const int64_t bpb = update_bpb(B, N, num_sms < kMaxSms ? num_sms : kMaxSms);
   const unsigned blocks = (unsigned)(B * bpb);
   const bool smem_keys = K <= HIST_SMEM_KEYS;
   const size_t hsm = smem_keys ? K * 4 : 0;
-  k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist);
+  k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist, table);
   const int64_t ch = chunk < 1 ? 1 : (chunk > N ? N : chunk);
   k_scan<<<1, 1024, 0, s>>>(hist, B, N, K, ch, accumulate, off, cursor, counts, merges);
   if (smem_keys)
-    k_scatter_block<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, cursor, order);
+    k_scatter_block<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, table, cursor, order);
   else
     k_scatter<<<(unsigned)((P + 511) / 512 < num_sms * 4 ? (P + 511) / 512 : num_sms * 4), 512, 0,
                 s>>>(ids, B, N, K, cursor, order);
