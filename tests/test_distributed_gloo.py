@@ -51,7 +51,21 @@ def test_sharded_lloyd_matches_single_process(oracle, prec):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q, prec)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda t: t[0])
+    res = []
+    import queue as _queue
+    import time as _time
+    deadline = _time.time() + 240
+    while len(res) < world and _time.time() < deadline:
+        try:
+            res.append(q.get(timeout=2))
+        except _queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+    for p in procs:
+        if p.exitcode is None and len(res) < world:
+            p.terminate()
+    assert len(res) == world, "a rank failed"
+    res = sorted(res, key=lambda t: t[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
