@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libflashkmeans.so")
+LIB_PATH = os.environ.get("FK_LIB_PATH") or os.path.join(_HERE, "_lib", "libflashkmeans.so")
 
 FK_OK, FK_EINVAL, FK_EUNSUPPORTED, FK_ECUDA, FK_EWORKSPACE = range(5)
 FK_F32, FK_BF16, FK_F16, FK_F64 = range(4)

@@ -433,26 +433,12 @@ FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, f
   best = p ? colbase : best;
 }
 
-// Debug (mode 5): min tree without the capture, to time the capture's share.
-FK_DEV void epi_chunk_nocapture(uint32_t (&v)[32], int colbase, float& M, int& best) {
-  const float* s = reinterpret_cast<const float*>(v);
-  float a[11];
-#pragma unroll
-  for (int j = 0; j < 10; ++j) a[j] = fmin3(s[3 * j], s[3 * j + 1], s[3 * j + 2]);
-  a[10] = fminf(s[30], s[31]);
-  const float mc = fmin3(fmin3(a[0], a[1], a[2]), fmin3(a[3], a[4], a[5]),
-                         fmin3(fmin3(a[6], a[7], a[8]), a[9], a[10]));
-  const bool p = mc < M;
-  M = p ? mc : M;
-  best = p ? colbase : best;
-}
-
 // AUG = true : the ||c||^2 bias rides in the GEMM as one extra K=16 step
 //              (A_ext = ones, B_ext = 3-way bf16 split of ||c||^2/2, main
 //              MMAs negate A), so the epilogue is a pure min-reduction.
 // AUG = false: bias applied in the epilogue from a smem ring (fp16 data,
 //              whose range cannot hold ||c||^2 safely).
-template <int FMT, bool AUG>
+template <int FMT, bool AUG, bool ALT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     fk_assign_tc2_kernel(const __grid_constant__ CUtensorMap tmx,
                          const __grid_constant__ CUtensorMap tmc,
@@ -493,12 +479,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   const int npairs = gridDim.x >> 1;
   // X row-tile ring: the 64 KB A region holds 2 slots of 2 K-atoms (d <= 128)
   // or 4 slots of 1 atom (d <= 64): deeper prefetch when a row tile is short.
-  const int a_slots = p.katoms == 1 ? 4 : 2;
+  const int a_log = p.katoms == 1 ? 2 : 1;  // 4 or 2 slots (power of two)
+  const int a_slots = 1 << a_log;
   const int a_slot_bytes = p.katoms * A_ATOM;
-  // Single-column-tile rows (K <= 256): the two epilogue warpgroups take
+  // ALT (single-column-tile rows, K <= 256): the two epilogue warpgroups take
   // alternate tiles (whole rows each, two tiles in flight, no merge) instead
   // of splitting every tile's columns.
-  const bool alt = p.ncol == 1;
+  constexpr bool alt = ALT;
   const int epi_warps_per_buf = alt ? 4 : 8;
 
   if (warp == W_PRODUCER && lane == 0) {
@@ -548,10 +535,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       uint32_t stage = 0, sphase = 0;
       const uint32_t a_bytes = p.katoms * A_ATOM;
       auto load_a = [&](int t, int j) {
-        const int slot = j % a_slots;
+        const int slot = j & (a_slots - 1);
         const int b = t / p.tiles_per_batch;
         const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
-        mbar_wait(&a_empty[slot], ((j / a_slots) & 1) ^ 1);
+        mbar_wait(&a_empty[slot], ((j >> a_log) & 1) ^ 1);
         if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
         const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
         for (int ka = 0; ka < p.katoms; ++ka)
@@ -609,8 +596,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       uint32_t stage = 0, sphase = 0, g = 0;
       int i = 0;
       for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
-        const int slot = i % a_slots;
-        mbar_wait(&a_full[slot], (i / a_slots) & 1);
+        const int slot = i & (a_slots - 1);
+        mbar_wait(&a_full[slot], (i >> a_log) & 1);
         tc_fence_after();
         const uint32_t a_base = smem_u32(sA + slot * a_slot_bytes);
         for (int c = 0; c < p.ncol; ++c, ++g) {
@@ -663,7 +650,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     const int wg = warp >> 2;        // column half of every tile (alt: tile parity)
     const int q = warp & 3;          // TMEM lane quarter
     const int row = q * 32 + lane;
-    const int ncols = alt ? BN : BN / 2;  // columns this warp reads per tile
     uint32_t g = 0;
     int i = 0;
     for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
@@ -673,7 +659,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       }
       const int b = t / p.tiles_per_batch;
       const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
-      const int slot = i % a_slots;
+      const int slot = i & (a_slots - 1);
       float M = __int_as_float(0x7f800000);
       int best = -1;
       float bestv[32];
@@ -713,9 +699,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           }
         };
         auto chunk = [&](uint32_t (&v)[32], int ch) {
-          if (AUG && p.debug_mode == 5)
-            epi_chunk_nocapture(v, col0 + 32 * ch, M, best);
-          else if (AUG)
+          if (AUG)
             epi_chunk_aug(v, col0 + 32 * ch, M, best, bestv);
           else
             epi_chunk(v, cnp + 128 * ch, col0 + 32 * ch, M, best, bestv);
@@ -727,7 +711,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           M = fminf(M, __uint_as_float(va[0]));
           continue;
         }
-        const int nch = ncols / 32;  // 4 (column split) or 8 (alternate tiles)
+        constexpr int nch = ALT ? 8 : 4;  // 32-column chunks this warp reads per tile
+#pragma unroll
         for (int ch = 0; ch < nch; ch += 2) {
           FK_TMEM_WAIT_LD(va);
           FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 1), vb);
@@ -791,6 +776,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   }
 }
 
+template <int FMT, bool AUG, bool ALT>
+static cudaError_t launch_pair_t(const CUtensorMap& tmx, const CUtensorMap& tmc,
+                                 const CUtensorMap& tmext, TcArgs a, int pairs,
+                                 cudaStream_t stream) {
+  static int attr_dev_mask = 0;  // one-time per device (keeps graph capture free of it)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!(attr_dev_mask & (1 << (dev & 31)))) {
+    cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, AUG, ALT>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES);
+    attr_dev_mask |= 1 << (dev & 31);
+  }
+  fk_assign_tc2_kernel<FMT, AUG, ALT><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(
+      tmx, tmc, tmext, a);
+  return cudaGetLastError();
+}
+
 template <int FMT, bool AUG>
 static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
                                const CUtensorMap& tmext, TcArgs a, int num_sms,
@@ -801,17 +803,8 @@ static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
   int pairs = num_sms / 2;
   if (a.total_tiles < pairs) pairs = a.total_tiles;
   if (pairs <= 0) return cudaSuccess;
-  static int attr_dev_mask = 0;  // one-time per device (keeps graph capture free of it)
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!(attr_dev_mask & (1 << (dev & 31)))) {
-    cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, AUG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         tc2::SMEM_BYTES);
-    attr_dev_mask |= 1 << (dev & 31);
-  }
-  fk_assign_tc2_kernel<FMT, AUG><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(tmx, tmc,
-                                                                                      tmext, a);
-  return cudaGetLastError();
+  return a.ncol == 1 ? launch_pair_t<FMT, AUG, true>(tmx, tmc, tmext, a, pairs, stream)
+                     : launch_pair_t<FMT, AUG, false>(tmx, tmc, tmext, a, pairs, stream);
 }
 
 // ---------------------------------------------------------------- host side
