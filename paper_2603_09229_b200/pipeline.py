@@ -13,12 +13,18 @@ centroid shift falls to shift_tol, or at max_iters.  B200 design:
 * ``_streaming_pass`` streams pinned host chunks over a dedicated copy stream
   into two device buffers (event-gated ping-pong), overlapping H2D of chunk
   t+1 with assign+update of chunk t, accumulating statistics on the device
-  and normalizing once per pass (pipeline.py:312-373).
+  and normalizing once per pass (pipeline.py:312-373).  Sources are either a
+  host-resident array (``HostStream``, pinned once) or an FKM1 file
+  (``ChunkStream``, pipeline.py:150-234): a reader thread ``readinto``s chunk
+  t+2 into one of two pinned staging buffers while chunk t+1 is copied and
+  chunk t computed.
 """
 
 from __future__ import annotations
 
 import math
+import threading
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -32,8 +38,8 @@ from .core import (INIT_METHODS, LOW_PRECISION, Assignments, Centroids, ClusterS
 from .flash_assign import TilingConfig
 from .tuner import CacheModel, ProblemShape, heuristic_config
 
-__all__ = ["LloydEngine", "HostStream", "PartialStats", "DeviceAssignmentStore", "lloyd_run",
-           "out_of_core_iteration", "chunked_stream_run", "ENGINES"]
+__all__ = ["LloydEngine", "HostStream", "ChunkStream", "PartialStats", "DeviceAssignmentStore",
+           "lloyd_run", "out_of_core_iteration", "chunked_stream_run", "ENGINES"]
 
 ENGINES = ("flash", "baseline")
 
@@ -346,6 +352,95 @@ class HostStream:
         self.close()
 
 
+class ChunkStream:
+    """Chunk-granular reader over an FKM1 file that never loads it whole
+    (pipeline.py:150-234): rows land directly in caller buffers (``readinto``;
+    pinned staging buffers in the streaming pass), one read at a time under a
+    lock.  Same surface as the reference: batch, total_points, dims,
+    precision, elem_bytes, chunk_points, n_chunks, bounds, read_rows_into,
+    read_rows, close."""
+
+    def __init__(self, path: str, chunk_points: int):
+        from .fileio import read_fkm1_header
+
+        if int(chunk_points) < 1:
+            raise ValueError("chunk_points must be >= 1")
+        h = read_fkm1_header(path)
+        self.path = path
+        self.batch, self.total_points, self.dims = h.batch, h.points, h.dims
+        self.precision = h.precision
+        self.elem_bytes = h.elem_bytes
+        self._dtype = h.dtype
+        self.chunk_points = min(int(chunk_points), h.points)
+        self._row_bytes = self.dims * self.elem_bytes
+        self._f = None
+        self._lock = threading.Lock()
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return self._dtype
+
+    @property
+    def n_chunks(self) -> int:
+        return -(-self.total_points // self.chunk_points)
+
+    def bounds(self, t: int) -> tuple[int, int]:
+        if not 0 <= t < self.n_chunks:
+            raise ValueError(f"chunk index {t} out of range")
+        lo = t * self.chunk_points
+        return lo, min(self.total_points, lo + self.chunk_points)
+
+    def _handle(self):
+        if self._f is None:
+            self._f = open(self.path, "rb", buffering=0)
+        return self._f
+
+    def read_rows_into(self, b: int, lo: int, hi: int, out):
+        """Rows [lo, hi) of batch element b into ``out`` (a host tensor or numpy
+        array of shape (>= rows, dims) and the stream's dtype); returns the view."""
+        from .fileio import host_bytes_view
+
+        rows = hi - lo
+        if not 0 <= b < self.batch or not 0 <= lo < hi <= self.total_points:
+            raise ValueError("row range outside the stream bounds")
+        t = torch.from_numpy(out) if isinstance(out, np.ndarray) else out
+        if t.dim() != 2 or t.shape[0] < rows or t.shape[1] != self.dims:
+            raise ValueError("destination buffer is too small for the requested rows")
+        if t.dtype != self._dtype or not t.is_contiguous() or t.is_cuda:
+            raise ValueError("destination buffer must be host memory of the stream dtype, row-major")
+        view = t[:rows]
+        mv = host_bytes_view(view)
+        nbytes = rows * self._row_bytes
+        from .fileio import FKM1_HEADER_BYTES
+
+        with self._lock:
+            f = self._handle()
+            f.seek(FKM1_HEADER_BYTES + (b * self.total_points + lo) * self._row_bytes)
+            got = 0
+            while got < nbytes:  # raw readinto may return partial counts
+                n = f.readinto(mv[got:])
+                if not n:
+                    break
+                got += n
+        if got != nbytes:
+            raise DataFormatError(f"short read: wanted {nbytes} bytes, got {got}")
+        return out[:rows] if isinstance(out, np.ndarray) else view
+
+    def read_rows(self, b: int, lo: int, hi: int) -> torch.Tensor:
+        return self.read_rows_into(b, lo, hi, torch.empty((hi - lo, self.dims), dtype=self._dtype))
+
+    def close(self) -> None:
+        if self._f is not None:
+            self._f.close()
+            self._f = None
+
+    def __enter__(self) -> "ChunkStream":
+        return self
+
+    def __exit__(self, *exc) -> None:
+        self.close()
+
+
 @dataclass
 class PartialStats:
     """One chunk's cluster sums/counts; combined in ascending chunk order (pipeline.py:237-258)."""
@@ -403,10 +498,20 @@ class DeviceAssignmentStore:
 class _StreamState:
     """Device buffers and streams for the chunk pipeline of one stream shape."""
 
-    def __init__(self, stream: HostStream, clusters: int, device):
+    def __init__(self, stream, clusters: int, device, keep_mind: bool = False):
         self.dev = device
         cp, d = stream.chunk_points, stream.dims
         self.buf = [torch.empty((1, cp, d), dtype=stream.dtype, device=device) for _ in range(2)]
+        # file-backed sources: two pinned staging buffers filled by a reader thread
+        self.staged = not isinstance(stream, HostStream)
+        if self.staged:
+            self.stage = [torch.empty((cp, d), dtype=stream.dtype, pin_memory=True) for _ in range(2)]
+            self.copied = [torch.cuda.Event() for _ in range(2)]
+            self.reader = ThreadPoolExecutor(max_workers=1)
+        # reseed_farthest needs every point's assigned distance of the pass
+        self.mind_all = (torch.empty((stream.batch, stream.total_points), dtype=torch.float32
+                                     if stream.dtype in LOW_PRECISION else stream.dtype, device=device)
+                         if keep_mind else None)
         self.mind = torch.empty((1, cp), dtype=torch.float32 if stream.dtype in LOW_PRECISION
                                 else stream.dtype, device=device)
         self.copy_stream = torch.cuda.Stream(device=device)
@@ -420,7 +525,7 @@ class _StreamState:
         self.merges = torch.zeros((), dtype=torch.int64, device=device)
 
 
-def _streaming_pass(stream: HostStream, master: torch.Tensor, operand: torch.Tensor, clusters: int,
+def _streaming_pass(stream, master: torch.Tensor, operand: torch.Tensor, clusters: int,
                     chunk: int, counters: Counters, store: DeviceAssignmentStore, st: _StreamState,
                     new_master: torch.Tensor, new_operand: torch.Tensor | None,
                     shift2: torch.Tensor, empty: torch.Tensor, allreduce=None):
@@ -436,23 +541,47 @@ def _streaming_pass(stream: HostStream, master: torch.Tensor, operand: torch.Ten
     store.begin_pass()
     compute = torch.cuda.current_stream(st.dev)
     tasks = [(b, t) for b in range(stream.batch) for t in range(stream.n_chunks)]
+    reads = {}
+
+    def submit_read(i):  # reader thread: wait until staging buffer i&1 was copied out
+        b, t = tasks[i]
+        lo, hi = stream.bounds(t)
+        k = i & 1
+        ev = st.copied[k] if i >= 2 else None
+
+        def job():
+            if ev is not None:
+                ev.synchronize()
+            stream.read_rows_into(b, lo, hi, st.stage[k])
+
+        reads[i] = st.reader.submit(job)
 
     def issue_copy(i):
         b, t = tasks[i]
         lo, hi = stream.bounds(t)
         k = i & 1
+        if st.staged:
+            reads.pop(i).result()
+            src = st.stage[k][: hi - lo]
+        else:
+            src = stream.view(b, lo, hi)
         with torch.cuda.stream(st.copy_stream):
             st.copy_stream.wait_event(st.free[k])
-            st.buf[k][0, : hi - lo].copy_(stream.view(b, lo, hi), non_blocking=True)
+            st.buf[k][0, : hi - lo].copy_(src, non_blocking=True)
             st.ready[k].record(st.copy_stream)
+            if st.staged:
+                st.copied[k].record(st.copy_stream)
+        if st.staged and i + 2 < len(tasks):
+            submit_read(i + 2)
 
     for k in range(2):  # both buffers start free
         st.free[k].record(compute)
+    if st.staged:
+        for i in range(min(2, len(tasks))):
+            submit_read(i)
     if tasks:
         issue_copy(0)
     for i, (b, t) in enumerate(tasks):
-        if i + 1 < len(tasks):
-            issue_copy(i + 1)
         lo, hi = stream.bounds(t)
         rows = hi - lo
         k = i & 1
@@ -460,14 +589,17 @@ def _streaming_pass(stream: HostStream, master: torch.Tensor, operand: torch.Ten
         xb = st.buf[k][:, :rows]
         ids_new = store.new[b: b + 1, lo:hi]   # contiguous: one row segment of (B, N)
         ids_old = store.old[b: b + 1, lo:hi]
+        mind = st.mind[:, :rows] if st.mind_all is None else st.mind_all[b: b + 1, lo:hi]
         ops.assign(xb, operand[b: b + 1], idx_prev=ids_old, changed=store.changed,
-                   idx_out=ids_new, mind_out=st.mind[:, :rows])
-        ops.objective(st.mind[:, :rows], out=st.obj_chunk)
+                   idx_out=ids_new, mind_out=mind)
+        ops.objective(mind, out=st.obj_chunk)
         st.obj[b: b + 1] += st.obj_chunk
         ops.update(xb, ids_new, clusters, chunk, accumulate=True, sums=st.sums[b: b + 1],
                    counts=st.counts[b: b + 1], merges=st.merges)
         st.free[k].record(compute)
         counters.elements_streamed += rows
+        if i + 1 < len(tasks):  # host may block on the file read while chunk i computes
+            issue_copy(i + 1)
     if allreduce is not None:
         red = torch.cat([st.sums.reshape(-1), st.counts.reshape(-1).double(), st.obj,
                          store.changed.reshape(1).double()])
@@ -479,28 +611,98 @@ def _streaming_pass(stream: HostStream, master: torch.Tensor, operand: torch.Ten
         store.changed.copy_((red[-1] > 0).to(torch.int32))
     ops.normalize(st.sums, st.counts, master, out=new_master, operand_out=new_operand, empty=empty,
                   shift2=shift2)
+    if st.mind_all is not None:
+        _reseed_from_stream(stream, st, master, new_master, new_operand, empty, shift2)
 
 
-def _init_from_stream(stream: HostStream, clusters: int, seed: int, method: str) -> torch.Tensor:
-    """Same row draws as the in-core initializer (pipeline.py:456-479)."""
+def _reseed_from_stream(stream, st: _StreamState, master, new_master, new_operand, empty, shift2):
+    """reseed_farthest for a streamed pass (pipeline.py:283-309, 366-371): each
+    empty cluster takes the next-farthest point of the pass (distance desc,
+    index asc), read back from the source; the shift is recomputed."""
+    em = empty.cpu().numpy()
+    if not em.any():
+        return
+    for b in range(stream.batch):
+        empties = np.flatnonzero(em[b])
+        if empties.size == 0:
+            continue
+        order = torch.sort(-st.mind_all[b].double(), stable=True).indices[: empties.size].cpu()
+        rows = torch.stack([stream.read_rows(b, int(r), int(r) + 1)[0] for r in order])
+        cid = torch.from_numpy(empties).to(st.dev)
+        rows = rows.to(st.dev)
+        new_master[b, cid] = rows.to(new_master.dtype)
+        if new_operand is not None:
+            new_operand[b, cid] = rows
+    diff = new_master.double() - master.double()
+    shift2.copy_((diff * diff).sum(-1).max())
+
+
+def _init_from_stream(stream, clusters: int, seed: int, method: str) -> torch.Tensor:
+    """Same row draws as the in-core initializer (pipeline.py:456-479); a
+    file-backed source reads only the chosen rows (plus, for k-means++, the
+    D^2 sweeps of pipeline.py:420-453)."""
     if method not in INIT_METHODS:
         raise ValueError(f"init method must be one of {INIT_METHODS}")
     if clusters > stream.total_points:
         raise ValueError(f"cannot place {clusters} clusters with only {stream.total_points} points")
-    idx = init_indices(stream.total_points, clusters, seed, stream.batch, method,
-                       stream.host if method == "kmeanspp" else None)
-    out = torch.stack([stream.host[b][torch.from_numpy(idx[b])] for b in range(stream.batch)])
-    return out.contiguous()
+    if isinstance(stream, HostStream):
+        idx = init_indices(stream.total_points, clusters, seed, stream.batch, method,
+                           stream.host if method == "kmeanspp" else None)
+        out = torch.stack([stream.host[b][torch.from_numpy(idx[b])] for b in range(stream.batch)])
+        return out.contiguous()
+    out = torch.empty((stream.batch, clusters, stream.dims), dtype=stream.dtype)
+    for b in range(stream.batch):
+        rng = np.random.default_rng((seed, b))
+        if method == "random_distinct":
+            idx = rng.choice(stream.total_points, size=clusters, replace=False)
+        else:
+            idx = _streaming_kmeanspp(stream, b, clusters, rng)
+        for j, i in enumerate(idx):
+            out[b, j] = stream.read_rows(b, int(i), int(i) + 1)[0]
+    return out
+
+
+def _streaming_kmeanspp(stream, b: int, k: int, rng: np.random.Generator) -> np.ndarray:
+    """k-means++ over a file stream with only an (N,) float64 weight table
+    resident; the D^2 arithmetic and RNG draws are those of the in-core seeding
+    (core.py:342-357), so the chosen rows match it bitwise."""
+    n = stream.total_points
+    idx = np.empty(k, np.int64)
+    idx[0] = rng.integers(n)
+    min_d2 = np.empty(n, np.float64)
+    buf = torch.empty((stream.chunk_points, stream.dims), dtype=stream.dtype)
+
+    def sweep(center: torch.Tensor, first: bool) -> None:
+        c64 = center.double().numpy()
+        for t in range(stream.n_chunks):
+            lo, hi = stream.bounds(t)
+            v = stream.read_rows_into(b, lo, hi, buf).double().numpy()
+            d2 = np.square(v - c64).sum(axis=1)
+            if first:
+                min_d2[lo:hi] = d2
+            else:
+                np.minimum(min_d2[lo:hi], d2, out=min_d2[lo:hi])
+
+    sweep(stream.read_rows(b, int(idx[0]), int(idx[0]) + 1)[0], True)
+    for j in range(1, k):
+        total = float(min_d2.sum())
+        choice = int(rng.choice(n, p=min_d2 / total)) if total > 0.0 else int(rng.integers(n))
+        idx[j] = choice
+        sweep(stream.read_rows(b, choice, choice + 1)[0], False)
+    return idx
 
 
 class _StreamRunner:
-    def __init__(self, stream: HostStream, clusters: int, device, chunk: int, allreduce=None):
+    def __init__(self, stream, clusters: int, device, chunk: int, allreduce=None,
+                 policy: str = "keep"):
+        if policy == "reseed_farthest" and allreduce is not None:
+            raise NotImplementedError("reseed_farthest with sharded streaming needs a global top-k")
         self.allreduce = allreduce
         self.stream = stream
         self.K = clusters
         self.chunk = chunk
         self.dev = device
-        self.st = _StreamState(stream, clusters, device)
+        self.st = _StreamState(stream, clusters, device, keep_mind=policy == "reseed_farthest")
         B, K, d = stream.batch, clusters, stream.dims
         self.mdt = master_dtype(stream.dtype)
         self.master = [torch.empty((B, K, d), dtype=self.mdt, device=device) for _ in range(2)]
@@ -527,37 +729,71 @@ class _StreamRunner:
         return bool(v[0] != 0), math.sqrt(float(v[1]))
 
 
-def out_of_core_iteration(stream: HostStream, c: Centroids, cfg: KMeansConfig, counters: Counters,
-                          store=None, workers: int | None = None, device=None):
-    """One streaming Lloyd iteration (pipeline.py:385-417): returns (new centroids,
-    assignment store, counters)."""
+def _check_stream_centroids(stream, c: Centroids, clusters: int) -> None:
     if c.batch != stream.batch or c.dims != stream.dims:
         raise ValueError("centroids do not match the stream shape")
-    if c.clusters != cfg.clusters:
+    if c.clusters != clusters:
         raise ValueError("centroid count does not match the configuration")
+    if c.precision != stream.precision:
+        raise ValueError("centroid precision does not match the stream")
+
+
+def out_of_core_iteration(stream, c: Centroids, cfg: KMeansConfig, counters: Counters,
+                          store=None, workers: int | None = None, device=None):
+    """One streaming Lloyd iteration (pipeline.py:385-417): returns (new
+    centroids, assignment store, counters); the caller finalizes (or aborts)
+    the store.  For an FKM1 ``ChunkStream`` a fresh store is the FKA1
+    ``AssignmentStore`` at "<dataset>.fka1" (as in the reference); a
+    host-array stream keeps its ids in a ``DeviceAssignmentStore``."""
+    from .fileio import AssignmentStore
+
+    _check_stream_centroids(stream, c, cfg.clusters)
     dev = device or device_of(c.data)
+    if dev.type != "cuda":
+        dev = torch.device("cuda", torch.cuda.current_device())
     tiling = _resolve_tiling(cfg, stream.total_points, stream.dims, stream.batch, stream.elem_bytes,
                              _workers(workers))
-    run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk)
-    if store is not None:
-        run.store = store
-    run.set(c.data)
-    run.one_pass(counters)
+    own_store = store is None
+    if store is None and getattr(stream, "path", None):
+        store = AssignmentStore(stream.path + ".fka1", stream.batch, stream.total_points)
+    try:
+        run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk,
+                            policy=cfg.empty_cluster_policy)
+        if isinstance(store, DeviceAssignmentStore):
+            run.store = store
+        run.set(c.data)
+        run.one_pass(counters)
+        if isinstance(store, AssignmentStore):
+            ids = run.store.new.cpu()
+            for b in range(stream.batch):
+                store.write_chunk(b, 0, ids[b])
+    except BaseException:
+        if own_store and isinstance(store, AssignmentStore):
+            store.abort()
+        raise
     counters.synchronized_merges += int(run.st.merges.item())
-    return Centroids(run.master[run.cur ^ 1].clone(), check_finite=False), run.store, counters
+    return (Centroids(run.master[run.cur ^ 1].clone(), check_finite=False),
+            store if store is not None else run.store, counters)
 
 
-def chunked_stream_run(stream: HostStream, cfg: KMeansConfig, assign_path: str | None = None,
+def chunked_stream_run(stream, cfg: KMeansConfig, assign_path: str | None = None,
                        workers: int | None = None, counters: Counters | None = None,
                        device=None) -> KMeansResult:
-    """Full out-of-core run (pipeline.py:482-530) with the in-core run's decisions."""
+    """Full out-of-core run (pipeline.py:482-530) with the in-core run's decisions.
+
+    The final assignments are written as an FKA1 file (atomically) to
+    ``assign_path``, default "<dataset>.fka1" for an FKM1 stream; a host-array
+    stream without ``assign_path`` keeps them in memory only."""
+    from .fileio import write_fka1
+
     counters = counters if counters is not None else Counters()
     if cfg.clusters > stream.total_points:
         raise ValueError("more clusters than points in the stream")
     dev = device or torch.device("cuda", torch.cuda.current_device())
     tiling = _resolve_tiling(cfg, stream.total_points, stream.dims, stream.batch, stream.elem_bytes,
                              _workers(workers))
-    run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk)
+    run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk,
+                        policy=cfg.empty_cluster_policy)
     run.set(_init_from_stream(stream, cfg.clusters, cfg.seed, cfg.init))
     history = []
     iterations = 0
@@ -571,5 +807,9 @@ def chunked_stream_run(stream: HostStream, cfg: KMeansConfig, assign_path: str |
         if shift <= cfg.shift_tol:
             break
     counters.synchronized_merges += int(run.st.merges.item())
-    return KMeansResult(Centroids(run.master[run.cur].clone(), check_finite=False),
-                        run.store.read_all(), np.array(history), iterations, counters)
+    a = run.store.read_all()
+    path = assign_path or (stream.path + ".fka1" if getattr(stream, "path", None) else None)
+    if path:
+        write_fka1(path, a)
+    return KMeansResult(Centroids(run.master[run.cur].clone(), check_finite=False), a,
+                        np.array(history), iterations, counters)
