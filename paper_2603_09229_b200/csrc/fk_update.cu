@@ -85,23 +85,34 @@ __global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, 
 }
 
 // ----------------------------------------------------------------- scan
-// One block of 1024 threads walks the keys in coalesced tiles of 1024:
-// block-wide exclusive scan per tile plus a running carry.  Also produces the
-// int64 counts and the reference's synchronized_merges count.
+// One block of 1024 threads per batch element b.  The block first reduces the
+// histogram of all earlier batch elements (its base offset; b*N when every id
+// is valid), then walks its own K keys in coalesced tiles of 1024: block-wide
+// exclusive scan per tile plus a running carry.  Also produces the int64
+// counts and the reference's synchronized_merges count.
 __global__ void __launch_bounds__(1024)
     k_scan(const int32_t* __restrict__ hist, int64_t B, int64_t N, int64_t K, int64_t chunk,
            int accumulate, int64_t* __restrict__ off, int32_t* __restrict__ cursor,
            int64_t* __restrict__ counts, int64_t* __restrict__ merges) {
   __shared__ int64_t warp_tot[32];
   __shared__ unsigned long long warp_mg[32];
-  const int64_t BK = B * K;
+  const int64_t b = blockIdx.x;
   const int t = threadIdx.x;
   const int lane = t & 31, w = t >> 5;
+  int64_t part = 0;
+  for (int64_t i = t; i < b * K; i += 1024) part += hist[i];
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) warp_tot[w] = part;
+  __syncthreads();
   int64_t carry = 0;
+  for (int i = 0; i < 32; ++i) carry += warp_tot[i];
+  __syncthreads();
   unsigned long long mg = 0;
-  for (int64_t base = 0; base < BK; base += 1024) {
-    const int64_t k = base + t;
-    const int64_t c = k < BK ? hist[k] : 0;
+  const uint32_t ch = (uint32_t)chunk;
+  for (int64_t base = 0; base < K; base += 1024) {
+    const int64_t kk = base + t;
+    const int64_t k = b * K + kk;
+    const int64_t c = kk < K ? hist[k] : 0;
     int64_t v = c;
     for (int o = 1; o < 32; o <<= 1) {
       const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
@@ -119,7 +130,7 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
     const int64_t run = carry + v - c + (w > 0 ? warp_tot[w - 1] : 0);  // exclusive prefix
-    if (k < BK) {
+    if (kk < K) {
       off[k] = run;
       cursor[k] = (int32_t)run;
       counts[k] = accumulate ? counts[k] + c : c;
@@ -127,16 +138,14 @@ __global__ void __launch_bounds__(1024)
         // reference merges: the run [s, e) of this key inside its batch element
         // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks
         // (all quantities < 2^31: 32-bit divisions)
-        const uint32_t b = (uint32_t)k / (uint32_t)K;
-        const uint32_t s0 = (uint32_t)(run - (int64_t)b * N), e = s0 + (uint32_t)c;
-        const uint32_t ch = (uint32_t)chunk;
+        const uint32_t s0 = (uint32_t)(run - b * N), e = s0 + (uint32_t)c;
         mg += (unsigned long long)((e - 1) / ch - s0 / ch + 1);
       }
     }
     carry += warp_tot[31];
     __syncthreads();
   }
-  if (t == 0) off[BK] = carry;
+  if (b == B - 1 && t == 0) off[B * K] = carry;
   for (int o = 16; o; o >>= 1) mg += __shfl_xor_sync(0xffffffffu, mg, o);
   if (lane == 0) warp_mg[w] = mg;
   __syncthreads();
@@ -490,7 +499,7 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   const size_t hsm = smem_keys ? K * 4 : 0;
   k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist, table);
   const int64_t ch = chunk < 1 ? 1 : (chunk > N ? N : chunk);
-  k_scan<<<1, 1024, 0, s>>>(hist, B, N, K, ch, accumulate, off, cursor, counts, merges);
+  k_scan<<<(unsigned)B, 1024, 0, s>>>(hist, B, N, K, ch, accumulate, off, cursor, counts, merges);
   if (smem_keys)
     k_scatter_block<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, table, cursor, order);
   else

@@ -140,4 +140,4 @@ def flash_assign(x: DataMatrix, c: Centroids, tiling: TilingConfig, counters: Co
     xd = to_device(x.data, dev)
     cd = to_device(c.data, dev)
     ids, mind = ops.assign(xd, cd)
-    return Assignments(ids, validate=False), mind, counters
+    return Assignments(ids, validate=False, id_bound=c.clusters), mind, counters
