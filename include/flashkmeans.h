@@ -141,6 +141,49 @@ FK_API fk_status fk_objective(fk_dtype mind_dt, const void* mind, int64_t B, int
 FK_API fk_status fk_scatter(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
                      int64_t K, int64_t d, double* sums, int64_t* counts, void* stream);
 
+/* ------------------------------------------------------------- k-means++
+ * D^2 seeding of init_centroids(method="kmeanspp") on the device:
+ *   fk_kmeanspp        <- _kmeanspp_indices      core.py:342-357
+ *   fk_kmeanspp_sweep  <- the per-chunk sweep of _streaming_kmeanspp
+ *                         (pipeline.py:435-443)
+ *   fk_kmeanspp_select <- total = min_d2.sum(); rng.choice(n, p=min_d2/total)
+ *                         (core.py:350-353, pipeline.py:446-450)
+ * The chosen indices equal the reference's for the same data and draws, bit for
+ * bit: distances and `total` follow numpy's pairwise summation order in f64,
+ * and choice() -- cumsum / normalise / searchsorted(side="right") -- is
+ * resolved from an exact prefix with a certified error window, falling back
+ * to numpy's literal serial cumsum when the draw lands inside it.
+ * The random stream stays with the caller (numpy PCG64 substream (seed, b)):
+ *   idx    : (B,K) int64; in: idx[b,0] = rng.integers(N); out: idx[b,1..K-1]
+ *   u      : (B,K-1) f64, u[b,j-1] = the rng.random() double of draw j
+ *   halted : (B) int32 out: K, or the first draw j whose total was 0.  The
+ *            reference then draws rng.integers(N) for j..K-1 (the table stays
+ *            all-zero), which the caller replays on its generator; idx[b, j..]
+ *            is left untouched.
+ *   min_d2 : (B,N) f64 scratch (the reference's resident weight table).
+ * Distances are computed from the exact f64 upcast of the data (f32, f64,
+ * bf16, f16).  Rows need d*8 <= 200 KiB.                                      */
+FK_API size_t fk_kmeanspp_workspace(int64_t B, int64_t N);
+FK_API fk_status fk_kmeanspp(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t d,
+                             int64_t K, const double* u, int64_t* idx, int32_t* halted,
+                             double* min_d2, void* workspace, size_t workspace_bytes, void* stream);
+/* Streaming pieces.  fk_kmeanspp_init sets halted[b] = K.  A sweep covers rows
+ * [0, rows) of X (B, rows, d) with batch stride x_batch_stride elements
+ * against centers (B, d) (batch stride c_batch_stride elements), writing
+ * min_d2 rows [0, rows) (batch stride m_batch_stride): first != 0 stores the
+ * distance, else the running minimum.  Sweeps for draw j skip batch elements
+ * with halted[b] < j.  fk_kmeanspp_select then picks idx[b, j] from the full
+ * (B, N) table.                                                               */
+FK_API fk_status fk_kmeanspp_init(int32_t* halted, int64_t B, int64_t N, int64_t K,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+FK_API fk_status fk_kmeanspp_sweep(fk_dtype dt, const void* X, int64_t B, int64_t rows, int64_t d,
+                                   int64_t x_batch_stride, const void* centers,
+                                   int64_t c_batch_stride, double* min_d2, int64_t m_batch_stride,
+                                   int32_t first, const int32_t* halted, int64_t j, void* stream);
+FK_API fk_status fk_kmeanspp_select(const double* min_d2, int64_t B, int64_t N, const double* u,
+                                    int64_t K, int64_t j, int64_t* idx, int32_t* halted,
+                                    void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

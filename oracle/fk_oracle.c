@@ -257,3 +257,79 @@ ORC_API void orc_normalize_f64(const double* sums, const int64_t* counts, const 
     }
   }
 }
+
+/* ------------------------------------------------------------- k-means++
+ * _kmeanspp_indices (core.py:342-357) leans on three numpy operations whose
+ * arithmetic is restated here (numpy 2.3.5, the reference's own dependency):
+ *   np.square(p64 - c).sum(axis=1) and min_d2.sum(): numpy's pairwise_sum
+ *     (numpy/_core/src/umath/loops_utils.h.src, PW_BLOCKSIZE = 128): n < 8
+ *     sequential from 0.0; n <= 128 eight strided accumulators combined as
+ *     ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a sequential tail; above 128
+ *     split at n2 = n/2 - (n/2)%8 and add the halves;
+ *   rng.choice(n, p=min_d2/total): cdf = cumsum(p) (serial), cdf /= cdf[-1],
+ *     searchsorted(cdf, u, side="right") with u = rng.random().
+ * The bitwise agreement with numpy is pinned by tests/test_oracle_golden.py. */
+static double orc_pw(const double* a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; ++i) res += a[i];
+    return res;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int k = 0; k < 8; ++k) r[k] = a[k];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int k = 0; k < 8; ++k) r[k] += a[i + k];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return orc_pw(a, n2) + orc_pw(a + n2, n - n2);
+}
+
+ORC_API double orc_pairwise_sum(const double* a, int64_t n) { return orc_pw(a, n); }
+
+/* min_d2 = (first ? d2 : min(min_d2, d2)), d2_i = pairwise sum_j (x_ij - c_j)^2
+ * over the f64 points (the reference upcasts with astype(float64)). */
+ORC_API void orc_kmeanspp_sweep(const double* x, int64_t n, int64_t d, const double* c,
+                                double* m, int first) {
+#pragma omp parallel
+  {
+    double* sq = (double*)malloc(sizeof(double) * (size_t)d);
+#pragma omp for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      const double* r = x + i * d;
+      for (int64_t j = 0; j < d; ++j) {
+        const double t = r[j] - c[j];
+        sq[j] = t * t;
+      }
+      const double v = orc_pw(sq, d);
+      if (first || v < m[i]) m[i] = v;
+    }
+    free(sq);
+  }
+}
+
+/* searchsorted(cumsum(m / total) / cumsum[-1], u, side="right"). */
+ORC_API int64_t orc_choice_cdf(const double* m, int64_t n, double total, double u) {
+  double* cdf = (double*)malloc(sizeof(double) * (size_t)n);
+  double s = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    s += m[i] / total;
+    cdf[i] = s;
+  }
+  const double last = cdf[n - 1];
+  int64_t lo = 0, hi = n; /* first index with cdf/last > u */
+  while (lo < hi) {
+    const int64_t mid = lo + (hi - lo) / 2;
+    if (cdf[mid] / last > u)
+      hi = mid;
+    else
+      lo = mid + 1;
+  }
+  free(cdf);
+  return lo;
+}

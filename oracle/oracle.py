@@ -68,6 +68,11 @@ def lib():
             getattr(L, name).argtypes = [P, P, I64, I64, P, P]
         for name in ("orc_normalize_f32", "orc_normalize_f64"):
             getattr(L, name).argtypes = [P, P, P, I64, I64, P, P]
+        L.orc_pairwise_sum.argtypes = [P, I64]
+        L.orc_pairwise_sum.restype = ctypes.c_double
+        L.orc_kmeanspp_sweep.argtypes = [P, I64, I64, P, P, ctypes.c_int]
+        L.orc_choice_cdf.argtypes = [P, I64, ctypes.c_double, ctypes.c_double]
+        L.orc_choice_cdf.restype = I64
         _lib = L
     return _lib
 
@@ -191,6 +196,46 @@ def init_indices(points: int, clusters: int, seed: int, batch: int) -> np.ndarra
         rng = np.random.default_rng((seed, b))
         idx[b] = rng.choice(points, size=clusters, replace=False)
     return idx
+
+
+def pairwise_sum(a: np.ndarray) -> float:
+    """numpy's pairwise summation of a 1-D f64 array (min_d2.sum())."""
+    a = np.ascontiguousarray(a, np.float64)
+    return float(lib().orc_pairwise_sum(_p(a), a.shape[0]))
+
+
+def kmeanspp_indices(points: np.ndarray, k: int, rng: np.random.Generator) -> np.ndarray:
+    """_kmeanspp_indices (core.py:342-357) with the numpy arithmetic in C.
+
+    The generator is consumed exactly like the reference: one integers(n)
+    for the first index, then per draw one random() (inside choice) when the
+    total is positive, else integers(n)."""
+    p64 = np.ascontiguousarray(points, np.float64)
+    n, d = p64.shape
+    L = lib()
+    idx = np.empty(k, np.int64)
+    idx[0] = rng.integers(n)
+    m = np.empty(n, np.float64)
+    c = np.ascontiguousarray(p64[idx[0]])
+    L.orc_kmeanspp_sweep(_p(p64), n, d, _p(c), _p(m), 1)
+    for j in range(1, k):
+        total = float(L.orc_pairwise_sum(_p(m), n))
+        if total > 0.0:
+            choice = int(L.orc_choice_cdf(_p(m), n, total, float(rng.random())))
+        else:
+            choice = int(rng.integers(n))
+        idx[j] = choice
+        c = np.ascontiguousarray(p64[choice])
+        L.orc_kmeanspp_sweep(_p(p64), n, d, _p(c), _p(m), 0)
+    return idx
+
+
+def kmeanspp_init_indices(x: np.ndarray, clusters: int, seed: int) -> np.ndarray:
+    """init_centroids(method="kmeanspp") row choice per batch (core.py:373-379)."""
+    out = np.empty((x.shape[0], clusters), np.int64)
+    for b in range(x.shape[0]):
+        out[b] = kmeanspp_indices(x[b], clusters, np.random.default_rng((seed, b)))
+    return out
 
 
 def init_centroids(x: np.ndarray, clusters: int, seed: int) -> np.ndarray:

@@ -52,12 +52,25 @@ def _declare(L):
     L.fk_objective.argtypes = [ctypes.c_int, P, I64, I64, P, P, SZ, P]
     L.fk_scatter.restype = ctypes.c_int
     L.fk_scatter.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, P, P, P]
+    L.fk_kmeanspp_workspace.restype = SZ
+    L.fk_kmeanspp_workspace.argtypes = [I64, I64]
+    L.fk_kmeanspp.restype = ctypes.c_int
+    L.fk_kmeanspp.argtypes = [ctypes.c_int, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]
+    L.fk_kmeanspp_init.restype = ctypes.c_int
+    L.fk_kmeanspp_init.argtypes = [P, I64, I64, I64, P, SZ, P]
+    L.fk_kmeanspp_sweep.restype = ctypes.c_int
+    L.fk_kmeanspp_sweep.argtypes = [ctypes.c_int, P, I64, I64, I64, I64, P, I64, P, I64, I32, P,
+                                    I64, P]
+    L.fk_kmeanspp_select.restype = ctypes.c_int
+    L.fk_kmeanspp_select.argtypes = [P, I64, I64, P, I64, I64, P, P, P, SZ, P]
 
 
 EXPORTED = (
     "fk_version", "fk_status_string", "fk_last_cuda_error", "fk_device_supported",
     "fk_assign_workspace", "fk_assign", "fk_update_workspace", "fk_update", "fk_normalize",
     "fk_row_norms", "fk_objective_workspace", "fk_objective", "fk_scatter",
+    "fk_kmeanspp_workspace", "fk_kmeanspp", "fk_kmeanspp_init", "fk_kmeanspp_sweep",
+    "fk_kmeanspp_select",
 )
 
 

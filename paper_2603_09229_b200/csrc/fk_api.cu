@@ -206,4 +206,58 @@ fk_status fk_scatter(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, 
                                         reinterpret_cast<cudaStream_t>(stream)));
 }
 
+// ------------------------------------------------------------- k-means++
+size_t fk_kmeanspp_workspace(int64_t B, int64_t N) {
+  if (B < 1 || N < 1 || B * N > kMaxPoints) return 0;
+  return fk::kmeanspp_workspace_bytes(B, N);
+}
+
+fk_status fk_kmeanspp_init(int32_t* halted, int64_t B, int64_t N, int64_t K, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (!halted || B < 1 || N < 1 || K < 1 || K > N || B * N > kMaxPoints) return FK_EINVAL;
+  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N)) return FK_EWORKSPACE;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(
+      fk::launch_kmeanspp_init(halted, ws, B, N, K, reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_kmeanspp_sweep(fk_dtype dt, const void* X, int64_t B, int64_t rows, int64_t d,
+                            int64_t x_batch_stride, const void* centers, int64_t c_batch_stride,
+                            double* min_d2, int64_t m_batch_stride, int32_t first,
+                            const int32_t* halted, int64_t j, void* stream) {
+  if (!valid_dt(dt) || !X || !centers || !min_d2 || B < 1 || rows < 0 || d < 1 ||
+      d > (1 << 20) || (int64_t)d * 8 > 200 * 1024)
+    return FK_EINVAL;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_kmeanspp_sweep(dt, X, B, rows, d, x_batch_stride, centers,
+                                               c_batch_stride, nullptr, 0, 0, min_d2,
+                                               m_batch_stride, first ? 1 : 0, halted, j,
+                                               reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_kmeanspp_select(const double* min_d2, int64_t B, int64_t N, const double* u,
+                             int64_t K, int64_t j, int64_t* idx, int32_t* halted, void* ws,
+                             size_t ws_bytes, void* stream) {
+  if (!min_d2 || !u || !idx || !halted || B < 1 || N < 1 || K < 2 || K > N || j < 1 || j >= K ||
+      B * N > kMaxPoints)
+    return FK_EINVAL;
+  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N)) return FK_EWORKSPACE;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_kmeanspp_select(min_d2, B, N, u, K, j, idx, halted, ws,
+                                                reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_kmeanspp(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t d, int64_t K,
+                      const double* u, int64_t* idx, int32_t* halted, double* min_d2, void* ws,
+                      size_t ws_bytes, void* stream) {
+  if (!valid_dt(dt) || !X || !idx || !halted || !min_d2 || B < 1 || N < 1 || d < 1 || K < 1 ||
+      K > N || B * N > kMaxPoints || d > (1 << 20) || (int64_t)d * 8 > 200 * 1024)
+    return FK_EINVAL;
+  if (K > 1 && !u) return FK_EINVAL;
+  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N)) return FK_EWORKSPACE;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_kmeanspp(dt, X, B, N, d, K, u, idx, halted, min_d2, ws,
+                                         reinterpret_cast<cudaStream_t>(stream)));
+}
+
 }  // extern "C"

@@ -52,4 +52,20 @@ cudaError_t launch_scatter(int dt, const void* X, const int32_t* ids, int64_t B,
                            int64_t K, int64_t d, double* sums, int64_t* counts,
                            cudaStream_t stream);
 
+// fk_kmeanspp.cu
+size_t kmeanspp_workspace_bytes(int64_t B, int64_t N);
+cudaError_t launch_kmeanspp_init(int32_t* halted, void* ws, int64_t B, int64_t N, int64_t K,
+                                 cudaStream_t s);
+cudaError_t launch_kmeanspp_sweep(int dt, const void* X, int64_t B, int64_t rows, int64_t d,
+                                  int64_t x_sb, const void* cen, int64_t cen_sb,
+                                  const int64_t* idx, int64_t K, int64_t col, double* m,
+                                  int64_t m_sb, int first, const int32_t* halted, int64_t j,
+                                  cudaStream_t s);
+cudaError_t launch_kmeanspp_select(const double* m, int64_t B, int64_t N, const double* u,
+                                   int64_t K, int64_t j, int64_t* idx, int32_t* halted, void* ws,
+                                   cudaStream_t s);
+cudaError_t launch_kmeanspp(int dt, const void* X, int64_t B, int64_t N, int64_t d, int64_t K,
+                            const double* u, int64_t* idx, int32_t* halted, double* m, void* ws,
+                            cudaStream_t s);
+
 }  // namespace fk

@@ -195,3 +195,69 @@ def scatter(x: torch.Tensor, ids: torch.Tensor, clusters: int):
                             B, n, clusters, d, sums.data_ptr(), counts.data_ptr(), _stream(dev))
     N.check(st, "fk_scatter")
     return sums, counts
+
+
+def kmeanspp(x: torch.Tensor, clusters: int, first: torch.Tensor, u: torch.Tensor):
+    """Device k-means++ D^2 seeding (core._kmeanspp_indices, core.py:342-357).
+
+    ``first`` (B,) int64 holds each batch element's rng.integers(N) draw and
+    ``u`` (B, K-1) float64 the rng.random() doubles of draws 1..K-1 (the RNG
+    stays with the caller).  Returns (idx int64 (B,K), halted int32 (B,)):
+    halted[b] < K marks the first draw whose total was 0 -- the reference
+    switches to rng.integers(N) from there, which the caller replays.
+    """
+    dev = _require_cuda(x, first, u)
+    x = x.contiguous()
+    B, n, d = x.shape
+    K = int(clusters)
+    if first.shape != (B,) or u.shape != (B, max(K - 1, 0)) or u.dtype != torch.float64:
+        raise ValueError("first must be (B,) and u float64 (B, K-1)")
+    idx = torch.zeros((B, K), dtype=torch.int64, device=dev)
+    idx[:, 0] = first.to(torch.int64)
+    halted = torch.empty((B,), dtype=torch.int32, device=dev)
+    m = torch.empty((B, n), dtype=torch.float64, device=dev)
+    L = N.lib()
+    need = L.fk_kmeanspp_workspace(B, n)
+    ws = _ws.get(dev, need, "kmeanspp")
+    u = u.contiguous()
+    st = L.fk_kmeanspp(fk_dtype(x.dtype), x.data_ptr(), B, n, d, K, u.data_ptr() if K > 1 else None,
+                       idx.data_ptr(), halted.data_ptr(), m.data_ptr(), ws.data_ptr(), ws.numel(),
+                       _stream(dev))
+    N.check(st, "fk_kmeanspp")
+    return idx, halted
+
+
+class KmeansppStream:
+    """Streamed k-means++ pieces (pipeline._streaming_kmeanspp, pipeline.py:420-453):
+    the (N,) f64 weight table lives on the device, chunks of rows are swept
+    as they arrive, and ``select`` resolves one rng.choice draw."""
+
+    def __init__(self, points: int, clusters: int, device):
+        self.n, self.k, self.dev = int(points), int(clusters), torch.device(device)
+        self.m = torch.empty((1, self.n), dtype=torch.float64, device=self.dev)
+        self.idx = torch.zeros((1, self.k), dtype=torch.int64, device=self.dev)
+        self.halted = torch.empty((1,), dtype=torch.int32, device=self.dev)
+        self.u = torch.zeros((1, max(self.k - 1, 1)), dtype=torch.float64, device=self.dev)
+        L = N.lib()
+        need = L.fk_kmeanspp_workspace(1, self.n)
+        self.ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.dev)
+        N.check(L.fk_kmeanspp_init(self.halted.data_ptr(), 1, self.n, self.k, self.ws.data_ptr(),
+                                   self.ws.numel(), _stream(self.dev)), "fk_kmeanspp_init")
+
+    def sweep(self, rows: torch.Tensor, lo: int, center: torch.Tensor, first: bool, j: int) -> None:
+        """min_d2[lo:lo+len(rows)] <- D^2 against ``center`` for draw j."""
+        rows = rows.contiguous()
+        n, d = rows.shape
+        center = center.contiguous()
+        st = N.lib().fk_kmeanspp_sweep(fk_dtype(rows.dtype), rows.data_ptr(), 1, n, d, n * d,
+                                       center.data_ptr(), d, self.m[0, lo:].data_ptr(), self.n,
+                                       1 if first else 0, self.halted.data_ptr(), int(j),
+                                       _stream(self.dev))
+        N.check(st, "fk_kmeanspp_sweep")
+
+    def select(self, j: int, u: float) -> None:
+        self.u[0, j - 1] = u
+        st = N.lib().fk_kmeanspp_select(self.m.data_ptr(), 1, self.n, self.u.data_ptr(), self.k,
+                                        int(j), self.idx.data_ptr(), self.halted.data_ptr(),
+                                        self.ws.data_ptr(), self.ws.numel(), _stream(self.dev))
+        N.check(st, "fk_kmeanspp_select")

@@ -230,7 +230,7 @@ def lloyd_run(x: DataMatrix, cfg: KMeansConfig, engine: str = "flash", workers: 
     xd = to_device(x.data, dev)
     if engine == "baseline":
         return _lloyd_baseline(DataMatrix(xd, check_finite=False), cfg, counters)
-    idx = init_indices(x.points, cfg.clusters, cfg.seed, x.batch, cfg.init, x.data)
+    idx = init_indices(x.points, cfg.clusters, cfg.seed, x.batch, cfg.init, xd)
     it_ = torch.from_numpy(idx).to(dev)
     c0 = torch.stack([xd[b].index_select(0, it_[b]) for b in range(x.batch)])
     eng = LloydEngine(xd, cfg.clusters, tiling.update_chunk)
@@ -637,58 +637,72 @@ def _reseed_from_stream(stream, st: _StreamState, master, new_master, new_operan
     shift2.copy_((diff * diff).sum(-1).max())
 
 
-def _init_from_stream(stream, clusters: int, seed: int, method: str) -> torch.Tensor:
+def _init_from_stream(stream, clusters: int, seed: int, method: str, device=None) -> torch.Tensor:
     """Same row draws as the in-core initializer (pipeline.py:456-479); a
     file-backed source reads only the chosen rows (plus, for k-means++, the
-    D^2 sweeps of pipeline.py:420-453)."""
+    D^2 sweeps of pipeline.py:420-453, streamed through the device)."""
     if method not in INIT_METHODS:
         raise ValueError(f"init method must be one of {INIT_METHODS}")
     if clusters > stream.total_points:
         raise ValueError(f"cannot place {clusters} clusters with only {stream.total_points} points")
-    if isinstance(stream, HostStream):
-        idx = init_indices(stream.total_points, clusters, seed, stream.batch, method,
-                           stream.host if method == "kmeanspp" else None)
-        out = torch.stack([stream.host[b][torch.from_numpy(idx[b])] for b in range(stream.batch)])
-        return out.contiguous()
     out = torch.empty((stream.batch, clusters, stream.dims), dtype=stream.dtype)
     for b in range(stream.batch):
         rng = np.random.default_rng((seed, b))
         if method == "random_distinct":
             idx = rng.choice(stream.total_points, size=clusters, replace=False)
         else:
-            idx = _streaming_kmeanspp(stream, b, clusters, rng)
+            dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+            idx = _streaming_kmeanspp(stream, b, clusters, rng, dev)
         for j, i in enumerate(idx):
             out[b, j] = stream.read_rows(b, int(i), int(i) + 1)[0]
     return out
 
 
-def _streaming_kmeanspp(stream, b: int, k: int, rng: np.random.Generator) -> np.ndarray:
-    """k-means++ over a file stream with only an (N,) float64 weight table
-    resident; the D^2 arithmetic and RNG draws are those of the in-core seeding
-    (core.py:342-357), so the chosen rows match it bitwise."""
+def _stream_rows_host(stream, b: int, lo: int, hi: int, buf: torch.Tensor | None) -> torch.Tensor:
+    if isinstance(stream, HostStream):
+        return stream.view(b, lo, hi)  # pinned slice: a true async DMA
+    return stream.read_rows_into(b, lo, hi, buf)
+
+
+def _streaming_kmeanspp(stream, b: int, k: int, rng: np.random.Generator, device) -> np.ndarray:
+    """k-means++ over a chunk stream (pipeline.py:420-453): the (N,) f64 weight
+    table is device-resident, every chunk is swept by fk_kmeanspp_sweep as it
+    arrives and each choice() draw is resolved by fk_kmeanspp_select -- the
+    same arithmetic as the in-core seeding, so the chosen rows match it (and
+    the reference) index for index.  One host read per draw fetches the
+    chosen index (its row is the next sweep's center)."""
+    from . import ops
+
     n = stream.total_points
     idx = np.empty(k, np.int64)
     idx[0] = rng.integers(n)
-    min_d2 = np.empty(n, np.float64)
-    buf = torch.empty((stream.chunk_points, stream.dims), dtype=stream.dtype)
+    if k == 1:
+        return idx
+    pp = ops.KmeansppStream(n, k, device)
+    buf = None
+    if not isinstance(stream, HostStream):
+        buf = torch.empty((stream.chunk_points, stream.dims), dtype=stream.dtype).pin_memory()
 
-    def sweep(center: torch.Tensor, first: bool) -> None:
-        c64 = center.double().numpy()
+    def sweep(row: int, first: bool, j: int) -> None:
+        center = stream.read_rows(b, row, row + 1)[0].to(device)
         for t in range(stream.n_chunks):
             lo, hi = stream.bounds(t)
-            v = stream.read_rows_into(b, lo, hi, buf).double().numpy()
-            d2 = np.square(v - c64).sum(axis=1)
-            if first:
-                min_d2[lo:hi] = d2
-            else:
-                np.minimum(min_d2[lo:hi], d2, out=min_d2[lo:hi])
+            rows = _stream_rows_host(stream, b, lo, hi, buf).to(device, non_blocking=buf is None)
+            pp.sweep(rows, lo, center, first, j)
 
-    sweep(stream.read_rows(b, int(idx[0]), int(idx[0]) + 1)[0], True)
+    sweep(int(idx[0]), True, 1)
     for j in range(1, k):
-        total = float(min_d2.sum())
-        choice = int(rng.choice(n, p=min_d2 / total)) if total > 0.0 else int(rng.integers(n))
-        idx[j] = choice
-        sweep(stream.read_rows(b, choice, choice + 1)[0], False)
+        state = rng.bit_generator.state
+        pp.select(j, float(rng.random()))
+        got = pp.idx[0, j].item()
+        if int(pp.halted[0].item()) == j:  # total == 0: the reference draws integers from here on
+            rng.bit_generator.state = state
+            for jj in range(j, k):
+                idx[jj] = rng.integers(n)
+            return idx
+        idx[j] = got
+        if j + 1 < k:
+            sweep(int(got), False, j + 1)
     return idx
 
 
@@ -794,7 +808,7 @@ def chunked_stream_run(stream, cfg: KMeansConfig, assign_path: str | None = None
                              _workers(workers))
     run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk,
                         policy=cfg.empty_cluster_policy)
-    run.set(_init_from_stream(stream, cfg.clusters, cfg.seed, cfg.init))
+    run.set(_init_from_stream(stream, cfg.clusters, cfg.seed, cfg.init, run.dev))
     history = []
     iterations = 0
     for it in range(1, cfg.max_iters + 1):

@@ -167,14 +167,14 @@ def test_chunk_stream_reads(tmp_path):
     s.close()
 
 
-@pytest.mark.parametrize("method", ["random_distinct", "kmeanspp"])
+@pytest.mark.parametrize("method", ["random_distinct", pytest.param("kmeanspp", marks=pytest.mark.gpu)])
 def test_stream_init_matches_in_core(tmp_path, method):
     x = fk.generate_dataset(2, 300, 5, 6, 1.0, 3, "single")
     p = str(tmp_path / "x.fkm1")
     fk.write_fkm1(p, x)
     with fk.ChunkStream(p, 37) as s:
         c_stream = _init_from_stream(s, 7, 11, method)
-    idx = init_indices(300, 7, 11, 2, method, x.data)
+    idx = init_indices(300, 7, 11, 2, method, x.data.cuda() if method == "kmeanspp" else x.data)
     c_core = torch.stack([x.data[b][torch.from_numpy(idx[b])] for b in range(2)])
     assert torch.equal(c_stream, c_core)
 

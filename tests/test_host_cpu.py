@@ -143,12 +143,6 @@ class TestInit:
         c = fk.init_centroids(x, 9, 4)
         assert np.array_equal(c.numpy(), oracle.init_centroids(xo, 9, 4))
 
-    def test_kmeanspp_matches_reference(self, reference):
-        xr = reference.generate_dataset(2, 300, 5, 4, 1.0, 3, "double")
-        cr = reference.init_centroids(xr, 6, 9, "kmeanspp")
-        c = fk.init_centroids(fk.DataMatrix(torch.from_numpy(xr.data)), 6, 9, "kmeanspp")
-        assert np.array_equal(c.numpy(), cr.data)
-
     def test_init_validation(self):
         x = fk.generate_dataset(1, 5, 2, 2, 0.5, 0)
         with pytest.raises(ValueError):
