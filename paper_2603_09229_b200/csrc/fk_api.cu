@@ -120,7 +120,8 @@ fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B, int64_
         ext = reinterpret_cast<uint8_t*>(ws) + al256((size_t)B * kpad * 4);
         st = cuda_status(fk::launch_cn_ext(dt, C, B, K, d, kpad, ext, s));
       } else {
-        st = cuda_status(fk::launch_cn_pad(dt, C, B, K, d, kpad, cn, s));
+        st = cuda_status(fk::launch_cn_pad(dt, C, B, K, d, kpad, cn, s,
+                                           fk::assign_tc_bias_mode(fmt) == 2 ? 0.5f : 1.0f));
       }
       if (st != FK_OK) return st;
       return cuda_status(fk::launch_assign_tc(fmt, X, C, cn, ext, B, N, K, d, idx_out,

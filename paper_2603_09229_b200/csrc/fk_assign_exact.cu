@@ -48,7 +48,7 @@ __global__ void k_row_norms_exact(const T* __restrict__ M, int64_t rows, int64_t
 // columns beyond K never win the argmin.
 template <typename T>
 __global__ void k_cn_pad(const T* __restrict__ C, int64_t B, int64_t K, int64_t d, int kpad,
-                         float* out) {
+                         float* out, float scale) {
   // one warp per (padded) centroid row; lanes stride over the features
   const int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -65,7 +65,7 @@ __global__ void k_cn_pad(const T* __restrict__ C, int64_t B, int64_t K, int64_t 
     acc = fmaf(v, v, acc);
   }
   for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) out[gi] = acc;
+  if (lane == 0) out[gi] = acc * scale;  // scale 0.5 (exact): the TMEM-seed bias ||c||^2/2
 }
 
 // Bias operand for the bias-in-GEMM FlashAssign: ||c||^2 / 2 split into three
@@ -225,16 +225,16 @@ __global__ void __launch_bounds__(EX_ROWS)
 
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_cn_pad(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
-                          float* cn_pad, cudaStream_t stream) {
+                          float* cn_pad, cudaStream_t stream, float scale) {
   const int64_t n = B * kpad * 32;  // one warp per row
   const int th = 256;
   const unsigned grid = (unsigned)((n + th - 1) / th);
   if (dt == DT_BF16)
-    k_cn_pad<__nv_bfloat16><<<grid, th, 0, stream>>>((const __nv_bfloat16*)C, B, K, d, kpad, cn_pad);
+    k_cn_pad<__nv_bfloat16><<<grid, th, 0, stream>>>((const __nv_bfloat16*)C, B, K, d, kpad, cn_pad, scale);
   else if (dt == DT_F16)
-    k_cn_pad<__half><<<grid, th, 0, stream>>>((const __half*)C, B, K, d, kpad, cn_pad);
+    k_cn_pad<__half><<<grid, th, 0, stream>>>((const __half*)C, B, K, d, kpad, cn_pad, scale);
   else
-    k_cn_pad<float><<<grid, th, 0, stream>>>((const float*)C, B, K, d, kpad, cn_pad);
+    k_cn_pad<float><<<grid, th, 0, stream>>>((const float*)C, B, K, d, kpad, cn_pad, scale);
   return cudaGetLastError();
 }
 

@@ -433,17 +433,26 @@ FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, f
   best = p ? colbase : best;
 }
 
-// AUG = true : the ||c||^2 bias rides in the GEMM as one extra K=16 step
-//              (A_ext = ones, B_ext = 3-way bf16 split of ||c||^2/2, main
-//              MMAs negate A), so the epilogue is a pure min-reduction.
-// AUG = false: bias applied in the epilogue from a smem ring (fp16 data,
-//              whose range cannot hold ||c||^2 safely).
-template <int FMT, bool AUG, bool ALT>
+// BIAS = 1 (bias-in-GEMM): the ||c||^2 bias rides in the GEMM as one extra
+//              K=16 step (A_ext = ones, B_ext = 3-way bf16 split of
+//              ||c||^2/2, main MMAs negate A), so the epilogue is a pure
+//              min-reduction.
+// BIAS = 2 (TMEM seed): after draining a TMEM accumulator the epilogue warps
+//              store ||c||^2/2 of the tile that will reuse it (two tiles
+//              ahead) into it with tcgen05.st; the MMAs (A negated)
+//              accumulate onto the seed.  No extra MMA step, no fp16 range
+//              issue, still a pure min-reduction epilogue.
+// BIAS = 0 (epilogue bias): bias added in the epilogue from a smem ring.
+template <int FMT, int BIAS, bool ALT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     fk_assign_tc2_kernel(const __grid_constant__ CUtensorMap tmx,
                          const __grid_constant__ CUtensorMap tmc,
                          const __grid_constant__ CUtensorMap tmext, const TcArgs p) {
   using namespace tc2;
+  constexpr bool AUG = BIAS == 1;   // bias as an extra MMA step
+  constexpr bool SEED = BIAS == 2;  // bias seeded into TMEM by the epilogue
+  constexpr bool EPI = BIAS == 0;   // bias added in the epilogue
+  constexpr bool NEG = BIAS != 0;   // accumulator holds ||c||^2/2 - x.c
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -590,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     // (uniform datapath); one elected lane issues each tcgen05 instruction.
     if (leader) {
       const uint32_t idesc = make_idesc_f16(FMT, 2 * BM, BN);
-      const uint32_t idesc_main = AUG ? (idesc | kIdescNegateA) : idesc;
+      const uint32_t idesc_main = NEG ? (idesc | kIdescNegateA) : idesc;
       const uint32_t idesc_ext = make_idesc_f16(1, 2 * BM, BN);
       const uint64_t aext_desc = make_sdesc_sw32(smem_u32(sAext));
       uint32_t stage = 0, sphase = 0, g = 0;
@@ -603,7 +612,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         for (int c = 0; c < p.ncol; ++c, ++g) {
           const uint32_t buf = g % NBUF;
           if (pair == 0 && lane == 0) trace_ev(p, g, 6);
-          mbar_wait(&t_empty[buf], ((g / NBUF) & 1) ^ 1);
+          // SEED: every use of a buffer (the first two included) waits for its seed
+          mbar_wait(&t_empty[buf], SEED ? ((g / NBUF) & 1) : (((g / NBUF) & 1) ^ 1));
           tc_fence_after();
           if (pair == 0 && lane == 0) trace_ev(p, g, 0);
           const uint32_t d_tmem = tmem_base + buf * BN;
@@ -616,7 +626,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               if (p.debug_mode != 2) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)  // +32 B along K = +2 in the descriptor's address field
-                  tc_mma_f16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc_main, (ka | k) != 0);
+                  tc_mma_f16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc_main,
+                                 SEED || (ka | k) != 0);
               }
               tc_commit_cg2_mc(&b_empty[stage], 0x3);
             }
@@ -650,6 +661,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     const int wg = warp >> 2;        // column half of every tile (alt: tile parity)
     const int q = warp & 3;          // TMEM lane quarter
     const int row = q * 32 + lane;
+    constexpr int nch = ALT ? 8 : 4;  // 32-column chunks this warp reads per tile
+    // SEED: write ||c||^2/2 of pair-tile g2 (all rows alike) into TMEM buffer
+    // g2 % NBUF, then hand the buffer to the MMA.
+    auto seed_and_release = [&](uint32_t g2) __attribute__((always_inline)) {
+      const uint32_t sbuf = g2 % NBUF;
+      const int i2 = (int)(g2 / p.ncol);
+      if (pair + i2 * npairs < p.total_tiles && (!alt || (i2 & 1) == wg)) {
+        const uint32_t cs = g2 % CN_SLOTS;
+        mbar_wait(&cn_full[cs], (g2 / CN_SLOTS) & 1);
+        const uint32_t src = smem_u32(sCN + cs * BN + (alt ? 0 : wg * (BN / 2)));
+        const uint32_t saddr =
+            tmem_base + (uint32_t(q * 32) << 16) + sbuf * BN + (alt ? 0 : wg * (BN / 2));
+#pragma unroll 4
+        for (int k = 0; k < 4 * nch; ++k) {  // 8 columns per store: few live registers
+          const float4 f0 = lds128(src + 32 * k), f1 = lds128(src + 32 * k + 16);
+          const uint32_t v[8] = {__float_as_uint(f0.x), __float_as_uint(f0.y), __float_as_uint(f0.z),
+                                 __float_as_uint(f0.w), __float_as_uint(f1.x), __float_as_uint(f1.y),
+                                 __float_as_uint(f1.z), __float_as_uint(f1.w)};
+          tmem_st_x8(saddr + 8 * k, v);
+        }
+        tmem_wait_st();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&cn_empty[cs]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(&t_empty[sbuf]);
+        else
+          mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[sbuf]), 0));
+      }
+    };
+    if (SEED) {
+      // the first use of each buffer; ALT: a warpgroup seeds only its own tiles
+      for (uint32_t g0 = 0; g0 < NBUF; ++g0)
+        if (!alt || (int)(g0 & 1) == wg) seed_and_release(g0);
+    }
     uint32_t g = 0;
     int i = 0;
     for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
@@ -683,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           if (lane == 0) mbar_arrive(&a_empty[slot]);
         }
         uint32_t cnp = 0;
-        if (!AUG) {
+        if (EPI) {
           mbar_wait(&cn_full[cslot], (g / CN_SLOTS) & 1);
           cnp = smem_u32(sCN + cslot * BN + (alt ? 0 : wg * (BN / 2)));
         }
@@ -699,19 +748,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           }
         };
         auto chunk = [&](uint32_t (&v)[32], int ch) {
-          if (AUG)
+          if (NEG)
             epi_chunk_aug(v, col0 + 32 * ch, M, best, bestv);
           else
             epi_chunk(v, cnp + 128 * ch, col0 + 32 * ch, M, best, bestv);
         };
         if (p.debug_mode == 1) {
           FK_TMEM_WAIT_LD(va);
-          release_tmem();
-          if (!AUG && lane == 0) mbar_arrive(&cn_empty[cslot]);
+          release_tmem();  // (debug mode 1 does not support SEED: garbage accumulators are fine for timing)
+          if (EPI && lane == 0) mbar_arrive(&cn_empty[cslot]);
           M = fminf(M, __uint_as_float(va[0]));
           continue;
         }
-        constexpr int nch = ALT ? 8 : 4;  // 32-column chunks this warp reads per tile
 #pragma unroll
         for (int ch = 0; ch < nch; ch += 2) {
           FK_TMEM_WAIT_LD(va);
@@ -720,14 +768,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           FK_TMEM_WAIT_LD(vb);
           if (ch + 2 < nch) {
             FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 2), va);
-          } else {
+          } else if (!SEED) {
             release_tmem();  // every TMEM read of this buffer has landed
             if (tr) trace_ev(p, g, 3);
           }
           chunk(vb, ch + 1);
         }
+        if (SEED) {
+          seed_and_release(g + NBUF);  // reads done: seed the tile that reuses this buffer
+          if (tr) trace_ev(p, g, 3);
+        }
         if (tr) trace_ev(p, g, 4);
-        if (!AUG) {
+        if (EPI) {
           __syncwarp();
           if (lane == 0) mbar_arrive(&cn_empty[cslot]);
         }
@@ -760,7 +812,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         if (grow < p.N) {
           const size_t o = (size_t)b * p.N + grow;
           p.idx_out[o] = idx;
-          p.mind_out[o] = fmaxf(0.f, AUG ? fmaf(2.f, M, xn) : xn + M);
+          p.mind_out[o] = fmaxf(0.f, NEG ? fmaf(2.f, M, xn) : xn + M);
           if (p.idx_prev) ch = p.idx_prev[o] != idx;
         }
         if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
@@ -776,7 +828,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   }
 }
 
-template <int FMT, bool AUG, bool ALT>
+template <int FMT, int BIAS, bool ALT>
 static cudaError_t launch_pair_t(const CUtensorMap& tmx, const CUtensorMap& tmc,
                                  const CUtensorMap& tmext, TcArgs a, int pairs,
                                  cudaStream_t stream) {
@@ -784,16 +836,16 @@ static cudaError_t launch_pair_t(const CUtensorMap& tmx, const CUtensorMap& tmc,
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_dev_mask & (1 << (dev & 31)))) {
-    cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, AUG, ALT>,
+    cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, BIAS, ALT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES);
     attr_dev_mask |= 1 << (dev & 31);
   }
-  fk_assign_tc2_kernel<FMT, AUG, ALT><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(
+  fk_assign_tc2_kernel<FMT, BIAS, ALT><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(
       tmx, tmc, tmext, a);
   return cudaGetLastError();
 }
 
-template <int FMT, bool AUG>
+template <int FMT, int BIAS>
 static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
                                const CUtensorMap& tmext, TcArgs a, int num_sms,
                                cudaStream_t stream) {
@@ -803,8 +855,8 @@ static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
   int pairs = num_sms / 2;
   if (a.total_tiles < pairs) pairs = a.total_tiles;
   if (pairs <= 0) return cudaSuccess;
-  return a.ncol == 1 ? launch_pair_t<FMT, AUG, true>(tmx, tmc, tmext, a, pairs, stream)
-                     : launch_pair_t<FMT, AUG, false>(tmx, tmc, tmext, a, pairs, stream);
+  return a.ncol == 1 ? launch_pair_t<FMT, BIAS, true>(tmx, tmc, tmext, a, pairs, stream)
+                     : launch_pair_t<FMT, BIAS, false>(tmx, tmc, tmext, a, pairs, stream);
 }
 
 // ---------------------------------------------------------------- host side
@@ -839,15 +891,21 @@ static bool make_map(CUtensorMap* m, const void* base, int fmt, int64_t inner, i
   return r == CUDA_SUCCESS;
 }
 
+constexpr int kDefaultBiasMode = 1;
+
 bool assign_tc_supported(int64_t d) { return d >= 8 && d <= 128 && (d % 8) == 0; }
 
-// Bias-in-GEMM is used for bf16 data (fp16 cannot hold ||c||^2/2 safely);
-// FK_ASSIGN_AUG=0 forces the epilogue-bias variant (A/B comparisons).
-bool assign_tc_uses_ext(int fmt) {
+// Where the ||c||^2/2 bias enters (FK_ASSIGN_BIAS=0 epilogue, 1 bias-in-GEMM,
+// 2 TMEM seed; A/B comparisons).  The legacy FK_ASSIGN_AUG=0 means 0.
+int assign_tc_bias_mode(int fmt) {
   (void)fmt;
-  const char* e = getenv("FK_ASSIGN_AUG");
-  return !(e && atoi(e) == 0);
+  const char* e = getenv("FK_ASSIGN_BIAS");
+  if (e && e[0] >= '0' && e[0] <= '2') return e[0] - '0';
+  const char* a = getenv("FK_ASSIGN_AUG");
+  if (a && atoi(a) == 0) return 0;
+  return kDefaultBiasMode;
 }
+bool assign_tc_uses_ext(int fmt) { return assign_tc_bias_mode(fmt) == 1; }
 
 cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
                              const void* cn_ext, int64_t B, int64_t N, int64_t K, int64_t d,
@@ -885,17 +943,23 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     CUtensorMap tmx2, tmc2, tmext;
     if (!make_map(&tmx2, X, fmt, d, N, B, tc2::BM)) return cudaErrorInvalidValue;
     if (!make_map(&tmc2, C, fmt, d, K, B, tc2::BNH)) return cudaErrorInvalidValue;
-    const bool aug = cn_ext != nullptr && assign_tc_uses_ext(fmt);
+    const int bias = cn_ext != nullptr ? 1 : (assign_tc_bias_mode(fmt) == 2 ? 2 : 0);
+    const bool aug = bias == 1;
     if (aug) {
       if (!make_map(&tmext, cn_ext, 1, 16, a.kpad, B, tc2::BNH, 16, CU_TENSOR_MAP_SWIZZLE_32B))
         return cudaErrorInvalidValue;
     } else {
       tmext = tmc2;  // unused
     }
-    cudaError_t e = fmt == 1 ? (aug ? launch_pair<1, true>(tmx2, tmc2, tmext, a, num_sms, stream)
-                                    : launch_pair<1, false>(tmx2, tmc2, tmext, a, num_sms, stream))
-                             : (aug ? launch_pair<0, true>(tmx2, tmc2, tmext, a, num_sms, stream)
-                                    : launch_pair<0, false>(tmx2, tmc2, tmext, a, num_sms, stream));
+    cudaError_t e;
+    if (fmt == 1)
+      e = bias == 1   ? launch_pair<1, 1>(tmx2, tmc2, tmext, a, num_sms, stream)
+          : bias == 2 ? launch_pair<1, 2>(tmx2, tmc2, tmext, a, num_sms, stream)
+                      : launch_pair<1, 0>(tmx2, tmc2, tmext, a, num_sms, stream);
+    else
+      e = bias == 1   ? launch_pair<0, 1>(tmx2, tmc2, tmext, a, num_sms, stream)
+          : bias == 2 ? launch_pair<0, 2>(tmx2, tmc2, tmext, a, num_sms, stream)
+                      : launch_pair<0, 0>(tmx2, tmc2, tmext, a, num_sms, stream);
     if (trace_path && e == cudaSuccess) {  // debug only: synchronous dump
       unsigned long long h[TR_N * TR_EV];
       cudaMemcpyAsync(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost, stream);

@@ -12,6 +12,7 @@ enum Dt { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2, DT_F64 = 3 };
 bool assign_tc_supported(int64_t d);
 int assign_tc_kpad(int64_t K);
 bool assign_tc_uses_ext(int fmt);
+int assign_tc_bias_mode(int fmt);  // 0 epilogue, 1 bias-in-GEMM, 2 TMEM seed
 cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
                              const void* cn_ext, int64_t B, int64_t N, int64_t K, int64_t d,
                              int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
@@ -19,7 +20,7 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
 
 // fk_assign_exact.cu
 cudaError_t launch_cn_pad(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
-                          float* cn_pad, cudaStream_t stream);
+                          float* cn_pad, cudaStream_t stream, float scale = 1.0f);
 // (B, kpad, 16) operand [hi, mid, lo, 0...] of ||c||^2 / 2 (+inf beyond K)
 cudaError_t launch_cn_ext(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
                           void* out, cudaStream_t stream);

@@ -76,66 +76,27 @@ FK_DEV double to_f64(__half v) { return (double)__half2float(v); }
 // 8 consecutive elements (16-byte aligned) widened to f64.
 template <typename T>
 FK_DEV void load8(const T* p, double* o);
-// Exact 16-bit -> f64 widening with integer ops (the F2F conversion pipe is
-// narrow): normal numbers and zeros re-bias the exponent; anything else
-// (subnormal, inf, nan) takes the converting path.
-FK_DEV double bf16_bits_f64(uint32_t b) {
-  const uint32_t a = b & 0x7fffu;
-  const uint32_t hi = (a ? (a << 13) + 0x38000000u : 0u) | ((b & 0x8000u) << 16);
-  return __hiloint2double((int)hi, 0);
-}
-FK_DEV bool bf16_fast_ok(uint32_t b) {
-  const uint32_t a = b & 0x7fffu;
-  return a == 0 || (a >= 0x80u && a < 0x7f80u);
-}
-FK_DEV double f16_bits_f64(uint32_t h) {
-  const uint32_t a = h & 0x7fffu;
-  const uint32_t hi = (a ? (a << 10) + 0x3F000000u : 0u) | ((h & 0x8000u) << 16);
-  return __hiloint2double((int)hi, 0);
-}
-FK_DEV bool f16_fast_ok(uint32_t h) {
-  const uint32_t a = h & 0x7fffu;
-  return a == 0 || (a >= 0x400u && a < 0x7c00u);
-}
-
+// bf16 -> f32 is a 16-bit shift (exact); f32 -> f64 one F2F.
 template <>
 FK_DEV void load8<__nv_bfloat16>(const __nv_bfloat16* p, double* o) {
   const uint4 v = *reinterpret_cast<const uint4*>(p);
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  bool ok = true;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    o[2 * k] = bf16_bits_f64(w[k] & 0xffffu);
-    o[2 * k + 1] = bf16_bits_f64(w[k] >> 16);
-    ok = ok && bf16_fast_ok(w[k] & 0xffffu) && bf16_fast_ok(w[k] >> 16);
-  }
-  if (!ok) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      o[2 * k] = (double)__uint_as_float(w[k] << 16);
-      o[2 * k + 1] = (double)__uint_as_float(w[k] & 0xffff0000u);
-    }
+    o[2 * k] = (double)__uint_as_float(w[k] << 16);
+    o[2 * k + 1] = (double)__uint_as_float(w[k] & 0xffff0000u);
   }
 }
 template <>
 FK_DEV void load8<__half>(const __half* p, double* o) {
   const uint4 v = *reinterpret_cast<const uint4*>(p);
   const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  bool ok = true;
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
-    o[2 * k] = f16_bits_f64(w[k] & 0xffffu);
-    o[2 * k + 1] = f16_bits_f64(w[k] >> 16);
-    ok = ok && f16_fast_ok(w[k] & 0xffffu) && f16_fast_ok(w[k] >> 16);
-  }
-  if (!ok) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const __half2 h = *reinterpret_cast<const __half2*>(&w[k]);
-      const float2 f = __half22float2(h);
-      o[2 * k] = (double)f.x;
-      o[2 * k + 1] = (double)f.y;
-    }
+    const __half2 h = *reinterpret_cast<const __half2*>(&w[k]);
+    const float2 f = __half22float2(h);
+    o[2 * k] = (double)f.x;
+    o[2 * k + 1] = (double)f.y;
   }
 }
 template <>
@@ -183,6 +144,27 @@ FK_DEV double pw_leaf_row(const T* x, const double* c, int n) {
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
   for (; i < n; ++i) res = __dadd_rn(res, sqd(to_f64(x[i]), c[i]));
   return res;
+}
+
+// Same leaf for a compile-time d (multiple of 8, 8 <= D <= 128): fully
+// unrolled, centre read as 16-B pairs, no tail.
+template <typename T, int D>
+FK_DEV double pw_leaf_row_fixed(const T* x, const double* c) {
+  static_assert(D % 8 == 0 && D >= 8 && D <= kLeaf, "fixed leaf");
+  double r[8], v[8];
+#pragma unroll
+  for (int i = 0; i < D; i += 8) {
+    load8<T>(x + i, v);
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+      const double2 cc = *reinterpret_cast<const double2*>(c + i + k);
+      const double s0 = sqd(v[k], cc.x), s1 = sqd(v[k + 1], cc.y);
+      r[k] = i == 0 ? s0 : __dadd_rn(r[k], s0);
+      r[k + 1] = i == 0 ? s1 : __dadd_rn(r[k + 1], s1);
+    }
+  }
+  return __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                   __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
 }
 
 // Rows longer than 128: numpy splits at n2 = n/2 rounded down to a multiple of
@@ -284,7 +266,7 @@ FK_DEV DD block_excl_scan(DD v, DD* warp_buf, DD* total) {
 // ------------------------------------------------------------------ sweep
 // min_d2[b, i] = (first ? d2 : min(min_d2[b, i], d2)), d2 = numpy-order
 // ||x_i - center_b||^2 in f64.  center_b = cen + b*cen_sb + (idx ? idx[b*K + col] : 0)*d.
-template <typename T>
+template <typename T, int D>
 __global__ void __launch_bounds__(kSweepRows) k_pp_sweep(
     const T* __restrict__ X, int64_t rows, int d, int64_t x_sb, const T* __restrict__ cen,
     int64_t cen_sb, const int64_t* __restrict__ idx, int64_t K, int64_t col,
@@ -341,7 +323,8 @@ __global__ void __launch_bounds__(kSweepRows) k_pp_sweep(
   __syncthreads();
   const int t = threadIdx.x;
   if (t < nr) {
-    const double v = pw_row<T>(tile + (size_t)t * stride_elems, c, d);
+    const double v = D > 0 ? pw_leaf_row_fixed<T, (D > 0 ? D : 8)>(tile + (size_t)t * stride_elems, c)
+                           : pw_row<T>(tile + (size_t)t * stride_elems, c, d);
     double* mp = m + b * m_sb + r0 + t;
     *mp = first ? v : fmin(*mp, v);
   }
@@ -361,7 +344,7 @@ FK_DEV void cp_async_wait() {
 // aligned): each CTA walks tiles of 128 rows with a STAGES-deep cp.async ring
 // (padded rows: conflict-free 16-B reads), so HBM streaming overlaps the f64
 // arithmetic of the previous tiles.
-template <typename T, int STAGES>
+template <typename T, int STAGES, int D>
 __global__ void __launch_bounds__(kSweepRows) k_pp_sweep_pipe(
     const T* __restrict__ X, int64_t rows, int d, int64_t x_sb, const T* __restrict__ cen,
     int64_t cen_sb, const int64_t* __restrict__ idx, int64_t K, int64_t col,
@@ -412,7 +395,8 @@ __global__ void __launch_bounds__(kSweepRows) k_pp_sweep_pipe(
     const int64_t r0 = t * kSweepRows;
     const int nr = (int)i64min(kSweepRows, rows - r0);
     if ((int)threadIdx.x < nr) {
-      const double v = pw_row<T>(tiles + slot * tile_elems + (size_t)threadIdx.x * stride_elems, c, d);
+      const T* xr = tiles + slot * tile_elems + (size_t)threadIdx.x * stride_elems;
+      const double v = D > 0 ? pw_leaf_row_fixed<T, (D > 0 ? D : 8)>(xr, c) : pw_row<T>(xr, c, d);
       double* mp = m + b * m_sb + r0 + threadIdx.x;
       *mp = first ? v : fmin(*mp, v);
     }
@@ -502,6 +486,9 @@ __global__ void __launch_bounds__(256) k_pp_node(const double* __restrict__ m, i
                                                   double2* __restrict__ ddsum) {
   __shared__ double a[kNodeMax];
   __shared__ double V[(2 << kNodeLevels) - 1];
+  __shared__ uint8_t kind[(2 << kNodeLevels) - 1];
+  __shared__ int leaf_lo[kNodeMax / 32], leaf_n[kNodeMax / 32], leaf_v[kNodeMax / 32];
+  __shared__ int nleaf;
   __shared__ DD wb[32];
   const int b = blockIdx.y;
   if (halted[b] < j) return;
@@ -509,6 +496,7 @@ __global__ void __launch_bounds__(256) k_pp_node(const double* __restrict__ m, i
   int64_t lo0, n0;
   pw_walk(N, t1, node, lo0, n0);
   const double* src = m + b * m_sb + lo0;
+  if (threadIdx.x == 0) nleaf = 0;
   DD acc{0.0, 0.0};
   for (int k = threadIdx.x; k < n0; k += blockDim.x) {
     const double v = src[k];
@@ -525,10 +513,9 @@ __global__ void __launch_bounds__(256) k_pp_node(const double* __restrict__ m, i
     for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s = dd_add(s, wb[w]);
     ddsum[b * ((int64_t)1 << t1) + node] = make_double2(s.hi, s.lo);
   }
-  for (int r = rdepth; r >= 0; --r) {
+  // A: classify every node of the subtree (0 absent, 1 leaf, 2 internal), list the leaves
+  for (int r = 0; r <= rdepth; ++r) {
     const int cnt = 1 << r;
-    double* Vr = V + (cnt - 1);
-    const double* Vc = V + (2 * cnt - 1);
     for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
       int64_t lo = 0, n = n0;
       bool exists = true;
@@ -545,8 +532,52 @@ __global__ void __launch_bounds__(256) k_pp_node(const double* __restrict__ m, i
           n = h;
         }
       }
-      if (!exists) continue;
-      Vr[q] = n <= kLeaf ? pw_leaf_arr(a + lo, (int)n) : __dadd_rn(Vc[2 * q], Vc[2 * q + 1]);
+      const int vi = cnt - 1 + q;
+      kind[vi] = !exists ? 0 : (n <= kLeaf ? 1 : 2);
+      if (exists && n <= kLeaf) {
+        const int k = atomicAdd(&nleaf, 1);
+        leaf_lo[k] = (int)lo;
+        leaf_n[k] = (int)n;
+        leaf_v[k] = vi;
+      }
+    }
+  }
+  __syncthreads();
+  // B: leaves, 8 lanes each (lane k owns numpy's accumulator r[k]: conflict-free
+  // shared-memory rows), combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by shuffles
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane & 7;
+    const int nw = blockDim.x >> 5;
+    for (int L0 = warp * 4; L0 < nleaf; L0 += nw * 4) {
+      const int L = L0 + (lane >> 3);
+      const bool act = L < nleaf;
+      const int lo = act ? leaf_lo[L] : 0, n = act ? leaf_n[L] : 0;
+      double r = 0.0;
+      const int body = n >= 8 ? n - (n % 8) : 0;
+      if (body > 0) {
+        r = a[lo + sub];
+        for (int i = 8; i < body; i += 8) r = __dadd_rn(r, a[lo + i + sub]);
+      }
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+      r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+      if (act && sub == 0) {
+        double res = body > 0 ? r : 0.0;
+        for (int i = body; i < n; ++i) res = __dadd_rn(res, a[lo + i]);
+        V[leaf_v[L]] = res;
+      }
+    }
+  }
+  __syncthreads();
+  // C: internal nodes bottom-up
+  for (int r = rdepth - 1; r >= 0; --r) {
+    const int cnt = 1 << r;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+      const int vi = cnt - 1 + q;
+      if (kind[vi] == 2) {
+        const int ci = 2 * cnt - 1 + 2 * q;
+        V[vi] = __dadd_rn(V[ci], V[ci + 1]);
+      }
     }
     __syncthreads();
   }
@@ -877,6 +908,51 @@ WsLayout ws_layout(int64_t B, int64_t N) {
   return w;
 }
 
+int sweep_variant() {  // FK_PP_SWEEP=pipe selects the persistent cp.async ring (A/B runs)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FK_PP_SWEEP");
+    v = (e && e[0] == 'p') ? 1 : 0;
+  }
+  return v;
+}
+
+template <typename T, int D>
+cudaError_t sweep_fast(const T* Xt, int64_t B, int64_t rows, int d, int64_t x_sb, const T* Ct,
+                       int64_t cen_sb, const int64_t* idx, int64_t K, int64_t col, double* m,
+                       int64_t m_sb, int first, const int32_t* halted, int64_t j, cudaStream_t s,
+                       size_t cbytes, int stride_b) {
+  const size_t tile_b = (size_t)kSweepRows * stride_b;
+  const int se = stride_b / (int)sizeof(T);
+  if (sweep_variant() == 1 && cbytes + 2 * tile_b <= 220 * 1024) {
+    const int stages = cbytes + 3 * tile_b <= 110 * 1024 ? 3 : 2;
+    const size_t sm = cbytes + stages * tile_b;
+    int sms = 148, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int per_sm = stages == 3 ? 2 : 1;
+    const int64_t ntiles = (rows + kSweepRows - 1) / kSweepRows;
+    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm / B));
+    dim3 grid((unsigned)gx, (unsigned)B);
+    if (stages == 3) {
+      cudaFuncSetAttribute(k_pp_sweep_pipe<T, 3, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_pp_sweep_pipe<T, 3, D><<<grid, kSweepRows, sm, s>>>(Xt, rows, d, x_sb, Ct, cen_sb, idx, K, col,
+                                                           m, m_sb, first, halted, j, se);
+    } else {
+      cudaFuncSetAttribute(k_pp_sweep_pipe<T, 2, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      k_pp_sweep_pipe<T, 2, D><<<grid, kSweepRows, sm, s>>>(Xt, rows, d, x_sb, Ct, cen_sb, idx, K, col,
+                                                           m, m_sb, first, halted, j, se);
+    }
+    return cudaGetLastError();
+  }
+  const size_t smem = cbytes + tile_b;
+  cudaFuncSetAttribute(k_pp_sweep<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  dim3 grid((unsigned)((rows + kSweepRows - 1) / kSweepRows), (unsigned)B);
+  k_pp_sweep<T, D><<<grid, kSweepRows, smem, s>>>(Xt, rows, d, x_sb, Ct, cen_sb, idx, K, col, m, m_sb,
+                                                  first, halted, j, se);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t sweep_t(const void* X, int64_t B, int64_t rows, int d, int64_t x_sb, const void* cen,
                     int64_t cen_sb, const int64_t* idx, int64_t K, int64_t col, double* m,
@@ -890,39 +966,25 @@ cudaError_t sweep_t(const void* X, int64_t B, int64_t rows, int d, int64_t x_sb,
   if (rows <= 0) return cudaSuccess;
   const bool vec = (rb & 15) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
                    ((x_sb * (int64_t)sizeof(T)) & 15) == 0;
-  const size_t tile_b = (size_t)kSweepRows * stride_b;
-  static int use_pipe = -1;
-  if (use_pipe < 0) {
-    const char* e = getenv("FK_PP_SWEEP");
-    use_pipe = (e && e[0] == 't') ? 0 : 1;  // FK_PP_SWEEP=tile: the one-shot tile kernel (A/B)
-  }
-  if (use_pipe && vec && cbytes + 2 * tile_b <= 220 * 1024) {
-    const int stages = cbytes + 3 * tile_b <= 110 * 1024 ? 3 : 2;
-    const size_t sm = cbytes + stages * tile_b;
-    int sms = 148;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int per_sm = stages == 3 ? 2 : 1;
-    const int64_t ntiles = (rows + kSweepRows - 1) / kSweepRows;
-    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sms * per_sm / B));
-    dim3 grid((unsigned)gx, (unsigned)B);
-    if (stages == 3) {
-      cudaFuncSetAttribute(k_pp_sweep_pipe<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_pp_sweep_pipe<T, 3><<<grid, kSweepRows, sm, s>>>(Xt, rows, d, x_sb, Ct, cen_sb, idx, K, col, m,
-                                                        m_sb, first, halted, j, stride_b / (int)sizeof(T));
-    } else {
-      cudaFuncSetAttribute(k_pp_sweep_pipe<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      k_pp_sweep_pipe<T, 2><<<grid, kSweepRows, sm, s>>>(Xt, rows, d, x_sb, Ct, cen_sb, idx, K, col, m,
-                                                        m_sb, first, halted, j, stride_b / (int)sizeof(T));
+  if (vec && smem <= 200 * 1024) {
+#define FK_PP_FAST(DV)                                                                          \
+  return sweep_fast<T, DV>(Xt, B, rows, d, x_sb, Ct, cen_sb, idx, K, col, m, m_sb, first, halted, \
+                           j, s, cbytes, stride_b)
+    switch (d) {
+      case 16: FK_PP_FAST(16);
+      case 32: FK_PP_FAST(32);
+      case 64: FK_PP_FAST(64);
+      case 128: FK_PP_FAST(128);
+      default: FK_PP_FAST(0);
     }
-  } else if (smem <= 200 * 1024) {
-    cudaFuncSetAttribute(k_pp_sweep<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+#undef FK_PP_FAST
+  }
+  if (smem <= 200 * 1024) {
+    cudaFuncSetAttribute(k_pp_sweep<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     dim3 grid((unsigned)((rows + kSweepRows - 1) / kSweepRows), (unsigned)B);
-    k_pp_sweep<T><<<grid, kSweepRows, smem, s>>>(Xt, rows, d, x_sb, Ct, cen_sb, idx, K, col, m, m_sb,
-                                                 first, halted, j, stride_b / (int)sizeof(T));
-  } else if ((rb & 15) == 0 && (reinterpret_cast<uintptr_t>(X) & 15) == 0 &&
-             ((x_sb * (int64_t)sizeof(T)) & 15) == 0 && cbytes <= 200 * 1024) {
+    k_pp_sweep<T, 0><<<grid, kSweepRows, smem, s>>>(Xt, rows, d, x_sb, Ct, cen_sb, idx, K, col, m,
+                                                    m_sb, first, halted, j, stride_b / (int)sizeof(T));
+  } else if (vec && cbytes <= 200 * 1024) {
     cudaFuncSetAttribute(k_pp_sweep_global<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     dim3 grid((unsigned)((rows + 127) / 128), (unsigned)B);
     k_pp_sweep_global<T><<<grid, 128, cbytes, s>>>(Xt, rows, d, x_sb, Ct, cen_sb, idx, K, col, m,
