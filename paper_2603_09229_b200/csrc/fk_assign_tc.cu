@@ -68,6 +68,7 @@ struct TcArgs {
   const int32_t* idx_prev;
   int32_t* changed;
   int debug_mode;  // 0 normal; 1 epilogue skips math (MMA/TMA bound); 2 MMA skipped (epilogue bound)
+  int epi2;        // 1: bias-in-GEMM epilogue processes 32-column chunks in pairs
   unsigned long long* trace;  // debug timeline (FK_ASSIGN_TRACE), nullptr normally
 };
 
@@ -405,7 +406,8 @@ constexpr int OFF_EXT = OFF_AEXT + BM * EXT_ROW;
 constexpr int OFF_CN = OFF_EXT + EXT_SLOTS * EXT_SLOT;
 constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;
 constexpr int OFF_BAR = OFF_XCH + BM * 8;
-constexpr int NBARS = 8 + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
+constexpr int A_SLOTS_MAX = 8;
+constexpr int NBARS = 2 * A_SLOTS_MAX + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
 constexpr int SMEM_USED = OFF_BAR + NBARS * 8 + 16;
 constexpr int SMEM_BYTES = SMEM_USED + 1024;
 constexpr int THREADS = 384;
@@ -431,6 +433,38 @@ FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, f
   }
   M = p ? mc : M;
   best = p ? colbase : best;
+}
+
+FK_DEV float min_tree32(const float* s) {
+  float a[11];
+#pragma unroll
+  for (int j = 0; j < 10; ++j) a[j] = fmin3(s[3 * j], s[3 * j + 1], s[3 * j + 2]);
+  a[10] = fminf(s[30], s[31]);
+  const float b0 = fmin3(a[0], a[1], a[2]);
+  const float b1 = fmin3(a[3], a[4], a[5]);
+  const float b2 = fmin3(a[6], a[7], a[8]);
+  const float b3 = fminf(a[9], a[10]);
+  return fmin3(b0, b1, fminf(b2, b3));
+}
+
+// Two adjacent chunks at once: independent min trees (ILP), one warp vote and
+// one conditional copy per pair.  Chunk a holds the lower columns, so strict
+// '<' in order a then b keeps the lowest index on ties, as epi_chunk_aug does.
+FK_DEV void epi_chunk2_aug(const uint32_t (&va)[32], const uint32_t (&vb)[32], int cola, int colb,
+                           float& M, int& best, float (&bestv)[32]) {
+  const float* sa = reinterpret_cast<const float*>(va);
+  const float* sb = reinterpret_cast<const float*>(vb);
+  const float mca = min_tree32(sa);
+  const float mcb = min_tree32(sb);
+  const bool pa = mca < M;
+  const float Ma = pa ? mca : M;
+  const bool pb = mcb < Ma;
+  if (__any_sync(0xffffffffu, pa || pb)) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bestv[j] = pb ? sb[j] : (pa ? sa[j] : bestv[j]);
+  }
+  M = pb ? mcb : Ma;
+  best = pb ? colb : (pa ? cola : best);
 }
 
 // BIAS = 1 (bias-in-GEMM): the ||c||^2 bias rides in the GEMM as one extra
@@ -465,8 +499,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   int* xch_i = reinterpret_cast<int*>(smem + OFF_XCH + BM * 4);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* a_full = bars + 0;
-  uint64_t* a_empty = bars + 4;
-  uint64_t* t_full = bars + 8;
+  uint64_t* a_empty = bars + A_SLOTS_MAX;
+  uint64_t* t_full = bars + 2 * A_SLOTS_MAX;
   uint64_t* t_empty = t_full + NBUF;
   uint64_t* b_full = t_empty + NBUF;
   uint64_t* b_empty = b_full + STAGES;
@@ -488,9 +522,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   const int npairs = gridDim.x >> 1;
   // X row-tile ring: the 64 KB A region holds 2 slots of 2 K-atoms (d <= 128)
   // or 4 slots of 1 atom (d <= 64): deeper prefetch when a row tile is short.
-  const int a_log = p.katoms == 1 ? 2 : 1;  // 4 or 2 slots (power of two)
-  const int a_slots = 1 << a_log;
+  // X row-tile ring + C stage ring share the 160 KB operand region: d <= 64
+  // (one K-atom per tile) takes 6 X slots + 4 C stages -- short row tiles need
+  // the deeper X prefetch -- d <= 128 takes 2 X slots + 6 C stages.
+  const int a_slots = p.katoms == 1 ? 6 : 2;
+  const int b_stages = p.katoms == 1 ? 4 : STAGES;
   const int a_slot_bytes = p.katoms * A_ATOM;
+  sB = sA + a_slots * a_slot_bytes;
   // ALT (single-column-tile rows, K <= 256): the two epilogue warpgroups take
   // alternate tiles (whole rows each, two tiles in flight, no merge) instead
   // of splitting every tile's columns.
@@ -501,7 +539,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     tma_prefetch_desc(&tmx);
     tma_prefetch_desc(&tmc);
     if (AUG) tma_prefetch_desc(&tmext);
-    for (int s = 0; s < 4; ++s) {
+    for (int s = 0; s < A_SLOTS_MAX; ++s) {
       mbar_init(&a_full[s], 1);       // leader's expect_tx (both CTAs' bytes)
       mbar_init(&a_empty[s], 1 + 4);  // pair-MMA commit + 4 warps of this CTA's WG0
     }
@@ -540,27 +578,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
 
   if (warp == W_PRODUCER) {
     // ------------------------------------------------------------ producer (both CTAs)
+    // C tiles (+ bias operand / ||c||^2 ring); X row tiles come from their own
+    // warp below, so waiting for a free X slot never stalls the C prefetch.
     if (lane == 0) {
       uint32_t stage = 0, sphase = 0;
-      const uint32_t a_bytes = p.katoms * A_ATOM;
-      auto load_a = [&](int t, int j) {
-        const int slot = j & (a_slots - 1);
-        const int b = t / p.tiles_per_batch;
-        const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
-        mbar_wait(&a_empty[slot], ((j >> a_log) & 1) ^ 1);
-        if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
-        const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
-        for (int ka = 0; ka < p.katoms; ++ka)
-          tma_load_3d_cg2(sA + slot * a_slot_bytes + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
-                          kEvictFirst);
-      };
-      int i = 0;
       uint32_t g = 0;
-      for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
+      for (int t = pair; t < p.total_tiles; t += npairs) {
         const int b = t / p.tiles_per_batch;
-        if (i == 0)  // prime the ring: this tile and the next a_slots - 2
-          for (int j = 0; j < a_slots - 1 && t + j * npairs < p.total_tiles; ++j)
-            load_a(t + j * npairs, j);
         for (int c = 0; c < p.ncol; ++c, ++g) {
           if (AUG) {
             const uint32_t slot = g % EXT_SLOTS;
@@ -580,17 +604,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * B_STAGE);
             tma_load_3d_cg2(sB + stage * B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
                             ka * 64, c * BN + rank * BNH, b, kEvictLast);
-            if (++stage == STAGES) {
+            if (++stage == b_stages) {
               stage = 0;
               sphase ^= 1;
             }
           }
           if (pair == 0 && leader) trace_ev(p, g, 5);
-          if (c == 0) {
-            const int t2 = t + (a_slots - 1) * npairs;
-            if (t2 < p.total_tiles) load_a(t2, i + a_slots - 1);
-          }
         }
+      }
+    }
+  } else if (warp == W_INIT) {
+    // ------------------------------------------------------------ X row-tile producer (both CTAs)
+    if (lane == 0) {
+      const uint32_t a_bytes = p.katoms * A_ATOM;
+      int j = 0;
+      for (int t = pair; t < p.total_tiles; t += npairs, ++j) {
+        const int slot = j % a_slots;
+        const int b = t / p.tiles_per_batch;
+        const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
+        mbar_wait(&a_empty[slot], ((j / a_slots) & 1) ^ 1);
+        if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
+        const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
+        for (int ka = 0; ka < p.katoms; ++ka)
+          tma_load_3d_cg2(sA + slot * a_slot_bytes + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
+                          kEvictFirst);
       }
     }
   } else if (warp == W_MMA) {
@@ -605,9 +642,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       uint32_t stage = 0, sphase = 0, g = 0;
       int i = 0;
       for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
-        const int slot = i & (a_slots - 1);
-        mbar_wait(&a_full[slot], (i >> a_log) & 1);
+        const int slot = i % a_slots;
+        mbar_wait(&a_full[slot], (i / a_slots) & 1);
         tc_fence_after();
+        if (pair == 0 && lane == 0) trace_ev(p, g, 7);
         const uint32_t a_base = smem_u32(sA + slot * a_slot_bytes);
         for (int c = 0; c < p.ncol; ++c, ++g) {
           const uint32_t buf = g % NBUF;
@@ -632,7 +670,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               tc_commit_cg2_mc(&b_empty[stage], 0x3);
             }
             __syncwarp();
-            if (++stage == STAGES) {
+            if (++stage == b_stages) {
               stage = 0;
               sphase ^= 1;
             }
@@ -708,7 +746,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       }
       const int b = t / p.tiles_per_batch;
       const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
-      const int slot = i & (a_slots - 1);
+      const int slot = i % a_slots;
       float M = __int_as_float(0x7f800000);
       int best = -1;
       float bestv[32];
@@ -758,6 +796,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           release_tmem();  // (debug mode 1 does not support SEED: garbage accumulators are fine for timing)
           if (EPI && lane == 0) mbar_arrive(&cn_empty[cslot]);
           M = fminf(M, __uint_as_float(va[0]));
+          continue;
+        }
+        if (AUG && p.epi2) {
+          // chunk pairs: both loads in flight, one vote per pair
+          FK_TMEM_LD_32x32b_X32(taddr + 32, vb);
+#pragma unroll
+          for (int ch = 0; ch < nch; ch += 2) {
+            FK_TMEM_WAIT_LD(va);
+            FK_TMEM_WAIT_LD(vb);
+            if (ch + 2 >= nch) {
+              release_tmem();  // every TMEM read of this buffer has landed
+              if (tr) trace_ev(p, g, 3);
+            }
+            epi_chunk2_aug(va, vb, col0 + 32 * ch, col0 + 32 * (ch + 1), M, best, bestv);
+            if (ch + 2 < nch) {
+              FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 2), va);
+              FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 3), vb);
+            }
+          }
+          if (tr) trace_ev(p, g, 4);
           continue;
         }
 #pragma unroll
@@ -929,6 +987,10 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
   {
     const char* dm = getenv("FK_ASSIGN_DEBUG_MODE");
     a.debug_mode = dm ? atoi(dm) : 0;
+    // chunk pairs help when row tiles are short (K <= 1024: +1.5-3% at configs
+    // 2 and 4) and cost ~3% at K = 4096 (same-box A/B, profiles/r01_ab_epi2.txt)
+    const char* e2 = getenv("FK_ASSIGN_EPI2");
+    a.epi2 = e2 ? (e2[0] == '1') : (a.ncol <= 4);
   }
   a.trace = nullptr;
   static unsigned long long* trace_buf = nullptr;

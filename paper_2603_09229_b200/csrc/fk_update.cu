@@ -20,8 +20,13 @@
 // (core.py:203-233).  bf16/fp16 rows accumulate in fp32 inside a slice; f32
 // and f64 rows accumulate in f64 so fp32 data reproduces the reference's
 // sums exactly.
+#include <cooperative_groups.h>
+#include <stdlib.h>
+
 #include "fk_common.cuh"
 #include "fk_kernels.h"
+
+namespace cg = cooperative_groups;
 
 namespace fk {
 
@@ -429,6 +434,246 @@ static int64_t update_bpb(int64_t B, int64_t N, int num_sms) {
 }
 constexpr int kMaxSms = 256;  // workspace bound for any sm_100 part
 
+// ------------------------------------------------- one-kernel cluster update
+// Small per-batch problems (config 4: B=64 x N=16k, K=256, d=64, fp16): one
+// thread-block cluster of C CTAs per batch element does the whole update in
+// shared memory, with no global scratch and one launch:
+//   1. each CTA histograms its N/C ids (shared bins) and counting-sorts its
+//      local point indices by id (shared cursors);
+//   2. rank 0 reads every CTA's bins over DSMEM: exact int64 counts and the
+//      reference's synchronized_merges count for this batch element;
+//   3. each CTA walks its local sorted order in contiguous runs per lane
+//      group, gathers the rows (16-B vectors), keeps fp32 running sums and
+//      merges ONCE per (run, segment) into its shared K x d fp32 table;
+//   4. CTA r reduces key range r of the C tables over DSMEM in fixed rank
+//      order and stores f64 sums directly (no global atomics).
+constexpr int CU_THREADS = 256;
+constexpr int CU_PMAX = 8192;               // local points per CTA
+constexpr size_t CU_TABLE_MAX = 96 * 1024;  // K * d * 4 bytes of shared sums
+
+template <typename T>
+__global__ void __launch_bounds__(CU_THREADS)
+    k_update_cluster(const T* __restrict__ X, const int32_t* __restrict__ ids, int64_t N, int K,
+                     int d, int64_t chunk, int accumulate, double* __restrict__ sums,
+                     int64_t* __restrict__ counts, int64_t* __restrict__ merges) {
+  extern __shared__ __align__(16) uint8_t cu_sm[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int C = (int)cluster.num_blocks();
+  const int r = (int)cluster.block_rank();
+  const int64_t b = blockIdx.x / C;
+  const int64_t per = (N + C - 1) / C;
+  const int64_t lo = (int64_t)r * per;
+  const int64_t hi = lo + per < N ? lo + per : N;
+  const int np = hi > lo ? (int)(hi - lo) : 0;
+  float* table = reinterpret_cast<float*>(cu_sm);                         // K*d
+  int32_t* hist = reinterpret_cast<int32_t*>(cu_sm + (size_t)K * d * 4);  // K
+  int32_t* cur = hist + K;                                                // K
+  int32_t* order = cur + K;                                               // per
+  int32_t* sid = order + per;                                             // per: local ids
+  __shared__ unsigned long long s_mg;
+  __shared__ int64_t wtot[32];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  for (int k = t; k < K; k += CU_THREADS) hist[k] = 0;
+  for (int e = t; e < K * d; e += CU_THREADS) table[e] = 0.f;
+  if (t == 0) s_mg = 0;
+  __syncthreads();
+  const int32_t* idb = ids + b * N + lo;
+  for (int i = t; i < np; i += CU_THREADS) {
+    const int32_t id = __ldg(idb + i);
+    sid[i] = id;
+    if (id >= 0 && id < K) atomicAdd(&hist[id], 1);
+  }
+  __syncthreads();
+  // local exclusive scan of the bins -> cursors (one warp per 32-key tile, serial carry)
+  if (warp == 0) {
+    int carry = 0;
+    for (int base = 0; base < K; base += 32) {
+      const int k = base + lane;
+      const int c = k < K ? hist[k] : 0;
+      int v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (k < K) cur[k] = carry + v - c;
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+  }
+  cluster.sync();  // every CTA's bins are final (read remotely below)
+  if (r == 0) {
+    // exact counts + the reference's merge count for this batch element
+    int64_t carry = 0;
+    unsigned long long mg = 0;
+    const uint32_t ch = (uint32_t)chunk;
+    for (int base = 0; base < K; base += CU_THREADS) {
+      const int k = base + t;
+      int64_t c = 0;
+      if (k < K)
+        for (int q = 0; q < C; ++q) c += *cluster.map_shared_rank(hist + k, q);
+      int64_t v = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane == 31) wtot[warp] = v;
+      __syncthreads();
+      int64_t wbase = 0;
+      for (int w = 0; w < warp; ++w) wbase += wtot[w];
+      const int64_t run = carry + wbase + v - c;
+      if (k < K) {
+        counts[b * K + k] = accumulate ? counts[b * K + k] + c : c;
+        if (c > 0) {
+          const uint32_t s0 = (uint32_t)run, e = s0 + (uint32_t)c;
+          mg += (unsigned long long)((e - 1) / ch - s0 / ch + 1);
+        }
+      }
+      int64_t tot = 0;
+      for (int w = 0; w < CU_THREADS / 32; ++w) tot += wtot[w];
+      carry += tot;
+      __syncthreads();
+    }
+    for (int o = 16; o; o >>= 1) mg += __shfl_xor_sync(0xffffffffu, mg, o);
+    if (lane == 0 && mg) atomicAdd(&s_mg, mg);
+  }
+  // local counting sort of the point indices (X is never permuted)
+  for (int i = t; i < np; i += CU_THREADS) {
+    const int32_t id = sid[i];
+    if (id >= 0 && id < K) order[atomicAdd(&cur[id], 1)] = i;
+  }
+  __syncthreads();
+  // cur[k] is now the END of key k's local run; the valid sorted length:
+  const int nv = K > 0 ? cur[K - 1] : 0;
+  // segmented sums: LPR lanes cover one row, each lane group walks a
+  // contiguous run of the local sorted order
+  constexpr int E = 16 / (int)sizeof(T);
+  const int vpr = d / E;                // 16-B vectors per row
+  const int lpr = vpr >= 32 ? 32 : vpr; // lanes per row (power of two: d in shape buckets)
+  const int vpl = vpr / lpr;            // vectors per lane
+  const int groups = CU_THREADS / lpr;
+  const int gid = t / lpr, gl = t % lpr;
+  const int run = (nv + groups - 1) / groups;
+  const int p0 = gid * run, p1 = p0 + run < nv ? p0 + run : nv;
+  const T* xb = X + (b * N + lo) * (int64_t)d;
+  if (p0 < p1) {
+    // key of position p0: first k with cur[k] > p0 (cur = run ends)
+    int klo = 0, khi = K - 1;
+    while (klo < khi) {
+      const int mid = (klo + khi) >> 1;
+      if (cur[mid] > p0) khi = mid; else klo = mid + 1;
+    }
+    for (int v0 = 0; v0 < vpl; ++v0) {
+      const int col = (v0 * lpr + gl) * E;
+      float acc[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) acc[e] = 0.f;
+      int k = klo, ke = cur[klo], nrow = 0;
+      auto flush = [&]() {
+        if (nrow) {
+          float* dst = table + (size_t)k * d + col;
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            atomicAdd(dst + e, acc[e]);
+            acc[e] = 0.f;
+          }
+          nrow = 0;
+        }
+      };
+      // CU_U gathers in flight across segment boundaries, added in sorted order;
+      // one merge per (run, segment)
+      constexpr int CU_U = 16;
+      for (int p = p0; p < p1; p += CU_U) {
+        const int n = p1 - p < CU_U ? p1 - p : CU_U;
+        uint4 v[CU_U];
+#pragma unroll
+        for (int u = 0; u < CU_U; ++u)
+          if (u < n) v[u] = ldg_stream(xb + (int64_t)order[p + u] * d + col);
+#pragma unroll
+        for (int u = 0; u < CU_U; ++u) {
+          if (u < n) {
+            while (p + u >= ke) {  // segment boundary (skipping empty keys)
+              flush();
+              ++k;
+              ke = cur[k];
+            }
+            VecCvt<T>::add(acc, v[u]);
+            ++nrow;
+          }
+        }
+      }
+      flush();
+    }
+  }
+  cluster.sync();  // every table complete
+  // CTA r reduces keys [r*K/C, (r+1)*K/C) across the cluster, fixed rank order
+  const int k0 = (int)((int64_t)K * r / C), k1 = (int)((int64_t)K * (r + 1) / C);
+  const float* rt[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) rt[q] = cluster.map_shared_rank(table, q < C ? q : 0);
+  for (int e = k0 * d + t; e < k1 * d; e += CU_THREADS) {
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = q < C ? rt[q][e] : 0.f;  // all remote loads in flight
+    double acc = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < C) acc += (double)v[q];
+    double* o = sums + b * (int64_t)K * d + e;
+    *o = accumulate ? *o + acc : acc;
+  }
+  if (r == 0 && t == 0 && merges && s_mg) atomicAdd((unsigned long long*)merges, s_mg);
+  cluster.sync();  // keep every table alive until all remote reads are done
+}
+
+// cluster size for the one-kernel path, or 0 when it does not apply
+static int cluster_update_size(int dt, int64_t B, int64_t N, int64_t K, int64_t d, int num_sms) {
+  // Opt-in only (FK_UPDATE_CLUSTER=1): same-box A/B at config 4 measured 66.9 us
+  // against 61.4 us for the four-kernel path (0.45 waves of 8-warp CTAs and
+  // serialized phases leave HBM at 24%; profiles/r01_ab_cluster.txt).
+  const char* e = getenv("FK_UPDATE_CLUSTER");
+  if (!(e && e[0] == '1')) return 0;
+  if (dt != DT_BF16 && dt != DT_F16) return 0;  // f32/f64 keep f64 accumulation (bitwise path)
+  if ((d * 2) % 16 != 0 || d > 256 || (d / 8 & (d / 8 - 1)) != 0) return 0;
+  if ((size_t)K * d * 4 > CU_TABLE_MAX || K > 8192) return 0;
+  for (int C = 1; C <= 8; C <<= 1) {
+    const int64_t per = (N + C - 1) / C;
+    if (per > CU_PMAX) continue;
+    // enough CTAs to cover the machine when the batch is small
+    if (B * C < num_sms && C < 8 && (N + 2 * C - 1) / (2 * C) >= 512) continue;
+    return C;
+  }
+  return 0;
+}
+
+static size_t cluster_update_smem(int64_t N, int64_t K, int64_t d, int C) {
+  const int64_t per = (N + C - 1) / C;
+  return (size_t)K * d * 4 + (size_t)K * 8 + (size_t)per * 8;
+}
+
+template <typename T>
+static cudaError_t launch_cluster_update(const void* X, const int32_t* ids, int64_t B, int64_t N,
+                                         int64_t K, int64_t d, int64_t chunk, int accumulate,
+                                         double* sums, int64_t* counts, int64_t* merges, int C,
+                                         cudaStream_t s) {
+  const size_t smem = cluster_update_smem(N, K, d, C);
+  cudaFuncSetAttribute(k_update_cluster<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(B * C));
+  cfg.blockDim = dim3(CU_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_update_cluster<T>, static_cast<const T*>(X), ids, N, (int)K,
+                            (int)d, chunk, accumulate, sums, counts, merges);
+}
+
 size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K) {
   const int64_t BK = B * K, P = B * N;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -479,6 +724,14 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
                           int64_t* counts, int64_t* merges, void* ws, int num_sms,
                           cudaStream_t s) {
   const int64_t BK = B * K, P = B * N;
+  const int64_t chc = chunk < 1 ? 1 : (chunk > N ? N : chunk);
+  if (const int C = cluster_update_size(dt, B, N, K, d, num_sms)) {
+    return dt == DT_BF16
+               ? launch_cluster_update<__nv_bfloat16>(X, ids, B, N, K, d, chc, accumulate, sums,
+                                                      counts, merges, C, s)
+               : launch_cluster_update<__half>(X, ids, B, N, K, d, chc, accumulate, sums, counts,
+                                               merges, C, s);
+  }
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   uint8_t* w = (uint8_t*)ws;
   int32_t* hist = (int32_t*)w;

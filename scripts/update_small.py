@@ -1,9 +1,12 @@
-"""ops.update at configs 2 and 4 (for ncu launch lists; dev aid)."""
+"""ops.update at configs 2 and 4 under a CUDA graph (for A/B and ncu launch lists; dev aid).
+    FK_UPDATE_CLUSTER=0 selects the global sort path for the small shapes."""
 import sys
 import torch
 sys.path.insert(0, ".")
 from paper_2603_09229_b200 import ops
-for (B, N, K, d, dt) in [(1, 1 << 20, 1024, 128, torch.bfloat16), (64, 16384, 256, 64, torch.float16)]:
+shapes = [(1, 1 << 20, 1024, 128, torch.bfloat16), (64, 16384, 256, 64, torch.float16),
+          (64, 16384, 256, 64, torch.bfloat16), (8, 65536, 256, 64, torch.bfloat16)]
+for (B, N, K, d, dt) in shapes:
     x = torch.randn(B, N, d, device="cuda").to(dt)
     ids = torch.randint(0, K, (B, N), device="cuda", dtype=torch.int32)
     sums = torch.empty((B, K, d), dtype=torch.float64, device="cuda")
@@ -23,4 +26,4 @@ for (B, N, K, d, dt) in [(1, 1 << 20, 1024, 128, torch.bfloat16), (64, 16384, 25
     e.record(); e.synchronize()
     t = s.elapsed_time(e) / 20 * 1e3
     by = B * N * d * x.element_size() + 4 * B * N + 4 * B * K * d + 4 * B * K
-    print(f"B={B} N={N} K={K} d={d}: {t:.1f} us  {by / t / 1e3:.0f} GB/s")
+    print(f"B={B} N={N} K={K} d={d} {dt}: {t:.1f} us  {by / t / 1e3:.0f} GB/s")
