@@ -182,10 +182,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # FK_BENCH_SHARE_GPU=1 + FK_DIST_BACKEND=gloo: every rank on cuda:0 (a
+    # one-GPU rehearsal of the multi-rank code path; numbers are not scaling data)
+    if os.environ.get("FK_BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("FK_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     lo, hi = shard_bounds(N_TOTAL, world, rank)
     n_local = hi - lo
     x = make_shard(n_local, rank, dev)
@@ -222,13 +230,7 @@ def run_ours(args):
         if timers is not None:
             timers[3].record(stream)
         if eng.allreduce is not None:
-            eng.counts_f.copy_(eng.counts)
-            eng.obj_red.copy_(eng.obj)
-            eng.changed_f.copy_(eng.changed)
-            eng.allreduce(eng.red)
-            eng.counts.copy_(eng.counts_f)
-            eng.obj.copy_(eng.obj_red)
-            eng.changed.copy_((eng.changed_f[0] > 0).to(torch.int32))
+            eng.exchange()
         nxt = eng.cur ^ 1
         ops.normalize(eng.sums, eng.counts, eng.master[eng.cur], out=eng.master[nxt],
                       operand_out=eng.operand[nxt] if eng.operand is not eng.master else None,

@@ -141,6 +141,15 @@ FK_API fk_status fk_objective(fk_dtype mind_dt, const void* mind, int64_t B, int
 FK_API fk_status fk_scatter(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
                      int64_t K, int64_t d, double* sums, int64_t* counts, void* stream);
 
+/* ------------------------------------------------------ multi-GPU exchange
+ * Packs (unpack = 0) counts (B*K int64), objective (B f64) and the changed
+ * flag (int32) behind the sums in the single f64 all-reduce buffer
+ * red = [sums (B*K*d) | counts | objective | changed] -- `red` points at the
+ * counts part -- or unpacks the reduced values (changed = sum > 0).  One launch
+ * each way around the per-iteration NCCL all-reduce of the point-sharded path. */
+FK_API fk_status fk_stats_pack(int32_t unpack, int64_t* counts, double* objective, int32_t* changed,
+                               double* red, int64_t BK, int64_t B, void* stream);
+
 /* ------------------------------------------------------------- k-means++
  * D^2 seeding of init_centroids(method="kmeanspp") on the device:
  *   fk_kmeanspp        <- _kmeanspp_indices      core.py:342-357

@@ -207,6 +207,14 @@ fk_status fk_scatter(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, 
                                         reinterpret_cast<cudaStream_t>(stream)));
 }
 
+// ------------------------------------------------------ multi-GPU exchange
+fk_status fk_stats_pack(int32_t unpack, int64_t* counts, double* objective, int32_t* changed,
+                        double* red, int64_t BK, int64_t B, void* stream) {
+  if (!counts || !objective || !changed || !red || BK < 1 || B < 1) return FK_EINVAL;
+  return cuda_status(fk::launch_stats_pack(unpack ? 1 : 0, counts, objective, changed, red, BK, B,
+                                           reinterpret_cast<cudaStream_t>(stream)));
+}
+
 // ------------------------------------------------------------- k-means++
 size_t fk_kmeanspp_workspace(int64_t B, int64_t N) {
   if (B < 1 || N < 1 || B * N > kMaxPoints) return 0;

@@ -53,6 +53,9 @@ cudaError_t launch_scatter(int dt, const void* X, const int32_t* ids, int64_t B,
                            int64_t K, int64_t d, double* sums, int64_t* counts,
                            cudaStream_t stream);
 
+cudaError_t launch_stats_pack(int unpack, int64_t* counts, double* obj, int32_t* changed,
+                              double* red, int64_t BK, int64_t B, cudaStream_t s);
+
 // fk_kmeanspp.cu
 size_t kmeanspp_workspace_bytes(int64_t B, int64_t N);
 cudaError_t launch_kmeanspp_init(int32_t* halted, void* ws, int64_t B, int64_t N, int64_t K,

@@ -674,6 +674,36 @@ static cudaError_t launch_cluster_update(const void* X, const int32_t* ids, int6
                             (int)d, chunk, accumulate, sums, counts, merges);
 }
 
+// --------------------------------------------- multi-GPU exchange packing
+// The per-iteration all-reduce moves ONE f64 buffer [sums | counts | obj | changed]
+// (distributed.py); counts are exact in f64 below 2^53.  One launch each way.
+__global__ void k_stats_pack(const int64_t* __restrict__ counts, const double* __restrict__ obj,
+                             const int32_t* __restrict__ changed, double* __restrict__ red,
+                             int64_t BK, int64_t B) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < BK) red[i] = (double)counts[i];
+  else if (i < BK + B) red[i] = obj[i - BK];
+  else if (i == BK + B) red[i] = (double)*changed;
+}
+__global__ void k_stats_unpack(const double* __restrict__ red, int64_t* __restrict__ counts,
+                               double* __restrict__ obj, int32_t* __restrict__ changed, int64_t BK,
+                               int64_t B) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < BK) counts[i] = (int64_t)red[i];
+  else if (i < BK + B) obj[i - BK] = red[i];
+  else if (i == BK + B) *changed = red[i] > 0.0 ? 1 : 0;
+}
+cudaError_t launch_stats_pack(int unpack, int64_t* counts, double* obj, int32_t* changed,
+                              double* red, int64_t BK, int64_t B, cudaStream_t s) {
+  const int64_t n = BK + B + 1;
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  if (unpack)
+    k_stats_unpack<<<grid, 256, 0, s>>>(red, counts, obj, changed, BK, B);
+  else
+    k_stats_pack<<<grid, 256, 0, s>>>(counts, obj, changed, red, BK, B);
+  return cudaGetLastError();
+}
+
 size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K) {
   const int64_t BK = B * K, P = B * N;
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };

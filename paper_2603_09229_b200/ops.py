@@ -261,3 +261,13 @@ class KmeansppStream:
                                         int(j), self.idx.data_ptr(), self.halted.data_ptr(),
                                         self.ws.data_ptr(), self.ws.numel(), _stream(self.dev))
         N.check(st, "fk_kmeanspp_select")
+
+
+def stats_pack(counts: torch.Tensor, obj: torch.Tensor, changed: torch.Tensor, red_tail: torch.Tensor,
+               unpack: bool = False) -> None:
+    """[counts | objective | changed] <-> the f64 tail of the all-reduce buffer (one launch)."""
+    dev = _require_cuda(counts, obj, changed, red_tail)
+    BK, B = counts.numel(), obj.numel()
+    st = N.lib().fk_stats_pack(1 if unpack else 0, counts.data_ptr(), obj.data_ptr(), changed.data_ptr(),
+                               red_tail.data_ptr(), BK, B, _stream(dev))
+    N.check(st, "fk_stats_pack")

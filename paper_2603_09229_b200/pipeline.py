@@ -174,17 +174,29 @@ class LloydEngine:
         self.be.update(self.x, self.ids[slot], self.K, self.chunk, sums=self.sums, counts=self.counts,
                    merges=self.merges_it)
         if self.allreduce is not None:
-            self.counts_f.copy_(self.counts)
-            self.obj_red.copy_(self.obj)
-            self.changed_f.copy_(self.changed)
-            self.allreduce(self.red)
-            self.counts.copy_(self.counts_f)
-            self.obj.copy_(self.obj_red)
-            self.changed.copy_((self.changed_f[0] > 0).to(torch.int32))
+            self.exchange()
         nxt = self.cur ^ 1
         self.be.normalize(self.sums, self.counts, self.master[self.cur], out=self.master[nxt],
                           operand_out=None if self.operand is self.master else self.operand[nxt],
                           empty=self.empty, shift2=self.shift2)
+
+    def exchange(self) -> None:
+        """Combine the point shards: pack [counts | objective | changed] behind the
+        sums, one in-place all-reduce of the f64 buffer, unpack (distributed.py)."""
+        tail = self.red[self.B * self.K * self.d:]
+        if hasattr(self.be, "stats_pack"):
+            self.be.stats_pack(self.counts, self.obj, self.changed, tail)
+        else:
+            self.counts_f.copy_(self.counts)
+            self.obj_red.copy_(self.obj)
+            self.changed_f.copy_(self.changed)
+        self.allreduce(self.red)
+        if hasattr(self.be, "stats_pack"):
+            self.be.stats_pack(self.counts, self.obj, self.changed, tail, unpack=True)
+        else:
+            self.counts.copy_(self.counts_f)
+            self.obj.copy_(self.obj_red)
+            self.changed.copy_((self.changed_f[0] > 0).to(torch.int32))
 
     def poll(self):
         """(changed: bool, shift: float) -- the one device->host read per iteration."""
