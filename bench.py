@@ -211,36 +211,32 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
-    def step(timers=None):
-        # LloydEngine.iterate split into its phases so the kernels can be timed live
-        slot = eng.it & 1
-        eng.changed.zero_()
-        eng.shift2.zero_()
-        eng.merges_it.zero_()
-        if timers is not None:
-            timers[0].record(stream)
-        eng.assign(slot, eng.it > 0)
-        if timers is not None:
-            timers[1].record(stream)
-        ops.objective(eng.mind, out=eng.obj)
-        if timers is not None:
-            timers[2].record(stream)
-        ops.update(eng.x, eng.ids[slot], eng.K, eng.chunk, sums=eng.sums, counts=eng.counts,
-                   merges=eng.merges_it)
-        if timers is not None:
-            timers[3].record(stream)
-        if eng.allreduce is not None:
-            eng.exchange()
-        nxt = eng.cur ^ 1
-        ops.normalize(eng.sums, eng.counts, eng.master[eng.cur], out=eng.master[nxt],
-                      operand_out=eng.operand[nxt] if eng.operand is not eng.master else None,
-                      empty=eng.empty, shift2=eng.shift2)
-        eng.it += 1
-        eng.poll()
-        eng.commit()
+    # One step = one Lloyd iteration as lloyd_run executes it (LloydEngine.run):
+    # the next assign is queued before the host reads this iteration's flags,
+    # so the GPU does not idle on the poll.  Phases are timed live with events
+    # on the launching stream (eager launches, no graphs, so events can sit
+    # between the kernels).
+    eng.use_graphs = False
 
-    for _ in range(args.warmup):
-        step()
+    def run_steps(n, timers=None):
+        def t(s, k):
+            if timers is not None:
+                timers[s][k].record(stream)
+        t(0, 0)
+        eng.enq_assign(eng.it & 1, eng.it > 0, eng.cur)
+        t(0, 1)
+        for s in range(n):
+            slot = eng.it & 1
+            eng.enq_rest(slot, None, None if timers is None else timers[s][2:4])
+            eng.it += 1
+            if s + 1 < n:  # speculative: the run continues unless the flags say stop
+                t(s + 1, 0)
+                eng.enq_assign(eng.it & 1, True, eng.cur ^ 1)
+                t(s + 1, 1)
+            eng.wait_flags()  # the poll (changed, shift) every iteration reads
+            eng.cur ^= 1  # commit
+
+    run_steps(args.warmup)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -253,8 +249,7 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         t0.record(stream)
-        for s in range(args.steps):
-            step(timers[s])
+        run_steps(args.steps, timers)
         t1.record(stream)
         torch.cuda.synchronize()
         if world > 1:

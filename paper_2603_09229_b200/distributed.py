@@ -70,18 +70,14 @@ def lloyd_run_sharded(x_shard: torch.Tensor, total_points: int, lo: int, cfg: KM
     eng.set_centroids(init_centroids_sharded(x_shard, total_points, lo, cfg.clusters, cfg.seed,
                                              cfg.init, group))
     history = torch.empty((cfg.max_iters, eng.B), dtype=torch.float64, device=x_shard.device)
-    iterations = 0
-    slot = 0
-    for it in range(1, cfg.max_iters + 1):
-        iterations = it
-        slot = eng.iterate(history[it - 1])
-        changed, shift = eng.poll()
-        if it > 1 and not changed:
-            break
-        eng.commit()
-        if shift <= cfg.shift_tol:
-            break
-    counters.synchronized_merges += int(eng.merges.item())
+    # every rank takes the same decisions: the flags are reduced in the exchange
+    iterations, slot, merges = eng.run(cfg.max_iters, cfg.shift_tol, history)
+    if x_shard.is_cuda:
+        torch.cuda.synchronize(x_shard.device)
+    # merges: each rank counted its own shard's segments; the reference count is global
+    mg = torch.tensor([float(merges)], dtype=torch.float64, device=x_shard.device)
+    dist.all_reduce(mg, op=dist.ReduceOp.SUM, group=group)
+    counters.synchronized_merges += int(mg.item())
     return KMeansResult(Centroids(eng.centroids.clone(), check_finite=False),
                         Assignments(eng.ids[slot].clone(), validate=False),
                         history[:iterations].cpu().numpy(), iterations, counters)

@@ -198,6 +198,110 @@ class LloydEngine:
             self.obj.copy_(self.obj_red)
             self.changed.copy_((self.changed_f[0] > 0).to(torch.int32))
 
+    # ------------------------------------------------- pipelined iteration
+    # Split of one iteration into (assign) and (rest) so that the NEXT
+    # iteration's assign can be queued before the host reads this one's
+    # decision flags: the GPU never idles on the host's poll.  Speculation is
+    # safe: the speculative assign reads the new centroid slot and writes only
+    # the other assignment slot, `mind` and `changed` (zeroed after this
+    # iteration's flags were copied out in stream order); if the run stops,
+    # its results are simply not used.
+    def _graph(self, key, fn):
+        if not self.use_graphs:
+            fn()
+            return
+        gr = self._graphs.get(key)
+        if gr is None:
+            fn()  # eager once (first launches set kernel attributes, outside capture)
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                fn()
+            self._graphs[key] = gr
+            return
+        gr.replay()
+
+    def enq_assign(self, slot: int, compare: bool, csrc: int) -> None:
+        """Queue iteration work part 1: assignment into ids[slot] against operand[csrc]."""
+        def fn():
+            self.changed.zero_()
+            self.be.assign(self.x, self.operand[csrc],
+                           idx_prev=self.ids[slot ^ 1] if compare else None,
+                           changed=self.changed if compare else None, idx_out=self.ids[slot],
+                           mind_out=self.mind)
+        self._graph(("a", slot, compare, csrc), fn)
+
+    def enq_rest(self, slot: int, history_row: torch.Tensor | None = None, timers=None) -> None:
+        """Queue part 2: objective, update, shard exchange, normalize into the
+        other centroid slot, then an async copy of [changed, shift2, merges]
+        to pinned host memory (read by wait_flags)."""
+        if not hasattr(self, "_flags_h"):
+            self._flags_d = torch.zeros(3, dtype=torch.float64, device=self.dev)
+            self._flags_h = torch.zeros(3, dtype=torch.float64).pin_memory() if self.x.is_cuda \
+                else torch.zeros(3, dtype=torch.float64)
+            self._flags_ev = torch.cuda.Event() if self.x.is_cuda else None
+
+        def fn():
+            self.shift2.zero_()
+            self.merges_it.zero_()
+            self.be.objective(self.mind, out=self.obj)
+            if timers is not None:  # bench: live per-kernel timing (eager only)
+                timers[0].record()
+            self.be.update(self.x, self.ids[slot], self.K, self.chunk, sums=self.sums,
+                           counts=self.counts, merges=self.merges_it)
+            if timers is not None:
+                timers[1].record()
+            if self.allreduce is not None:
+                self.exchange()
+            nxt = self.cur ^ 1
+            self.be.normalize(self.sums, self.counts, self.master[self.cur], out=self.master[nxt],
+                              operand_out=None if self.operand is self.master else self.operand[nxt],
+                              empty=self.empty, shift2=self.shift2)
+            self._flags_d[0].copy_(self.changed)
+            self._flags_d[1].copy_(self.shift2)
+            self._flags_d[2].copy_(self.merges_it)
+        if timers is not None:
+            fn()
+        else:
+            self._graph(("r", slot, self.cur), fn)
+        if history_row is not None:
+            history_row.copy_(self.obj)
+        self._flags_h.copy_(self._flags_d, non_blocking=True)
+        if self._flags_ev is not None:
+            self._flags_ev.record()
+
+    def wait_flags(self):
+        """(changed, shift, merges of this iteration) once its flags reached the host."""
+        if self._flags_ev is not None:
+            self._flags_ev.synchronize()
+        f = self._flags_h.tolist()
+        return f[0] != 0, math.sqrt(f[1]), int(f[2])
+
+    def run(self, max_iters: int, shift_tol: float, history: torch.Tensor | None = None,
+            stop_on_repeat: bool = True):
+        """lloyd_run's loop (pipeline.py:128-147, policy "keep") with the next
+        assign queued speculatively before each poll.  Returns (iterations,
+        assignment slot of the last iteration, committed merge count)."""
+        merges = 0
+        slot = 0
+        it = 0
+        self.enq_assign(0, False, self.cur)
+        while it < max_iters:
+            it += 1
+            slot = (it - 1) & 1
+            self.enq_rest(slot, None if history is None else history[it - 1])
+            spec = it < max_iters
+            if spec:  # assume the commit: next assign against the new centroids
+                self.enq_assign(slot ^ 1, True, self.cur ^ 1)
+            changed, shift, mg = self.wait_flags()
+            if stop_on_repeat and it > 1 and not changed:
+                break  # assignments repeated: the update reproduces c bitwise
+            self.cur ^= 1
+            merges += mg
+            if shift <= shift_tol:
+                break
+        self.it = it
+        return it, slot, merges
+
     def poll(self):
         """(changed: bool, shift: float) -- the one device->host read per iteration."""
         v = torch.stack([self.changed.to(torch.float64), self.shift2]).cpu()
@@ -248,6 +352,13 @@ def lloyd_run(x: DataMatrix, cfg: KMeansConfig, engine: str = "flash", workers: 
     eng = LloydEngine(xd, cfg.clusters, tiling.update_chunk)
     eng.set_centroids(c0)
     history = torch.empty((cfg.max_iters, x.batch), dtype=torch.float64, device=dev)
+    if cfg.empty_cluster_policy != "reseed_farthest":
+        iterations, slot, merges = eng.run(cfg.max_iters, cfg.shift_tol, history)
+        torch.cuda.synchronize(dev)  # a speculative assign may still be in flight
+        counters.synchronized_merges += merges
+        return KMeansResult(Centroids(eng.centroids.clone(), check_finite=False),
+                            Assignments(eng.ids[slot].clone(), validate=False),
+                            history[:iterations].cpu().numpy(), iterations, counters)
     iterations = 0
     slot = 0
     for it in range(1, cfg.max_iters + 1):
@@ -256,9 +367,8 @@ def lloyd_run(x: DataMatrix, cfg: KMeansConfig, engine: str = "flash", workers: 
         changed, shift = eng.poll()
         if it > 1 and not changed:
             break  # assignments repeated: the update reproduces c bitwise
-        if cfg.empty_cluster_policy == "reseed_farthest":
-            eng.reseed_farthest(slot)
-            _, shift = eng.poll()
+        eng.reseed_farthest(slot)
+        _, shift = eng.poll()
         eng.commit()
         if shift <= cfg.shift_tol:
             break

@@ -34,9 +34,23 @@ def run(name, B, N, K, d, dtype, reps=20):
     tn = t(lambda: ops.normalize(eng.sums, eng.counts, eng.master[eng.cur], out=eng.master[eng.cur ^ 1],
                                   operand_out=None if eng.operand is eng.master else eng.operand[eng.cur ^ 1],
                                   empty=eng.empty, shift2=eng.shift2))
+    # pipelined loop (LloydEngine.run: next assign queued before the poll)
+    def pipe(graphs):
+        eng.use_graphs = graphs
+        for _ in range(2):
+            eng.run(4, -1.0, stop_on_repeat=False)  # warm: captures every (slot, centroid-slot) graph once
+            eng.run(3, -1.0, stop_on_repeat=False)
+        torch.cuda.synchronize()
+        s2, e2 = ev(), ev()
+        s2.record()
+        its, _, _ = eng.run(reps, -1.0, stop_on_repeat=False)
+        e2.record(); torch.cuda.synchronize()
+        return s2.elapsed_time(e2) / its
+    t_pipe = pipe(True)
+    t_pipe_eager = pipe(False)
     fl = 2 * B * N * K * d
     by = B * N * d * x.element_size() + 4 * B * N + 4 * B * K * d + 4 * B * K
-    print(f"{name}: iteration {t_it*1e3:.1f} us | assign {ta*1e3:.1f} us ({fl/ta/1e9:.0f} TF/s) | "
+    print(f"{name}: iteration {t_it*1e3:.1f} us (pipelined {t_pipe*1e3:.1f} us graphs, {t_pipe_eager*1e3:.1f} us eager) | assign {ta*1e3:.1f} us ({fl/ta/1e9:.0f} TF/s) | "
           f"update {tu*1e3:.1f} us ({by/tu/1e6:.0f} GB/s) | normalize {tn*1e3:.1f} us | "
           f"{B*N/(t_it*1e-3)/1e9:.2f} Gpoints/s")
 

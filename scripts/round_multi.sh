@@ -1,6 +1,5 @@
-# one-GPU rehearsal of the multi-rank bench path (gloo, both ranks on cuda:0) + GPU tests + bench
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
-FK_BENCH_SHARE_GPU=1 FK_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu > gpurun_out/bench_rehearsal2.json 2> gpurun_out/bench_rehearsal2.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 1 --steps 5 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_torchrun1.json 2> gpurun_out/bench_torchrun1.err
+timeout 300 python scripts/config_perf.py > gpurun_out/config_perf.txt 2>&1
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+FK_BENCH_SHARE_GPU=1 FK_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_rehearsal2.json 2> gpurun_out/bench_rehearsal2.err

@@ -188,3 +188,40 @@ def test_baseline_engine_agrees_on_separated_blobs():
     assert rf.iterations_run == rb.iterations_run
     assert np.array_equal(rf.assignments.numpy(), rb.assignments.numpy())
     np.testing.assert_allclose(rf.centroids.numpy(), rb.centroids.numpy(), rtol=1e-12)
+
+
+@pytest.mark.parametrize("stop_iter_cap", [3, 40])
+def test_pipelined_run_equals_stepwise_loop(stop_iter_cap):
+    """LloydEngine.run queues the next assign before each poll (speculation);
+    its decisions and results must equal the plain iterate/poll/commit loop.
+    f32 data: every kernel is deterministic, so the comparison is bitwise."""
+    from paper_2603_09229_b200 import LloydEngine
+
+    x = fk.generate_dataset(2, 5000, 11, 24, 1.5, 3, "single").data.cuda()
+    c0 = torch.stack([x[b, :37] for b in range(2)]).float()
+
+    eng = LloydEngine(x, 37, 777)
+    eng.set_centroids(c0)
+    hist_a = torch.empty((stop_iter_cap, 2), dtype=torch.float64, device="cuda")
+    its_a, slot_a, merges_a = eng.run(stop_iter_cap, 0.0, hist_a)
+    torch.cuda.synchronize()
+    c_a, ids_a = eng.centroids.clone(), eng.ids[slot_a].clone()
+
+    ref = LloydEngine(x, 37, 777)
+    ref.set_centroids(c0)
+    hist_b = torch.empty((stop_iter_cap, 2), dtype=torch.float64, device="cuda")
+    its_b, slot_b = 0, 0
+    for it in range(1, stop_iter_cap + 1):
+        its_b = it
+        slot_b = ref.iterate(hist_b[it - 1])
+        changed, shift = ref.poll()
+        if it > 1 and not changed:
+            break
+        ref.commit()
+        if shift <= 0.0:
+            break
+    assert its_a == its_b
+    assert torch.equal(c_a, ref.centroids)
+    assert torch.equal(ids_a, ref.ids[slot_b])
+    assert torch.equal(hist_a[:its_a], hist_b[:its_b])
+    assert merges_a == int(ref.merges.item())
