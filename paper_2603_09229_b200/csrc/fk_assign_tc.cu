@@ -57,7 +57,7 @@ static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB dynamic shared memory");
 
 struct TcArgs {
   int B, N, K, d;
-  int katoms;           // ceil(d / 64), 1 or 2
+  int katoms;           // ceil(d / 64): 1 or 2 (single-CTA kernel), 1..4 (pair kernel)
   int tiles_per_batch;  // ceil(N / 128)
   int total_tiles;      // B * tiles_per_batch
   int ncol;             // ceil(K / 256)
@@ -399,19 +399,36 @@ constexpr int CN_SLOTS = 6;              // ||c||^2 ring (bias in the epilogue)
 constexpr int EXT_ROW = 32;              // 16 bf16: [hi, mid, lo, 0...] of ||c||^2 / 2
 constexpr int EXT_SLOT = BNH * EXT_ROW;  // 4 KB per CTA per column tile
 constexpr int EXT_SLOTS = 4;             // bias-in-GEMM operand ring
-constexpr int OFF_A = 0;
-constexpr int OFF_B = OFF_A + 2 * A_SLOT;
-constexpr int OFF_AEXT = OFF_B + STAGES * B_STAGE;         // constant ones operand (4 KB)
+// Layout: the small rings first, then ONE operand region shared by the X
+// row-tile ring and the C stage ring, sized per d (see operand_plan).
+constexpr int OFF_AEXT = 0;                                // constant ones operand (4 KB)
 constexpr int OFF_EXT = OFF_AEXT + BM * EXT_ROW;
 constexpr int OFF_CN = OFF_EXT + EXT_SLOTS * EXT_SLOT;
 constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;
 constexpr int OFF_BAR = OFF_XCH + BM * 8;
 constexpr int A_SLOTS_MAX = 8;
 constexpr int NBARS = 2 * A_SLOTS_MAX + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
-constexpr int SMEM_USED = OFF_BAR + NBARS * 8 + 16;
-constexpr int SMEM_BYTES = SMEM_USED + 1024;
+constexpr int OFF_OPS = ((OFF_BAR + NBARS * 8 + 16) + 1023) & ~1023;  // 1 KB aligned (SW128)
+constexpr int SMEM_BYTES = 232448;                          // 227 KB: the whole opt-in carve-out
+constexpr int OPS_BYTES = SMEM_BYTES - 1024 - OFF_OPS;      // minus the base-alignment slack
 constexpr int THREADS = 384;
-static_assert(SMEM_BYTES <= 232448, "exceeds 227 KB dynamic shared memory");
+constexpr int KATOMS_MAX = 4;                               // d <= 256
+static_assert(2 * KATOMS_MAX * A_ATOM + 4 * B_STAGE <= OPS_BYTES, "d = 256 plan does not fit");
+static_assert(2 * 2 * A_ATOM + STAGES * B_STAGE <= OPS_BYTES, "d = 128 plan does not fit");
+// (X slots, C stages) per K-atom count: deep X prefetch for short rows,
+// deep C prefetch otherwise, at least one column tile of C for d = 256.
+__host__ __device__ inline void operand_plan(int katoms, int& a_slots, int& b_stages) {
+  if (katoms == 1) {
+    a_slots = 6;
+    b_stages = 4;
+  } else if (katoms == 4) {
+    a_slots = 2;
+    b_stages = 4;
+  } else {
+    a_slots = 2;
+    b_stages = STAGES;
+  }
+}
 }  // namespace tc2
 
 // Epilogue chunk when the bias is already in the accumulator (s = ||c||^2/2 - x.c).
@@ -490,8 +507,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sA = smem + OFF_A;
-  uint8_t* sB = smem + OFF_B;
+  uint8_t* sA = smem + OFF_OPS;
+  uint8_t* sB;
   uint8_t* sAext = smem + OFF_AEXT;
   uint8_t* sExt = smem + OFF_EXT;
   float* sCN = reinterpret_cast<float*>(smem + OFF_CN);
@@ -525,8 +542,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   // X row-tile ring + C stage ring share the 160 KB operand region: d <= 64
   // (one K-atom per tile) takes 6 X slots + 4 C stages -- short row tiles need
   // the deeper X prefetch -- d <= 128 takes 2 X slots + 6 C stages.
-  const int a_slots = p.katoms == 1 ? 6 : 2;
-  const int b_stages = p.katoms == 1 ? 4 : STAGES;
+  int a_slots, b_stages;
+  operand_plan(p.katoms, a_slots, b_stages);
   const int a_slot_bytes = p.katoms * A_ATOM;
   sB = sA + a_slots * a_slot_bytes;
   // ALT (single-column-tile rows, K <= 256): the two epilogue warpgroups take
@@ -951,7 +968,7 @@ static bool make_map(CUtensorMap* m, const void* base, int fmt, int64_t inner, i
 
 constexpr int kDefaultBiasMode = 1;
 
-bool assign_tc_supported(int64_t d) { return d >= 8 && d <= 128 && (d % 8) == 0; }
+bool assign_tc_supported(int64_t d) { return d >= 8 && d <= 256 && (d % 8) == 0; }
 
 // Where the ||c||^2/2 bias enters (FK_ASSIGN_BIAS=0 epilogue, 1 bias-in-GEMM,
 // 2 TMEM seed; A/B comparisons).  The legacy FK_ASSIGN_AUG=0 means 0.
@@ -1001,7 +1018,7 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     a.trace = trace_buf;
   }
   const char* cta = getenv("FK_ASSIGN_CTA");
-  if (!(cta && atoi(cta) == 1)) {
+  if (!(cta && atoi(cta) == 1) || d > 128) {  // the single-CTA kernel (A/B only) stops at d = 128
     CUtensorMap tmx2, tmc2, tmext;
     if (!make_map(&tmx2, X, fmt, d, N, B, tc2::BM)) return cudaErrorInvalidValue;
     if (!make_map(&tmc2, C, fmt, d, K, B, tc2::BNH)) return cudaErrorInvalidValue;

@@ -2,7 +2,8 @@
 
 Covers the shapes the reference's own tests exercise (ragged tiles, K=1,
 N < tile, d not a multiple of the vector width) plus the B200 buckets:
-the CUDA-core fallbacks (d > 128 or d % 8 != 0 for bf16/fp16), the global
+the tensor-core K-atom counts 1-4 (d up to 256), the CUDA-core fallbacks
+(d > 256 or d % 8 != 0 for bf16/fp16), the global
 histogram path (K beyond the shared-memory bins, BASELINE config 5's
 K=65536), and the batched config-4 shape (B=64, d=64, K=256, fp16).
 """
@@ -61,7 +62,11 @@ def check_assign(ops, oracle, x, c, exact):
     (2, 300, 1, 64, torch.float16),       # K = 1
     (3, 257, 255, 128, torch.bfloat16),   # ragged rows and columns
     (1, 1000, 513, 120, torch.bfloat16),  # d not a multiple of 64 (zero-filled K atom)
-    (1, 700, 100, 200, torch.bfloat16),   # d > 128: CUDA-core fallback
+    (1, 700, 100, 200, torch.bfloat16),   # d = 200: 4 K atoms on the tensor cores (last one ragged)
+    (2, 3000, 700, 256, torch.bfloat16),  # d = 256: widest tensor-core bucket
+    (1, 2000, 300, 136, torch.float16),   # d = 136: 3 K atoms, fp16
+    (1, 900, 64, 192, torch.float16),     # d = 192, single column tile (alternate-tile epilogue)
+    (1, 700, 100, 264, torch.bfloat16),   # d > 256: CUDA-core fallback
     (1, 700, 50, 6, torch.float16),       # d % 8 != 0: CUDA-core fallback
     (64, 16384, 256, 64, torch.float16),  # BASELINE config 4 shape
     (1, 20000, 65536 // 8, 32, torch.bfloat16),
@@ -112,3 +117,15 @@ def test_streaming_large_k(ops):
     assert r_st.iterations_run == r_in.iterations_run
     assert np.array_equal(r_st.assignments.numpy(), r_in.assignments.numpy())
     np.testing.assert_allclose(r_st.centroids.numpy(), r_in.centroids.numpy(), rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("d", [136, 200, 256])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_wide_rows_integer_grid_bitwise(ops, oracle, d, dtype):
+    """Integer-grid data: every product and sum is exact, so the tensor-core
+    result must equal the oracle bit for bit (ids, ties, min_dists) for 3-4
+    K atoms as well."""
+    g = torch.Generator().manual_seed(d)
+    x = torch.randint(-4, 5, (2, 777, d), generator=g).to(dtype)
+    c = torch.randint(-4, 5, (2, 300, d), generator=g).to(dtype)
+    check_assign(ops, oracle, x, c, exact=True)

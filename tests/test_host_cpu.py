@@ -129,9 +129,12 @@ class TestTuner:
 
     def test_shape_bucket(self):
         b = fk.shape_bucket(fk.ProblemShape(1 << 23, 4096, 128), torch.bfloat16)
-        assert b["assign"]["kernel"] == "fk_assign_tc" and b["assign"]["k_atoms"] == 2
+        assert b["assign"]["kernel"].startswith("fk_assign_tc2") and b["assign"]["k_atoms"] == 2
+        b256 = fk.shape_bucket(fk.ProblemShape(1 << 20, 1024, 256), torch.bfloat16)
+        assert b256["assign"]["k_atoms"] == 4 and b256["assign"]["c_stages"] == 4
         assert fk.shape_bucket(fk.ProblemShape(100, 8, 16), torch.float32)["assign"]["kernel"].endswith("<exact>")
-        assert fk.shape_bucket(fk.ProblemShape(100, 8, 200), torch.float16)["assign"]["kernel"].endswith("<lowp>")
+        assert fk.shape_bucket(fk.ProblemShape(100, 8, 264), torch.float16)["assign"]["kernel"].endswith("<lowp>")
+        assert fk.shape_bucket(fk.ProblemShape(100, 8, 201), torch.float16)["assign"]["kernel"].endswith("<lowp>")
 
 
 class TestInit:
