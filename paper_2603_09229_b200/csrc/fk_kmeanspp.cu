@@ -167,6 +167,19 @@ FK_DEV double pw_leaf_row_fixed(const T* x, const double* c) {
                    __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
 }
 
+// Compile-time d above 128: numpy's split into two halves of fixed size.
+template <typename T, int D>
+FK_DEV double pw_row_fixed(const T* x, const double* c) {
+  if constexpr (D <= kLeaf) {
+    return pw_leaf_row_fixed<T, D>(x, c);
+  } else {
+    constexpr int D2 = (D / 2) - (D / 2) % 8;
+    const double a = pw_row_fixed<T, D2>(x, c);
+    const double b = pw_row_fixed<T, D - D2>(x + D2, c + D2);
+    return __dadd_rn(a, b);
+  }
+}
+
 // Rows longer than 128: numpy splits at n2 = n/2 rounded down to a multiple of
 // 8 (keeps every leaf 16-B aligned for all element types).
 template <typename T>
@@ -323,7 +336,7 @@ __global__ void __launch_bounds__(kSweepRows) k_pp_sweep(
   __syncthreads();
   const int t = threadIdx.x;
   if (t < nr) {
-    const double v = D > 0 ? pw_leaf_row_fixed<T, (D > 0 ? D : 8)>(tile + (size_t)t * stride_elems, c)
+    const double v = D > 0 ? pw_row_fixed<T, (D > 0 ? D : 8)>(tile + (size_t)t * stride_elems, c)
                            : pw_row<T>(tile + (size_t)t * stride_elems, c, d);
     double* mp = m + b * m_sb + r0 + t;
     *mp = first ? v : fmin(*mp, v);
@@ -396,7 +409,7 @@ __global__ void __launch_bounds__(kSweepRows) k_pp_sweep_pipe(
     const int nr = (int)i64min(kSweepRows, rows - r0);
     if ((int)threadIdx.x < nr) {
       const T* xr = tiles + slot * tile_elems + (size_t)threadIdx.x * stride_elems;
-      const double v = D > 0 ? pw_leaf_row_fixed<T, (D > 0 ? D : 8)>(xr, c) : pw_row<T>(xr, c, d);
+      const double v = D > 0 ? pw_row_fixed<T, (D > 0 ? D : 8)>(xr, c) : pw_row<T>(xr, c, d);
       double* mp = m + b * m_sb + r0 + threadIdx.x;
       *mp = first ? v : fmin(*mp, v);
     }
@@ -975,6 +988,8 @@ cudaError_t sweep_t(const void* X, int64_t B, int64_t rows, int d, int64_t x_sb,
       case 32: FK_PP_FAST(32);
       case 64: FK_PP_FAST(64);
       case 128: FK_PP_FAST(128);
+      case 192: FK_PP_FAST(192);
+      case 256: FK_PP_FAST(256);
       default: FK_PP_FAST(0);
     }
 #undef FK_PP_FAST

@@ -56,12 +56,13 @@ def test_forced_exact_fallback_matches(kpp_golden):
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32, torch.float64])
 def test_device_kmeanspp_random_matches_oracle(oracle, dtype):
     from paper_2603_09229_b200.core import kmeanspp_indices_device
 
     g = torch.Generator().manual_seed(11)
-    for (B, n, d, k) in [(3, 2053, 32, 17), (1, 20000, 128, 24), (2, 129, 9, 129)]:
+    for (B, n, d, k) in [(3, 2053, 32, 17), (1, 20000, 128, 24), (2, 129, 9, 129), (1, 3000, 256, 12),
+                         (1, 2000, 192, 10)]:
         x = (torch.randn(B, n, d, generator=g) * 4).to(dtype)
         idx = kmeanspp_indices_device(x.cuda(), k, 5)
         x64 = x.double().numpy()
