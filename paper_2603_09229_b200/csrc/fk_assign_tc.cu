@@ -756,14 +756,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     }
     uint32_t g = 0;
     int i = 0;
+    // (batch, tile-in-batch) of t, advanced without a division per tile
+    int tb = pair / p.tiles_per_batch, tr_ = pair - tb * p.tiles_per_batch;
+    const int step_b = npairs / p.tiles_per_batch, step_r = npairs - step_b * p.tiles_per_batch;
     for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
+      const int b = tb, trow = tr_;
+      tb += step_b;
+      tr_ += step_r;
+      if (tr_ >= p.tiles_per_batch) {
+        tr_ -= p.tiles_per_batch;
+        ++tb;
+      }
       if (alt && (i & 1) != wg) {  // the other warpgroup owns this tile
         ++g;
         continue;
       }
-      const int b = t / p.tiles_per_batch;
-      const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
+      const int row0 = trow * (2 * BM) + rank * BM;
       const int slot = i % a_slots;
+      // previous assignment of this row, loaded now so its HBM latency overlaps
+      // the row tile's chunks instead of sitting at the end of the tile
+      int prev_id = -2;
+      if (p.idx_prev && (alt || wg == 0) && row0 + row < p.N)
+        prev_id = __ldg(p.idx_prev + (size_t)b * p.N + row0 + row);
       float M = __int_as_float(0x7f800000);
       int best = -1;
       float bestv[32];
@@ -888,7 +902,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           const size_t o = (size_t)b * p.N + grow;
           p.idx_out[o] = idx;
           p.mind_out[o] = fmaxf(0.f, NEG ? fmaf(2.f, M, xn) : xn + M);
-          if (p.idx_prev) ch = p.idx_prev[o] != idx;
+          if (p.idx_prev) ch = prev_id != idx;
         }
         if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
       }
@@ -930,8 +944,13 @@ static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
   int pairs = num_sms / 2;
   if (a.total_tiles < pairs) pairs = a.total_tiles;
   if (pairs <= 0) return cudaSuccess;
-  return a.ncol == 1 ? launch_pair_t<FMT, BIAS, true>(tmx, tmc, tmext, a, pairs, stream)
-                     : launch_pair_t<FMT, BIAS, false>(tmx, tmc, tmext, a, pairs, stream);
+  static int alt_env = -1;  // FK_ASSIGN_ALT=0: split single-column-tile rows across both WGs (A/B)
+  if (alt_env < 0) {
+    const char* e = getenv("FK_ASSIGN_ALT");
+    alt_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return (a.ncol == 1 && alt_env) ? launch_pair_t<FMT, BIAS, true>(tmx, tmc, tmext, a, pairs, stream)
+                                  : launch_pair_t<FMT, BIAS, false>(tmx, tmc, tmext, a, pairs, stream);
 }
 
 // ---------------------------------------------------------------- host side
