@@ -204,6 +204,19 @@ def pairwise_sum(a: np.ndarray) -> float:
     return float(lib().orc_pairwise_sum(_p(a), a.shape[0]))
 
 
+def kmeanspp_sweep(points64: np.ndarray, center64: np.ndarray, m: np.ndarray, first: bool) -> None:
+    """One D^2 sweep in numpy order into m (in place)."""
+    p = np.ascontiguousarray(points64, np.float64)
+    c = np.ascontiguousarray(center64, np.float64)
+    lib().orc_kmeanspp_sweep(_p(p), p.shape[0], p.shape[1], _p(c), _p(m), 1 if first else 0)
+
+
+def choice_cdf(m: np.ndarray, total: float, u: float) -> int:
+    """searchsorted(cumsum(m/total)/cumsum[-1], u, side="right")."""
+    m = np.ascontiguousarray(m, np.float64)
+    return int(lib().orc_choice_cdf(_p(m), m.shape[0], float(total), float(u)))
+
+
 def kmeanspp_indices(points: np.ndarray, k: int, rng: np.random.Generator) -> np.ndarray:
     """_kmeanspp_indices (core.py:342-357) with the numpy arithmetic in C.
 

@@ -23,7 +23,8 @@ import torch.distributed as dist
 from .core import Assignments, Centroids, Counters, KMeansConfig, KMeansResult, init_indices
 from .pipeline import LloydEngine
 
-__all__ = ["shard_bounds", "make_allreduce", "init_centroids_sharded", "lloyd_run_sharded"]
+__all__ = ["shard_bounds", "make_allreduce", "init_centroids_sharded", "kmeanspp_indices_sharded",
+           "lloyd_run_sharded"]
 
 
 def shard_bounds(points: int, world: int, rank: int) -> tuple[int, int]:
@@ -40,13 +41,87 @@ def make_allreduce(group=None):
     return allreduce
 
 
-def init_centroids_sharded(x_shard: torch.Tensor, total_points: int, lo: int, clusters: int,
-                           seed: int, method: str = "random_distinct", group=None) -> torch.Tensor:
-    """Replicated initial centroids from a row-sharded dataset."""
-    if method != "random_distinct":
-        raise NotImplementedError("sharded k-means++ seeding is not implemented (SURVEY §8f rank 3)")
+def _center_row(x_shard: torch.Tensor, b: int, row: int, lo: int, group) -> torch.Tensor:
+    """Global row `row` of batch element b, replicated on every rank (the owner
+    contributes it through an all-reduce; f64 holds every data type exactly)."""
+    n_local = x_shard.shape[1]
+    v = torch.zeros((x_shard.shape[2],), dtype=torch.float64, device=x_shard.device)
+    if lo <= row < lo + n_local:
+        v.copy_(x_shard[b, row - lo].double())
+    dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
+    return v.to(x_shard.dtype)
+
+
+def kmeanspp_indices_sharded(x_shard: torch.Tensor, total_points: int, lo: int, clusters: int,
+                             seed: int, group=None, backend=None) -> np.ndarray:
+    """k-means++ seeding (core.py:342-357) over row shards, index for index equal
+    to the single-process seeding.
+
+    Every rank sweeps its own rows against the current center into its slice
+    of the (N,) f64 weight table; the slices are all-gathered (one collective
+    per draw), and every rank runs the identical numpy-order total and
+    certified choice() on the full table.  So all ranks draw the same index
+    without further communication.  The numpy substream (seed, b) is consumed
+    on every rank exactly as the reference does."""
+    from . import ops as _ops
+
+    be = _ops if backend is None else backend
     B, n_local, d = x_shard.shape
-    idx = init_indices(total_points, clusters, seed, B, method)
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    bounds = [shard_bounds(total_points, world, r) for r in range(world)]
+    if bounds[rank][0] != lo or bounds[rank][1] - bounds[rank][0] != n_local:
+        raise ValueError("x_shard must be this rank's shard_bounds() rows")
+    maxn = max(h - l for l, h in bounds)
+    dev = x_shard.device
+    out = np.empty((B, clusters), np.int64)
+    for b in range(B):
+        rng = np.random.default_rng((seed, b))
+        idx = out[b]
+        idx[0] = rng.integers(total_points)
+        if clusters == 1:
+            continue
+        pp = be.KmeansppStream(total_points, clusters, dev)
+        send = torch.zeros((maxn,), dtype=torch.float64, device=dev)
+        recv = torch.empty((world * maxn,), dtype=torch.float64, device=dev)
+
+        def sweep(row: int, first: bool, j: int) -> None:
+            center = _center_row(x_shard, b, row, lo, group)
+            if n_local:
+                pp.sweep(x_shard[b], lo, center, first, j)
+            send[:n_local].copy_(pp.m[0, lo:lo + n_local])
+            dist.all_gather(list(recv.view(world, maxn).unbind(0)), send, group=group)
+            for r, (l, h) in enumerate(bounds):
+                if h > l and r != rank:
+                    pp.m[0, l:h].copy_(recv[r * maxn:r * maxn + (h - l)])
+
+        sweep(int(idx[0]), True, 1)
+        for j in range(1, clusters):
+            state = rng.bit_generator.state
+            pp.select(j, float(rng.random()))
+            got = int(pp.idx[0, j].item())
+            if int(pp.halted[0].item()) == j:  # total == 0: rng.integers from here on
+                rng.bit_generator.state = state
+                for jj in range(j, clusters):
+                    idx[jj] = rng.integers(total_points)
+                break
+            idx[j] = got
+            if j + 1 < clusters:
+                sweep(got, False, j + 1)
+    return out
+
+
+def init_centroids_sharded(x_shard: torch.Tensor, total_points: int, lo: int, clusters: int,
+                           seed: int, method: str = "random_distinct", group=None,
+                           backend=None) -> torch.Tensor:
+    """Replicated initial centroids from a row-sharded dataset."""
+    B, n_local, d = x_shard.shape
+    if method == "kmeanspp":
+        idx = kmeanspp_indices_sharded(x_shard, total_points, lo, clusters, seed, group, backend)
+    elif method == "random_distinct":
+        idx = init_indices(total_points, clusters, seed, B, method)
+    else:
+        raise ValueError(f"unknown init method {method!r}")
     buf = torch.zeros((B, clusters, d), dtype=torch.float64, device=x_shard.device)
     for b in range(B):
         sel = np.flatnonzero((idx[b] >= lo) & (idx[b] < lo + n_local))
@@ -68,7 +143,7 @@ def lloyd_run_sharded(x_shard: torch.Tensor, total_points: int, lo: int, cfg: KM
     eng = LloydEngine(x_shard, cfg.clusters, update_chunk or total_points,
                       allreduce=make_allreduce(group), backend=backend)
     eng.set_centroids(init_centroids_sharded(x_shard, total_points, lo, cfg.clusters, cfg.seed,
-                                             cfg.init, group))
+                                             cfg.init, group, backend))
     history = torch.empty((cfg.max_iters, eng.B), dtype=torch.float64, device=x_shard.device)
     # every rank takes the same decisions: the flags are reduced in the exchange
     iterations, slot, merges = eng.run(cfg.max_iters, cfg.shift_tol, history)

@@ -6,6 +6,9 @@ sys.path.insert(0, ".")
 from paper_2603_09229_b200 import ops
 shapes = [(1, 1 << 20, 1024, 128, torch.bfloat16), (64, 16384, 256, 64, torch.float16),
           (64, 16384, 256, 64, torch.bfloat16), (8, 65536, 256, 64, torch.bfloat16)]
+import os
+if os.environ.get("SHAPE"):
+    shapes = [shapes[int(os.environ["SHAPE"])]]
 for (B, N, K, d, dt) in shapes:
     x = torch.randn(B, N, d, device="cuda").to(dt)
     ids = torch.randint(0, K, (B, N), device="cuda", dtype=torch.int32)

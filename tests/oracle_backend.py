@@ -51,3 +51,27 @@ def normalize(sums, counts, prev, out=None, operand_out=None, empty=None, shift2
             e[b, lst] = 1
         empty.copy_(torch.from_numpy(e))
     return out, operand_out, empty
+
+
+class KmeansppStream:
+    """CPU stand-in for ops.KmeansppStream (the (N,) weight table on the host)."""
+
+    def __init__(self, points, clusters, device=None):
+        self.n, self.k = int(points), int(clusters)
+        self.m = torch.zeros((1, self.n), dtype=torch.float64)
+        self.idx = torch.zeros((1, self.k), dtype=torch.int64)
+        self.halted = torch.full((1,), self.k, dtype=torch.int32)
+
+    def sweep(self, rows, lo, center, first, j):
+        n = rows.shape[0]
+        seg = np.ascontiguousarray(self.m[0, lo:lo + n].numpy())
+        O.kmeanspp_sweep(rows.double().numpy(), center.double().numpy(), seg, first)
+        self.m[0, lo:lo + n] = torch.from_numpy(seg)
+
+    def select(self, j, u):
+        m = self.m[0].numpy()
+        total = O.pairwise_sum(m)
+        if total > 0.0:
+            self.idx[0, j] = O.choice_cdf(m, total, u)
+        else:
+            self.halted[0] = j

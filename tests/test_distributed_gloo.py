@@ -82,3 +82,57 @@ def test_sharded_lloyd_matches_single_process(oracle, prec):
         else:
             np.testing.assert_allclose(r[3], c_ref, rtol=1e-12)
     assert np.array_equal(res[0][3], res[1][3])  # replicas never diverge
+
+
+def _kpp_worker(rank, world, port, result_q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle_backend
+        from kmeanspp_cases import CASES, make_case
+        from paper_2603_09229_b200.distributed import kmeanspp_indices_sharded, shard_bounds
+
+        out = {}
+        for name in ("batched_f64", "duplicates_f32", "k_eq_n_f64"):
+            spec = CASES[name]
+            x = make_case(spec)
+            lo, hi = shard_bounds(x.shape[1], world, rank)
+            out[name] = kmeanspp_indices_sharded(torch.from_numpy(np.ascontiguousarray(x[:, lo:hi])),
+                                                 x.shape[1], lo, spec["k"], spec["seed"],
+                                                 backend=oracle_backend)
+        result_q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_kmeanspp_matches_reference_golden():
+    """World-3 k-means++ over row shards draws the reference's indices (golden)."""
+    world = 3
+    port = 31500 + (os.getpid() % 2000)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_kpp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    import queue as _queue
+    import time as _time
+    res, deadline = [], _time.time() + 240
+    while len(res) < world and _time.time() < deadline:
+        try:
+            res.append(q.get(timeout=2))
+        except _queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+    for p in procs:
+        if p.exitcode is None and len(res) < world:
+            p.terminate()
+    assert len(res) == world, "a rank failed"
+    for p in procs:
+        p.join(timeout=60)
+    gold = np.load(os.path.join(ROOT, "tests", "golden", "kmeanspp_golden.npz"))
+    for _, out in res:
+        for name, idx in out.items():
+            assert np.array_equal(idx, gold[name]), name

@@ -104,3 +104,22 @@ def test_lloyd_run_with_kmeanspp_init(kpp_golden):
     assert torch.equal(c.data.cpu(), x.data[0][torch.from_numpy(gold[0])][None])
     res = fk.lloyd_run(x, fk.KMeansConfig(spec["k"], max_iters=5, seed=spec["seed"], init="kmeanspp"))
     assert res.iterations_run >= 1
+
+
+def test_sharded_kmeanspp_device_world1(kpp_golden):
+    """The sharded seeding's device path (NCCL, world 1): sweep into the table
+    slice, all-gather, identical select -- index for index the golden draws."""
+    import torch.distributed as dist
+
+    from paper_2603_09229_b200.distributed import kmeanspp_indices_sharded
+
+    dist.init_process_group("nccl", init_method="tcp://127.0.0.1:29631", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        for name in ("batched_f64", "bf16_d128", "duplicates_f32"):
+            spec = CASES[name]
+            x = case_tensor(spec).cuda()
+            idx = kmeanspp_indices_sharded(x, x.shape[1], 0, spec["k"], spec["seed"])
+            assert np.array_equal(idx, kpp_golden[name]), name
+    finally:
+        dist.destroy_process_group()
