@@ -24,7 +24,7 @@ from .core import Assignments, Centroids, Counters, KMeansConfig, KMeansResult, 
 from .pipeline import LloydEngine
 
 __all__ = ["shard_bounds", "make_allreduce", "init_centroids_sharded", "kmeanspp_indices_sharded",
-           "lloyd_run_sharded"]
+           "reseed_farthest_sharded", "lloyd_run_sharded"]
 
 
 def shard_bounds(points: int, world: int, rank: int) -> tuple[int, int]:
@@ -132,6 +132,51 @@ def init_centroids_sharded(x_shard: torch.Tensor, total_points: int, lo: int, cl
     return buf
 
 
+def reseed_farthest_sharded(eng: LloydEngine, lo: int, group=None) -> None:
+    """reseed_farthest (pipeline.py:76-89) over row shards: each empty cluster, in
+    id order, takes the next point by decreasing assigned distance, ties to the
+    lowest GLOBAL index.  Each rank proposes its local top-E (stable sort:
+    distance desc, index asc); the candidates are all-gathered in rank order
+    (= global index order), so one stable sort of the union gives the global
+    order; the rows come from their owners through one all-reduce.  The empty
+    mask is replicated (counts are all-reduced), so every rank reseeds alike."""
+    nxt = eng.cur ^ 1
+    em = eng.empty.cpu().numpy()
+    if not em.any():
+        return
+    world = dist.get_world_size(group)
+    n_local, d, dev = eng.N, eng.d, eng.dev
+    for b in range(eng.B):
+        empties = np.flatnonzero(em[b])
+        E = int(empties.size)
+        if E == 0:
+            continue
+        md = eng.mind[b].double()
+        take = min(E, n_local)
+        order = torch.sort(-md, stable=True).indices[:take]
+        cand_d = torch.full((E,), float("-inf"), dtype=torch.float64, device=dev)
+        cand_i = torch.full((E,), -1.0, dtype=torch.float64, device=dev)
+        cand_d[:take] = md[order]
+        cand_i[:take] = (order + lo).double()
+        all_d = torch.empty((world * E,), dtype=torch.float64, device=dev)
+        all_i = torch.empty((world * E,), dtype=torch.float64, device=dev)
+        dist.all_gather(list(all_d.view(world, E).unbind(0)), cand_d, group=group)
+        dist.all_gather(list(all_i.view(world, E).unbind(0)), cand_i, group=group)
+        win = torch.sort(-all_d, stable=True).indices[:E]  # rank order = global index order on ties
+        gidx = all_i[win].long()
+        rows = torch.zeros((E, d), dtype=torch.float64, device=dev)
+        mine = (gidx >= lo) & (gidx < lo + n_local)
+        if bool(mine.any()):
+            rows[mine] = eng.x[b, gidx[mine] - lo].double()
+        dist.all_reduce(rows, op=dist.ReduceOp.SUM, group=group)
+        cid = torch.from_numpy(empties).to(dev)
+        eng.master[nxt][b, cid] = rows.to(eng.mdtype)
+        if eng.operand is not eng.master:
+            eng.operand[nxt][b, cid] = rows.to(eng.dtype)
+    diff = eng.master[nxt].double() - eng.master[eng.cur].double()
+    eng.shift2.copy_((diff * diff).sum(-1).max())
+
+
 def lloyd_run_sharded(x_shard: torch.Tensor, total_points: int, lo: int, cfg: KMeansConfig,
                       update_chunk: int | None = None, group=None, backend=None,
                       counters: Counters | None = None) -> KMeansResult:
@@ -146,7 +191,22 @@ def lloyd_run_sharded(x_shard: torch.Tensor, total_points: int, lo: int, cfg: KM
                                              cfg.init, group, backend))
     history = torch.empty((cfg.max_iters, eng.B), dtype=torch.float64, device=x_shard.device)
     # every rank takes the same decisions: the flags are reduced in the exchange
-    iterations, slot, merges = eng.run(cfg.max_iters, cfg.shift_tol, history)
+    if cfg.empty_cluster_policy != "reseed_farthest":
+        iterations, slot, merges = eng.run(cfg.max_iters, cfg.shift_tol, history)
+    else:  # stepwise: the reseed reads this iteration's min_dists before the commit
+        iterations, slot = 0, 0
+        for it in range(1, cfg.max_iters + 1):
+            iterations = it
+            slot = eng.iterate(history[it - 1])
+            changed, shift = eng.poll()
+            if it > 1 and not changed:
+                break
+            reseed_farthest_sharded(eng, lo, group)
+            _, shift = eng.poll()
+            eng.commit()
+            if shift <= cfg.shift_tol:
+                break
+        merges = int(eng.merges.item())
     if x_shard.is_cuda:
         torch.cuda.synchronize(x_shard.device)
     # merges: each rank counted its own shard's segments; the reference count is global

@@ -136,3 +136,61 @@ def test_sharded_kmeanspp_matches_reference_golden():
     for _, out in res:
         for name, idx in out.items():
             assert np.array_equal(idx, gold[name]), name
+
+
+def _reseed_worker(rank, world, port, result_q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle_backend
+        from paper_2603_09229_b200 import KMeansConfig
+        from paper_2603_09229_b200.distributed import lloyd_run_sharded, shard_bounds
+
+        g = np.load(os.path.join(ROOT, "tests", "golden", "reseed_golden.npz"))
+        x = g["x"]
+        lo, hi = shard_bounds(x.shape[1], world, rank)
+        cfg = KMeansConfig(48, max_iters=25, seed=5, empty_cluster_policy="reseed_farthest")
+        r = lloyd_run_sharded(torch.from_numpy(np.ascontiguousarray(x[:, lo:hi])), x.shape[1], lo, cfg,
+                              backend=oracle_backend)
+        result_q.put((rank, r.centroids.data.numpy(), r.assignments.values.numpy(),
+                      r.objective_history, r.iterations_run))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_reseed_farthest_matches_reference_golden():
+    """World-2 lloyd_run with reseed_farthest (duplicate rows leave clusters
+    empty on the first pass) reproduces the reference's golden run."""
+    world = 2
+    port = 33500 + (os.getpid() % 2000)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_reseed_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    import queue as _queue
+    import time as _time
+    res, deadline = [], _time.time() + 240
+    while len(res) < world and _time.time() < deadline:
+        try:
+            res.append(q.get(timeout=2))
+        except _queue.Empty:
+            if any(p.exitcode not in (None, 0) for p in procs):
+                break
+    for p in procs:
+        if p.exitcode is None and len(res) < world:
+            p.terminate()
+    assert len(res) == world, "a rank failed"
+    for p in procs:
+        p.join(timeout=60)
+    res = sorted(res, key=lambda t: t[0])
+    g = np.load(os.path.join(ROOT, "tests", "golden", "reseed_golden.npz"))
+    a = np.concatenate([r[2] for r in res], axis=1)
+    for r in res:
+        assert r[4] == int(g["iterations"])
+        assert np.array_equal(r[1], g["centroids"])
+        np.testing.assert_array_equal(r[3], g["history"])
+    assert np.array_equal(a, g["assignments"])
