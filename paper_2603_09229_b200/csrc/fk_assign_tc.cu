@@ -78,13 +78,17 @@ FK_DEV void trace_ev(const TcArgs& p, uint32_t g, int ev) {
   if (p.trace && g >= TR_G0 && g < TR_G0 + TR_N) p.trace[(g - TR_G0) * TR_EV + ev] = clock64();
 }
 
+// ||x||^2 of one row of the staged X tile over the 16-byte chunk positions
+// [j0, j1) of every K atom (the caller may split the 8 positions between
+// warpgroups; any split covers each element exactly once).
 template <int FMT>
-FK_DEV float row_norm_smem(const uint8_t* a_slot, int row, int katoms, int lane) {
+FK_DEV float row_norm_smem(const uint8_t* a_slot, int row, int katoms, int lane, int j0 = 0,
+                           int j1 = 8) {
   float acc = 0.f;
   for (int ka = 0; ka < katoms; ++ka) {
     const uint4* r = reinterpret_cast<const uint4*>(a_slot + ka * tc::A_ATOM + row * 128);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = j0; j < j1; ++j) {
       uint4 w = r[(j + lane) & 7];
       uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -405,7 +409,7 @@ constexpr int OFF_AEXT = 0;                                // constant ones oper
 constexpr int OFF_EXT = OFF_AEXT + BM * EXT_ROW;
 constexpr int OFF_CN = OFF_EXT + EXT_SLOTS * EXT_SLOT;
 constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;
-constexpr int OFF_BAR = OFF_XCH + BM * 8;
+constexpr int OFF_BAR = OFF_XCH + BM * 12;  // [min | idx | ||x||^2 part] exchange
 constexpr int A_SLOTS_MAX = 8;
 constexpr int NBARS = 2 * A_SLOTS_MAX + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
 constexpr int OFF_OPS = ((OFF_BAR + NBARS * 8 + 16) + 1023) & ~1023;  // 1 KB aligned (SW128)
@@ -514,6 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   float* sCN = reinterpret_cast<float*>(smem + OFF_CN);
   float* xch_m = reinterpret_cast<float*>(smem + OFF_XCH);
   int* xch_i = reinterpret_cast<int*>(smem + OFF_XCH + BM * 4);
+  float* xch_xn = reinterpret_cast<float*>(smem + OFF_XCH + BM * 8);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* a_full = bars + 0;
   uint64_t* a_empty = bars + A_SLOTS_MAX;
@@ -558,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     if (AUG) tma_prefetch_desc(&tmext);
     for (int s = 0; s < A_SLOTS_MAX; ++s) {
       mbar_init(&a_full[s], 1);       // leader's expect_tx (both CTAs' bytes)
-      mbar_init(&a_empty[s], 1 + 4);  // pair-MMA commit + 4 warps of this CTA's WG0
+      mbar_init(&a_empty[s], 1 + (ALT ? 4 : 8));  // pair-MMA commit + the row-norm warps
     }
     for (int s = 0; s < NBUF; ++s) {
       mbar_init(&t_full[s], 1);
@@ -795,8 +800,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             tmem_base + (uint32_t(q * 32) << 16) + buf * BN + (alt ? 0 : wg * (BN / 2));
         uint32_t va[32], vb[32];
         FK_TMEM_LD_32x32b_X32(taddr, va);
-        if (c == 0 && (alt || wg == 0)) {
-          xn = row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane);
+        if (c == 0) {  // ALT: the owning warpgroup; else each warpgroup half the chunk positions
+          xn = alt ? row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane)
+                   : row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane, 4 * wg,
+                                        4 * wg + 4);
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_empty[slot]);
         }
@@ -884,9 +891,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         if (wg == 1) {
           xch_m[row] = M;
           xch_i[row] = idx;
+          xch_xn[row] = xn;
         }
         named_bar_sync(1, 256);
         if (wg == 0) {
+          xn += xch_xn[row];
           const float M1 = xch_m[row];
           const int i1 = xch_i[row];
           if (M1 < M || (M1 == M && i1 >= 0 && (idx < 0 || i1 < idx))) {
