@@ -171,8 +171,13 @@ FK_API fk_status fk_stats_pack(int32_t unpack, int64_t* counts, double* objectiv
  *            is left untouched.
  *   min_d2 : (B,N) f64 scratch (the reference's resident weight table).
  * Distances are computed from the exact f64 upcast of the data (f32, f64,
- * bf16, f16).  Rows need d*8 <= 200 KiB.                                      */
-FK_API size_t fk_kmeanspp_workspace(int64_t B, int64_t N);
+ * bf16, f16).  Rows need d*8 <= 200 KiB.  The in-core sweep skips rows whose
+ * minimum provably cannot change (triangle inequality against the nearest
+ * chosen center, with rounding margins), so later draws read only the rows
+ * near the new center; the results are unchanged bit for bit.                */
+/* K and d size the in-core pruning state of fk_kmeanspp; the streaming pieces
+ * (init / select) need only fk_kmeanspp_workspace(B, N, 0, 0).               */
+FK_API size_t fk_kmeanspp_workspace(int64_t B, int64_t N, int64_t K, int64_t d);
 FK_API fk_status fk_kmeanspp(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t d,
                              int64_t K, const double* u, int64_t* idx, int32_t* halted,
                              double* min_d2, void* workspace, size_t workspace_bytes, void* stream);

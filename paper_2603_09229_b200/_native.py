@@ -55,7 +55,7 @@ def _declare(L):
     L.fk_stats_pack.restype = ctypes.c_int
     L.fk_stats_pack.argtypes = [I32, P, P, P, P, I64, I64, P]
     L.fk_kmeanspp_workspace.restype = SZ
-    L.fk_kmeanspp_workspace.argtypes = [I64, I64]
+    L.fk_kmeanspp_workspace.argtypes = [I64, I64, I64, I64]
     L.fk_kmeanspp.restype = ctypes.c_int
     L.fk_kmeanspp.argtypes = [ctypes.c_int, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]
     L.fk_kmeanspp_init.restype = ctypes.c_int

@@ -216,15 +216,15 @@ fk_status fk_stats_pack(int32_t unpack, int64_t* counts, double* objective, int3
 }
 
 // ------------------------------------------------------------- k-means++
-size_t fk_kmeanspp_workspace(int64_t B, int64_t N) {
-  if (B < 1 || N < 1 || B * N > kMaxPoints) return 0;
-  return fk::kmeanspp_workspace_bytes(B, N);
+size_t fk_kmeanspp_workspace(int64_t B, int64_t N, int64_t K, int64_t d) {
+  if (B < 1 || N < 1 || B * N > kMaxPoints || K < 0 || d < 0) return 0;
+  return fk::kmeanspp_workspace_bytes(B, N, K, d);
 }
 
 fk_status fk_kmeanspp_init(int32_t* halted, int64_t B, int64_t N, int64_t K, void* ws,
                            size_t ws_bytes, void* stream) {
   if (!halted || B < 1 || N < 1 || K < 1 || K > N || B * N > kMaxPoints) return FK_EINVAL;
-  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N)) return FK_EWORKSPACE;
+  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N, 0, 0)) return FK_EWORKSPACE;
   if (dev_info().major != 10) return FK_EUNSUPPORTED;
   return cuda_status(
       fk::launch_kmeanspp_init(halted, ws, B, N, K, reinterpret_cast<cudaStream_t>(stream)));
@@ -250,7 +250,7 @@ fk_status fk_kmeanspp_select(const double* min_d2, int64_t B, int64_t N, const d
   if (!min_d2 || !u || !idx || !halted || B < 1 || N < 1 || K < 2 || K > N || j < 1 || j >= K ||
       B * N > kMaxPoints)
     return FK_EINVAL;
-  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N)) return FK_EWORKSPACE;
+  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N, 0, 0)) return FK_EWORKSPACE;
   if (dev_info().major != 10) return FK_EUNSUPPORTED;
   return cuda_status(fk::launch_kmeanspp_select(min_d2, B, N, u, K, j, idx, halted, ws,
                                                 reinterpret_cast<cudaStream_t>(stream)));
@@ -263,7 +263,7 @@ fk_status fk_kmeanspp(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t 
       K > N || B * N > kMaxPoints || d > (1 << 20) || (int64_t)d * 8 > 200 * 1024)
     return FK_EINVAL;
   if (K > 1 && !u) return FK_EINVAL;
-  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N)) return FK_EWORKSPACE;
+  if (!ws || ws_bytes < fk_kmeanspp_workspace(B, N, K, d)) return FK_EWORKSPACE;
   if (dev_info().major != 10) return FK_EUNSUPPORTED;
   return cuda_status(fk::launch_kmeanspp(dt, X, B, N, d, K, u, idx, halted, min_d2, ws,
                                          reinterpret_cast<cudaStream_t>(stream)));

@@ -57,7 +57,7 @@ cudaError_t launch_stats_pack(int unpack, int64_t* counts, double* obj, int32_t*
                               double* red, int64_t BK, int64_t B, cudaStream_t s);
 
 // fk_kmeanspp.cu
-size_t kmeanspp_workspace_bytes(int64_t B, int64_t N);
+size_t kmeanspp_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d);
 cudaError_t launch_kmeanspp_init(int32_t* halted, void* ws, int64_t B, int64_t N, int64_t K,
                                  cudaStream_t s);
 cudaError_t launch_kmeanspp_sweep(int dt, const void* X, int64_t B, int64_t rows, int64_t d,

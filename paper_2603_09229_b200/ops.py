@@ -217,7 +217,7 @@ def kmeanspp(x: torch.Tensor, clusters: int, first: torch.Tensor, u: torch.Tenso
     halted = torch.empty((B,), dtype=torch.int32, device=dev)
     m = torch.empty((B, n), dtype=torch.float64, device=dev)
     L = N.lib()
-    need = L.fk_kmeanspp_workspace(B, n)
+    need = L.fk_kmeanspp_workspace(B, n, K, d)
     ws = _ws.get(dev, need, "kmeanspp")
     u = u.contiguous()
     st = L.fk_kmeanspp(fk_dtype(x.dtype), x.data_ptr(), B, n, d, K, u.data_ptr() if K > 1 else None,
@@ -239,7 +239,7 @@ class KmeansppStream:
         self.halted = torch.empty((1,), dtype=torch.int32, device=self.dev)
         self.u = torch.zeros((1, max(self.k - 1, 1)), dtype=torch.float64, device=self.dev)
         L = N.lib()
-        need = L.fk_kmeanspp_workspace(1, self.n)
+        need = L.fk_kmeanspp_workspace(1, self.n, 0, 0)
         self.ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.dev)
         N.check(L.fk_kmeanspp_init(self.halted.data_ptr(), 1, self.n, self.k, self.ws.data_ptr(),
                                    self.ws.numel(), _stream(self.dev)), "fk_kmeanspp_init")

@@ -123,3 +123,55 @@ def test_sharded_kmeanspp_device_world1(kpp_golden):
             assert np.array_equal(idx, kpp_golden[name]), name
     finally:
         dist.destroy_process_group()
+
+
+_TIE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+from fractions import Fraction
+from oracle import oracle as O
+from paper_2603_09229_b200 import ops
+
+def crafted(seed, n):
+    # a big first weight and tiny ones whose sum makes the pairwise total exactly 1:
+    # the serial cumsum then adds exact half-ulps (ties to even), whole ulps and
+    # 1.5 ulps, so numpy's chain depends on the parity of S/ulp at every step
+    rng = np.random.default_rng(seed)
+    tiny = rng.choice([2.0**-54, 2.0**-53, 3 * 2.0**-54, 5 * 2.0**-55, 0.0], size=n - 1)
+    rest = sum(Fraction(float(t)) for t in tiny)
+    m0 = float(1 - rest)
+    assert Fraction(m0) == 1 - rest
+    m = np.concatenate([[m0], tiny]).astype(np.float64)
+    perm = rng.permutation(n)          # the big weight anywhere
+    return m[perm]
+
+bad = 0
+for seed in range(6):
+    m = crafted(seed, 6000 + 977 * seed)
+    total = O.pairwise_sum(m)
+    pp = ops.KmeansppStream(m.size, 2, torch.device("cuda", 0))
+    pp.m[0].copy_(torch.from_numpy(m))
+    rng = np.random.default_rng(100 + seed)
+    for u in np.concatenate([rng.random(12), [0.0, 0.5, 1 - 2**-53]]):
+        pp.halted.fill_(2)
+        pp.select(1, float(u))
+        got = int(pp.idx[0, 1].item())
+        ref = O.choice_cdf(m, total, float(u))
+        bad += got != ref
+print("mismatches", bad)
+"""
+
+
+@pytest.mark.parametrize("forced", [False, True])
+def test_cumsum_ties_and_parity(forced):
+    """choice() on crafted tables whose serial cumsum resolves exact half-ulp
+    ties by parity: the certified path and the parallel exact walk (forced)
+    both reproduce numpy's searchsorted index."""
+    code = _TIE_SCRIPT % (ROOT, os.path.join(ROOT, "tests"))
+    env = dict(os.environ)
+    if forced:
+        env["FK_PP_FORCE_EXACT"] = "1"
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "mismatches 0" in r.stdout, r.stdout + r.stderr[-2000:]

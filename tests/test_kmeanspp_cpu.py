@@ -91,8 +91,9 @@ def test_kmeanspp_abi_validates_before_launch():
     from paper_2603_09229_b200 import _native as N
 
     L = N.lib()
-    assert L.fk_kmeanspp_workspace(0, 10) == 0
-    assert L.fk_kmeanspp_workspace(1, 10) > 0
+    assert L.fk_kmeanspp_workspace(0, 10, 3, 4) == 0
+    assert L.fk_kmeanspp_workspace(1, 10, 0, 0) > 0
+    assert L.fk_kmeanspp_workspace(1, 10, 3, 4) > L.fk_kmeanspp_workspace(1, 10, 0, 0)
     # K > N
     assert L.fk_kmeanspp(N.FK_F32, 16, 1, 10, 4, 11, 16, 16, 16, 16, 16, 1 << 20, None) == N.FK_EINVAL
     # missing u with K > 1
