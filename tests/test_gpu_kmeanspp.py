@@ -137,8 +137,11 @@ def crafted(seed, n):
     # the serial cumsum then adds exact half-ulps (ties to even), whole ulps and
     # 1.5 ulps, so numpy's chain depends on the parity of S/ulp at every step
     rng = np.random.default_rng(seed)
-    tiny = rng.choice([2.0**-54, 2.0**-53, 3 * 2.0**-54, 5 * 2.0**-55, 0.0], size=n - 1)
+    tiny = rng.choice([2.0**-54, 2.0**-53, 3 * 2.0**-54, 0.0], size=n - 1)
     rest = sum(Fraction(float(t)) for t in tiny)
+    if (rest / Fraction(2) ** -53).denominator != 1:  # keep 1 - rest a multiple of 2^-53
+        tiny[-1] += 2.0**-54
+        rest += Fraction(2) ** -54
     m0 = float(1 - rest)
     assert Fraction(m0) == 1 - rest
     m = np.concatenate([[m0], tiny]).astype(np.float64)
