@@ -89,3 +89,61 @@ def test_reseed_farthest_streamed_matches_reference(tmp_path, source):
     assert r.iterations_run == int(g["iterations"])
     assert np.array_equal(r.centroids.numpy(), g["centroids"])
     assert np.array_equal(r.assignments.numpy(), g["assignments"])
+
+
+def test_streaming_overlaps_copy_and_compute():
+    """Acceptance criterion 6's overlap half (test_acceptance.py:193-250), on the
+    device: a streamed pass from pinned host memory must take clearly less than
+    copying every chunk plus computing every chunk back to back (double
+    buffers + a copy stream), and at least as long as the longer of the two."""
+    from paper_2603_09229_b200 import ops
+    from paper_2603_09229_b200.pipeline import HostStream, _StreamRunner
+
+    N, K, d, chunk = 1 << 22, 16384, 128, 1 << 19
+    g = torch.Generator(device="cuda").manual_seed(0)
+    xd = (torch.randn((1, N, d), device="cuda", generator=g) * 3).to(torch.bfloat16)
+    host = xd.cpu().pin_memory()
+    c0 = xd[:, :K].float()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    # copy only: every chunk H2D
+    buf = torch.empty((1, chunk, d), dtype=torch.bfloat16, device="cuda")
+    a, b = ev(), ev()
+    torch.cuda.synchronize()
+    a.record()
+    for lo in range(0, N, chunk):
+        buf.copy_(host[:, lo:lo + chunk], non_blocking=True)
+    b.record()
+    torch.cuda.synchronize()
+    t_copy = a.elapsed_time(b)
+    # compute only: assign + update of every (device-resident) chunk
+    ids = torch.empty((1, chunk), dtype=torch.int32, device="cuda")
+    mind = torch.empty((1, chunk), dtype=torch.float32, device="cuda")
+    sums = torch.empty((1, K, d), dtype=torch.float64, device="cuda")
+    counts = torch.empty((1, K), dtype=torch.int64, device="cuda")
+    cop = c0.to(torch.bfloat16)
+    for _ in range(2):
+        ops.assign(xd[:, :chunk], cop, idx_out=ids, mind_out=mind)
+    torch.cuda.synchronize()
+    a.record()
+    for lo in range(0, N, chunk):
+        xc = xd[:, lo:lo + chunk]
+        ops.assign(xc, cop, idx_out=ids, mind_out=mind)
+        ops.update(xc, ids, K, chunk, accumulate=lo > 0, sums=sums, counts=counts)
+    b.record()
+    torch.cuda.synchronize()
+    t_compute = a.elapsed_time(b)
+    # the streamed pass
+    stream = HostStream(host, chunk, pin=False)
+    run = _StreamRunner(stream, K, torch.device("cuda", 0), N)
+    run.set(c0)
+    counters = fk.Counters()
+    run.one_pass(counters)
+    torch.cuda.synchronize()
+    a.record()
+    run.one_pass(counters)
+    b.record()
+    torch.cuda.synchronize()
+    t_pass = a.elapsed_time(b)
+    assert t_pass < 0.85 * (t_copy + t_compute), (t_pass, t_copy, t_compute)
+    assert t_pass > 0.9 * max(t_copy, t_compute), (t_pass, t_copy, t_compute)
