@@ -1,14 +1,15 @@
-"""ops.update at configs 2 and 4 under a CUDA graph (for A/B and ncu launch lists; dev aid).
+"""ops.update at configs 2, 4 and 3 under a CUDA graph (for A/B and ncu launch lists; dev aid).
     FK_UPDATE_CLUSTER=0 selects the global sort path for the small shapes."""
 import sys
 import torch
 sys.path.insert(0, ".")
 from paper_2603_09229_b200 import ops
 shapes = [(1, 1 << 20, 1024, 128, torch.bfloat16), (64, 16384, 256, 64, torch.float16),
-          (64, 16384, 256, 64, torch.bfloat16), (8, 65536, 256, 64, torch.bfloat16)]
+          (64, 16384, 256, 64, torch.bfloat16), (8, 65536, 256, 64, torch.bfloat16),
+          (1, 1 << 23, 4096, 128, torch.bfloat16)]
 import os
 if os.environ.get("SHAPE"):
-    shapes = [shapes[int(os.environ["SHAPE"])]]
+    shapes = [shapes[int(v)] for v in os.environ["SHAPE"].split(",")]
 for (B, N, K, d, dt) in shapes:
     x = torch.randn(B, N, d, device="cuda").to(dt)
     ids = torch.randint(0, K, (B, N), device="cuda", dtype=torch.int32)
