@@ -126,9 +126,10 @@ __global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, 
 // ----------------------------------------------------------------- scan
 // One block of 1024 threads per batch element b.  The block first reduces the
 // histogram of all earlier batch elements (its base offset; b*N when every id
-// is valid), then walks its own K keys in coalesced tiles of 1024: block-wide
-// exclusive scan per tile plus a running carry.  Also produces the int64
-// counts and the reference's synchronized_merges count.
+// is valid), then walks its own K keys in tiles of 4096 (4 consecutive keys
+// per thread, so K <= 4096 is one pass): block-wide exclusive scan per tile
+// plus a running carry.  Also produces the int64 counts and the reference's
+// synchronized_merges count.
 __global__ void __launch_bounds__(1024)
     k_scan(const int32_t* __restrict__ hist, int64_t B, int64_t N, int64_t K, int64_t chunk,
            int accumulate, int64_t* __restrict__ off, int32_t* __restrict__ cursor,
@@ -148,11 +149,16 @@ __global__ void __launch_bounds__(1024)
   __syncthreads();
   unsigned long long mg = 0;
   const uint32_t ch = (uint32_t)chunk;
-  for (int64_t base = 0; base < K; base += 1024) {
-    const int64_t kk = base + t;
-    const int64_t k = b * K + kk;
-    const int64_t c = kk < K ? hist[k] : 0;
-    int64_t v = c;
+  // tiles of 4096 keys, 4 consecutive keys per thread: one pass when K <= 4096
+  for (int64_t base = 0; base < K; base += 4096) {
+    int64_t c[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t kk = base + 4 * t + q;
+      c[q] = kk < K ? hist[b * K + kk] : 0;
+      sum += c[q];
+    }
+    int64_t v = sum;
     for (int o = 1; o < 32; o <<= 1) {
       const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
       if (lane >= o) v += u;
@@ -168,18 +174,24 @@ __global__ void __launch_bounds__(1024)
       warp_tot[lane] = x;  // inclusive over warps
     }
     __syncthreads();
-    const int64_t run = carry + v - c + (w > 0 ? warp_tot[w - 1] : 0);  // exclusive prefix
-    if (kk < K) {
-      off[k] = run;
-      cursor[k] = (int32_t)run;
-      counts[k] = accumulate ? counts[k] + c : c;
-      if (c > 0 && merges) {
-        // reference merges: the run [s, e) of this key inside its batch element
-        // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks
-        // (all quantities < 2^31: 32-bit divisions)
-        const uint32_t s0 = (uint32_t)(run - b * N), e = s0 + (uint32_t)c;
-        mg += (unsigned long long)((e - 1) / ch - s0 / ch + 1);
+    int64_t run = carry + v - sum + (w > 0 ? warp_tot[w - 1] : 0);  // exclusive prefix
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t kk = base + 4 * t + q;
+      if (kk < K) {
+        const int64_t k = b * K + kk;
+        off[k] = run;
+        cursor[k] = (int32_t)run;
+        counts[k] = accumulate ? counts[k] + c[q] : c[q];
+        if (c[q] > 0 && merges) {
+          // reference merges: the run [s, e) of this key inside its batch element
+          // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks
+          // (all quantities < 2^31: 32-bit divisions)
+          const uint32_t s0 = (uint32_t)(run - b * N), e = s0 + (uint32_t)c[q];
+          mg += (unsigned long long)((e - 1) / ch - s0 / ch + 1);
+        }
       }
+      run += c[q];
     }
     carry += warp_tot[31];
     __syncthreads();
@@ -220,6 +232,92 @@ __global__ void __launch_bounds__(1024)
     const int pos = atomicAdd(&sh[id], 1);
     order[pos] = (int32_t)i;
   });
+}
+
+// Staged variant (K <= SC_KMAX): the block's range is processed in sub-tiles
+// of SC_S points.  Each sub-tile is counting-sorted by key in shared memory
+// (local ranks from shared atomics, a block scan of the K counts) and then
+// written out in sorted order, so consecutive threads store consecutive
+// positions of the same key's run: one store instruction touches a few
+// 32-byte sectors instead of 32 scattered ones.  Staged entries pack
+// (local index << 14) | key into 32 bits.
+constexpr int SC_S = 16384;   // points per sub-tile (16 per thread)
+constexpr int SC_KMAX = 4096;  // keys: 3 K-int tables + the stage fit twice per SM
+__global__ void __launch_bounds__(1024)
+    k_scatter_staged(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K, int bpb,
+                     const int32_t* __restrict__ table, int32_t* __restrict__ cursor,
+                     int32_t* __restrict__ order) {
+  extern __shared__ int32_t sm[];
+  __shared__ int32_t wtot[32];
+  int32_t* gcur = sm;          // next global position of each key for this block
+  int32_t* lcnt = sm + K;      // sub-tile counts per key
+  int32_t* lbase = sm + 2 * K;  // exclusive scan of lcnt
+  uint32_t* stage = reinterpret_cast<uint32_t*>(sm + 3 * K);
+  int64_t b, lo, hi;
+  range_of(N, bpb, b, lo, hi);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int32_t* trow = table + (int64_t)blockIdx.x * K;
+  for (int k = t; k < K; k += 1024) {
+    const int32_t c = trow[k];
+    gcur[k] = c ? atomicAdd(&cursor[b * K + k], c) : 0;
+  }
+  for (int64_t s0 = lo; s0 < hi; s0 += SC_S) {
+    const int n = (int)(hi - s0 < SC_S ? hi - s0 : SC_S);
+    for (int k = t; k < K; k += 1024) lcnt[k] = 0;
+    __syncthreads();
+    int32_t id[16], rk[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) id[j] = t + 1024 * j < n ? __ldg(ids + s0 + t + 1024 * j) : -1;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) rk[j] = (id[j] >= 0 && id[j] < K) ? atomicAdd(&lcnt[id[j]], 1) : -1;
+    __syncthreads();
+    // exclusive scan of lcnt: 4 consecutive keys per thread (K <= 4096)
+    int v[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * t + q;
+      v[q] = k < K ? lcnt[k] : 0;
+      sum += v[q];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    if (lane == 31) wtot[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int x = wtot[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += u;
+      }
+      wtot[lane] = x;
+    }
+    __syncthreads();
+    int run = incl - sum + (w ? wtot[w - 1] : 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * t + q;
+      if (k < K) lbase[k] = run;
+      run += v[q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (rk[j] >= 0) stage[lbase[id[j]] + rk[j]] = ((uint32_t)(t + 1024 * j) << 14) | (uint32_t)id[j];
+    __syncthreads();
+    const int tot = wtot[31];
+    for (int p = t; p < tot; p += 1024) {
+      const uint32_t e = stage[p];
+      const int key = (int)(e & 0x3fffu);
+      order[gcur[key] + p - lbase[key]] = (int32_t)(s0 + (e >> 14));
+    }
+    __syncthreads();
+    for (int k = t; k < K; k += 1024) gcur[k] += lcnt[k];
+  }
 }
 
 // Large B*K: warp-aggregated cursor bumps straight in global memory.
@@ -815,7 +913,26 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist, table);
   const int64_t ch = chunk < 1 ? 1 : (chunk > N ? N : chunk);
   k_scan<<<(unsigned)B, 1024, 0, s>>>(hist, B, N, K, ch, accumulate, off, cursor, counts, merges);
-  if (smem_keys)
+  static int staged_env = -1;  // FK_UPDATE_SCATTER=block: the unstaged block scatter (A/B)
+  if (staged_env < 0) {
+    const char* e = getenv("FK_UPDATE_SCATTER");
+    staged_env = (e && e[0] == 'b') ? 0 : 1;
+  }
+  // staged only when a block's range spans at least one full sub-tile: short
+  // ranges pay the per-sub-tile scan and barriers without longer runs
+  // (configs 2 and 4: 3.5K points per block, 72 -> 74 and 62 -> 66 us staged)
+  if (smem_keys && K <= SC_KMAX && staged_env && (N + bpb - 1) / bpb >= SC_S) {
+    const size_t ssm = (3 * K + SC_S) * 4;
+    static int attr_dev_mask = 0;  // one-time per device (keeps graph capture free of it)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_dev_mask & (1 << (dev & 31)))) {
+      cudaFuncSetAttribute(k_scatter_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)((3 * SC_KMAX + SC_S) * 4));
+      attr_dev_mask |= 1 << (dev & 31);
+    }
+    k_scatter_staged<<<blocks, 1024, ssm, s>>>(ids, B, N, K, (int)bpb, table, cursor, order);
+  } else if (smem_keys)
     k_scatter_block<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, table, cursor, order);
   else
     k_scatter<<<(unsigned)((P + 511) / 512 < num_sms * 4 ? (P + 511) / 512 : num_sms * 4), 512, 0,
