@@ -19,7 +19,7 @@ for rep in sys.argv[2:]:
         return v * scale
     for r in rows[2:]:
         name = r[h.index("Kernel Name")]
-        key = next((k for k in ("fk_assign_tc2", "fk_assign_tc", "k_segsum", "k_scatter_block", "k_hist", "k_scan")
+        key = next((k for k in ("fk_assign_tc2", "fk_assign_tc", "k_segsum", "k_scatter_staged", "k_scatter_block", "k_hist", "k_scan")
                     if k in name), name[:40])
         if key == "fk_assign_tc2":
             key = "fk_assign_tc"
