@@ -151,6 +151,27 @@ def test_update_vs_oracle(ops, oracle, B, N, K, d, dtype):
         assert np.all(err <= 1e-6 * scale)
 
 
+@pytest.mark.parametrize("B,N,K", [(1, 5_000_003, 4096), (2, 2_600_001, 3001)])
+def test_update_staged_scatter_vs_oracle(ops, oracle, B, N, K):
+    """Shapes whose per-block point ranges span more than one 16K-point sub-tile
+    on a 148-SM B200 (the staged shared-memory counting sort of the scatter):
+    counts, merges and f32 sums bit-exact against the reference restatement,
+    with ragged sub-tiles and skewed keys."""
+    d = 8
+    g = torch.Generator().manual_seed(N + K)
+    # small integers (as f32): every partial sum is exact in any order
+    x = torch.randint(-8, 9, (B, N, d), generator=g).float()
+    ids = torch.randint(0, K, (B, N), generator=g, dtype=torch.int32)
+    ids[:, : N // 4] = ids[:, : N // 4] % 5
+    merges = torch.zeros((), dtype=torch.int64, device="cuda")
+    sums, counts = ops.update(x.cuda(), ids.cuda(), K, 65536, merges=merges)
+    torch.cuda.synchronize()
+    s_ref, c_ref, m_ref = oracle.sort_inverse_update(x.numpy(), ids.numpy(), K, 65536)
+    assert np.array_equal(counts.cpu().numpy(), c_ref)
+    assert np.array_equal(sums.cpu().numpy(), s_ref)
+    assert int(merges.item()) == m_ref
+
+
 def test_update_accumulate_and_merges(ops, oracle):
     x = torch.randn((1, 10000, 32)).float()
     ids = torch.randint(0, 40, (1, 10000), dtype=torch.int32)
