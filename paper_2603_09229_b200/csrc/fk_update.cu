@@ -555,10 +555,19 @@ __global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restr
 }
 
 // Blocks per batch element for the histogram / scatter passes: ~2 waves in
-// total, each block owning >= 2048 points so the shared histogram amortizes.
+// total, each block owning >= 8192 points so the per-block K-bin table, its
+// scan and its cursor reservations amortize (same-box A/B,
+// profiles/r01_ab_update_bpb.txt: 2048 -> 8192 points took config 2 from 73
+// to 69 us and config 4 from 63 to 57 us; config 3 is capped by the wave count).
 static int64_t update_bpb(int64_t B, int64_t N, int num_sms) {
+  static int64_t min_range = -1;  // FK_UPDATE_MIN_RANGE: points per block lower bound (A/B)
+  if (min_range < 0) {
+    const char* e = getenv("FK_UPDATE_MIN_RANGE");
+    min_range = e ? atoll(e) : 8192;
+    if (min_range < 2048) min_range = 2048;  // the workspace table is sized for >= 2048
+  }
   int64_t bpb = ((int64_t)num_sms * 2 + B - 1) / B;
-  const int64_t max_bpb = (N + 2047) / 2048;
+  const int64_t max_bpb = (N + min_range - 1) / min_range;
   if (bpb > max_bpb) bpb = max_bpb;
   return bpb < 1 ? 1 : bpb;
 }
