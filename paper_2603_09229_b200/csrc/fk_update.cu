@@ -407,7 +407,7 @@ template <typename T, typename A, int LPR, int VPL, int U>
 __global__ void __launch_bounds__(256)
     k_segsum(const T* __restrict__ X, const int32_t* __restrict__ order,
              const int64_t* __restrict__ off, int64_t BK, int64_t P, int64_t L, int64_t d,
-             double* __restrict__ sums) {
+             double* __restrict__ sums, const int32_t* __restrict__ ids, int64_t N, int64_t K) {
   constexpr int E = VecCvt<T>::E;
   constexpr int RPW = 32 / LPR;
   constexpr int NA = VPL * E;
@@ -417,13 +417,20 @@ __global__ void __launch_bounds__(256)
   const int64_t p0 = wg * L;
   if (p0 >= P) return;
   const int64_t p1 = (p0 + L < P) ? p0 + L : P;
-  // segment containing p0: largest key with off[key] <= p0 < off[key+1]
-  int64_t lo = 0, hi = BK;
-  while (hi - lo > 1) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (off[mid] <= p0) lo = mid; else hi = mid;
+  // segment containing p0 (largest key with off[key] <= p0 < off[key+1]) is
+  // the key of the point sorted to p0: two dependent loads instead of a
+  // log2(BK)-step binary search over off[]
+  const int32_t pt = order[p0];
+  const int64_t pb = pt / N;
+  int64_t key = pb * K + ids[pt];
+  if (key < 0 || key >= BK || off[key] > p0 || off[key + 1] <= p0) {
+    int64_t lo = 0, hi = BK;  // defensive (ids are validated by the caller)
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (off[mid] <= p0) lo = mid; else hi = mid;
+    }
+    key = lo;
   }
-  int64_t key = lo;
   int64_t seg_lo = off[key], seg_end = off[key + 1];
   A acc[NA];
 #pragma unroll
@@ -853,10 +860,19 @@ size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K) {
 template <typename T, typename A>
 static cudaError_t dispatch_segsum(const void* X, const int32_t* order, const int64_t* off,
                                    int64_t BK, int64_t P, int64_t d, double* sums, int num_sms,
-                                   cudaStream_t s) {
+                                   cudaStream_t s, const int32_t* ids, int64_t N, int64_t K) {
   constexpr int E = VecCvt<T>::E;
   const int th = 256;
-  const int64_t want_warps = (int64_t)num_sms * 8 * (th / 32);
+  // warp slices per SM: 32 (same-box A/B, profiles/r01_ab_segsum.txt: 64 -> 32
+  // took config 2 from 67.8 to 64.1 us and config 4 from 52 to 49.5 us, config 3
+  // unchanged; 16 starves config 3 of bytes in flight).  FK_SEGSUM_WPS overrides.
+  static int wps = -1;
+  if (wps < 0) {
+    const char* e = getenv("FK_SEGSUM_WPS");
+    wps = e ? atoi(e) : 32;
+    if (wps < 1) wps = 32;
+  }
+  const int64_t want_warps = (int64_t)num_sms * wps;
   int64_t L = (P + want_warps - 1) / want_warps;
   if (L < 64) L = 64;
   const int64_t warps = (P + L - 1) / L;
@@ -866,7 +882,7 @@ static cudaError_t dispatch_segsum(const void* X, const int32_t* order, const in
   const int64_t nvec = row_bytes / 16;  // 16-byte vectors per row
   const T* x = (const T*)X;
 #define FK_SEG(LPR, VPL, U) \
-  k_segsum<T, A, LPR, VPL, U><<<grid, th, 0, s>>>(x, order, off, BK, P, L, d, sums)
+  k_segsum<T, A, LPR, VPL, U><<<grid, th, 0, s>>>(x, order, off, BK, P, L, d, sums, ids, N, K)
   if (vec_ok) {
     switch (nvec) {
       case 1: FK_SEG(1, 1, 4); break;
@@ -948,10 +964,10 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
                 s>>>(ids, B, N, K, cursor, order);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   switch (dt) {
-    case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, order, off, BK, P, d, sums, num_sms, s);
-    case DT_F16: return dispatch_segsum<__half, float>(X, order, off, BK, P, d, sums, num_sms, s);
-    case DT_F32: return dispatch_segsum<float, double>(X, order, off, BK, P, d, sums, num_sms, s);
-    default: return dispatch_segsum<double, double>(X, order, off, BK, P, d, sums, num_sms, s);
+    case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, order, off, BK, P, d, sums, num_sms, s, ids, N, K);
+    case DT_F16: return dispatch_segsum<__half, float>(X, order, off, BK, P, d, sums, num_sms, s, ids, N, K);
+    case DT_F32: return dispatch_segsum<float, double>(X, order, off, BK, P, d, sums, num_sms, s, ids, N, K);
+    default: return dispatch_segsum<double, double>(X, order, off, BK, P, d, sums, num_sms, s, ids, N, K);
   }
 }
 
