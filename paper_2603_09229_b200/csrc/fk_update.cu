@@ -972,38 +972,77 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
 }
 
 // ----------------------------------------------------------------- normalize
+constexpr int NORM_RW = 4;  // centroid rows per warp in k_normalize
+
 template <typename TM, typename TO>
 __global__ void __launch_bounds__(256)
     k_normalize(const double* __restrict__ sums, const int64_t* __restrict__ counts,
-                const TM* prev, TM* out, TO* operand, uint8_t* empty, double* max_shift2,
-                int64_t BK, int64_t d) {
+                const TM* __restrict__ prev, TM* __restrict__ out, TO* __restrict__ operand,
+                uint8_t* __restrict__ empty, double* max_shift2, int64_t BK, int64_t d) {
   __shared__ double wmax[8];
-  const int64_t row = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  // NORM_RW rows per warp, every load of a pass (64 columns of each row) issued
+  // before the first division so the latencies overlap, and 4x fewer blocks
+  // (and shift atomics).  Each element is read and written by the same thread
+  // only, so out may alias prev.
+  constexpr int RW = NORM_RW, NR = 2;
+  const int64_t row0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * RW;
   const int lane = threadIdx.x & 31;
-  double sh = 0.0;
-  if (row < BK) {
-    const int64_t cnt = counts[row];
-    for (int64_t j = lane; j < d; j += 32) {
-      const int64_t o = row * d + j;
-      const TM old = prev[o];
-      TM nv = old;
-      if (cnt > 0) nv = (TM)(sums[o] / (double)cnt);  // correctly rounded, as numpy
-      out[o] = nv;
-      if (operand) operand[o] = (TO)(float)nv;
-      const double df = (double)nv - (double)old;
-      sh += df * df;
-    }
-    if (lane == 0 && empty) empty[row] = cnt > 0 ? 0 : 1;
+  int64_t cnt[RW];
+  double sh[RW];
+#pragma unroll
+  for (int q = 0; q < RW; ++q) {
+    cnt[q] = row0 + q < BK ? counts[row0 + q] : 0;
+    sh[q] = 0.0;
+  }
+  for (int64_t j0 = 0; j0 < d; j0 += 32 * NR) {
+    double sv[RW][NR];
+    TM pv[RW][NR];
+#pragma unroll
+    for (int q = 0; q < RW; ++q)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int64_t j = j0 + lane + 32 * r;
+        if (row0 + q < BK && j < d) {
+          sv[q][r] = sums[(row0 + q) * d + j];
+          pv[q][r] = prev[(row0 + q) * d + j];
+        }
+      }
+#pragma unroll
+    for (int q = 0; q < RW; ++q)
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const int64_t j = j0 + lane + 32 * r;
+        if (row0 + q < BK && j < d) {
+          const int64_t o = (row0 + q) * d + j;
+          TM nv = pv[q][r];
+          if (cnt[q] > 0) nv = (TM)(sv[q][r] / (double)cnt[q]);  // correctly rounded, as numpy
+          out[o] = nv;
+          if (operand) operand[o] = (TO)(float)nv;
+          const double df = (double)nv - (double)pv[q][r];
+          sh[q] += df * df;
+        }
+      }
+  }
+  if (lane == 0 && empty) {
+#pragma unroll
+    for (int q = 0; q < RW; ++q)
+      if (row0 + q < BK) empty[row0 + q] = cnt[q] > 0 ? 0 : 1;
   }
   if (max_shift2) {
-    for (int o = 16; o; o >>= 1) sh += __shfl_xor_sync(0xffffffffu, sh, o);
-    if (lane == 0) wmax[threadIdx.x >> 5] = sh;
+    double m = 0.0;
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      double v = sh[q];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      m = fmax(m, v);
+    }
+    if (lane == 0) wmax[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x == 0) {
-      double m = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, wmax[w]);
+      double mb = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mb = fmax(mb, wmax[w]);
       // non-negative doubles order like their bit patterns
-      atomicMax((unsigned long long*)max_shift2, (unsigned long long)__double_as_longlong(m));
+      atomicMax((unsigned long long*)max_shift2, (unsigned long long)__double_as_longlong(mb));
     }
   }
 }
@@ -1013,7 +1052,8 @@ static cudaError_t norm_dispatch(int operand_dt, const double* sums, const int64
                                  const void* prev, void* out, void* operand_out, uint8_t* empty,
                                  double* ms2, int64_t BK, int64_t d, cudaStream_t s) {
   const int th = 256;
-  const unsigned grid = (unsigned)((BK * 32 + th - 1) / th);
+  const int64_t rows_per_block = (th / 32) * NORM_RW;
+  const unsigned grid = (unsigned)((BK + rows_per_block - 1) / rows_per_block);
   const TM* pv = (const TM*)prev;
   TM* ov = (TM*)out;
   if (!operand_out)
