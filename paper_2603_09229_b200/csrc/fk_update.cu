@@ -241,9 +241,14 @@ __global__ void __launch_bounds__(1024)
 // positions of the same key's run: one store instruction touches a few
 // 32-byte sectors instead of 32 scattered ones.  Staged entries pack
 // (local index << 14) | key into 32 bits.
-constexpr int SC_S = 16384;   // points per sub-tile (16 per thread)
+#ifndef FK_SC_PT
+#define FK_SC_PT 16
+#endif
+constexpr int SC_PT = FK_SC_PT;      // points per thread per sub-tile
+constexpr int SC_S = 1024 * SC_PT;   // points per sub-tile
+constexpr int SC_MIN_RANGE = 16384;  // staged only for block ranges at least this long
 constexpr int SC_KMAX = 4096;  // keys: 3 K-int tables + the stage fit twice per SM
-__global__ void __launch_bounds__(1024)
+__global__ void __launch_bounds__(1024, SC_PT <= 8 ? 2 : 1)
     k_scatter_staged(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K, int bpb,
                      const int32_t* __restrict__ table, int32_t* __restrict__ cursor,
                      int32_t* __restrict__ order) {
@@ -265,11 +270,11 @@ __global__ void __launch_bounds__(1024)
     const int n = (int)(hi - s0 < SC_S ? hi - s0 : SC_S);
     for (int k = t; k < K; k += 1024) lcnt[k] = 0;
     __syncthreads();
-    int32_t id[16], rk[16];
+    int32_t id[SC_PT], rk[SC_PT];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) id[j] = t + 1024 * j < n ? __ldg(ids + s0 + t + 1024 * j) : -1;
+    for (int j = 0; j < SC_PT; ++j) id[j] = t + 1024 * j < n ? __ldg(ids + s0 + t + 1024 * j) : -1;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) rk[j] = (id[j] >= 0 && id[j] < K) ? atomicAdd(&lcnt[id[j]], 1) : -1;
+    for (int j = 0; j < SC_PT; ++j) rk[j] = (id[j] >= 0 && id[j] < K) ? atomicAdd(&lcnt[id[j]], 1) : -1;
     __syncthreads();
     // exclusive scan of lcnt: 4 consecutive keys per thread (K <= 4096)
     int v[4], sum = 0;
@@ -306,7 +311,7 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < SC_PT; ++j)
       if (rk[j] >= 0) stage[lbase[id[j]] + rk[j]] = ((uint32_t)(t + 1024 * j) << 14) | (uint32_t)id[j];
     __syncthreads();
     const int tot = wtot[31];
@@ -946,7 +951,7 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   // staged only when a block's range spans at least one full sub-tile: short
   // ranges pay the per-sub-tile scan and barriers without longer runs
   // (configs 2 and 4: 3.5K points per block, 72 -> 74 and 62 -> 66 us staged)
-  if (smem_keys && K <= SC_KMAX && staged_env && (N + bpb - 1) / bpb >= SC_S) {
+  if (smem_keys && K <= SC_KMAX && staged_env && (N + bpb - 1) / bpb >= SC_MIN_RANGE) {
     const size_t ssm = (3 * K + SC_S) * 4;
     static int attr_dev_mask = 0;  // one-time per device (keeps graph capture free of it)
     int dev = 0;
