@@ -395,7 +395,6 @@ constexpr int BN = 256;                  // centroids per pair tile
 constexpr int BNH = 128;                 // centroids staged per CTA
 constexpr int NBUF = 2;                  // TMEM accumulators (2 x 256 columns)
 constexpr int A_ATOM = BM * 128;         // 16 KB
-constexpr int A_SLOT = 2 * A_ATOM;       // d <= 128
 constexpr int B_STAGE = BNH * 128;       // 16 KB per CTA
 constexpr int STAGES = 6;
 constexpr int CN_SLOTS = 6;              // ||c||^2 ring (bias in the epilogue)

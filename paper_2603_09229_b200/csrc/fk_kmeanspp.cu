@@ -196,28 +196,6 @@ FK_DEV double pw_row(const T* x, const double* c, int n) {
   return n <= kLeaf ? pw_leaf_row<T>(x, c, n) : pw_row_rec<T>(x, c, n);
 }
 
-// numpy pairwise_sum leaf over a plain f64 array (n <= 128).
-FK_DEV double pw_leaf_arr(const double* a, int n) {
-  if (n < 8) {
-    double res = 0.;
-    for (int i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
-  }
-  double r[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) r[k] = a[k];
-  int i = 8;
-  const int body = n - (n % 8);
-  for (; i < body; i += 8) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) r[k] = __dadd_rn(r[k], a[i + k]);
-  }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-  return res;
-}
-
 // ------------------------------------------------------------ double-double
 struct DD {
   double hi, lo;
