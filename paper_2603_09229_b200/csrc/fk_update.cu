@@ -246,7 +246,10 @@ __global__ void __launch_bounds__(1024)
 #endif
 constexpr int SC_PT = FK_SC_PT;      // points per thread per sub-tile
 constexpr int SC_S = 1024 * SC_PT;   // points per sub-tile
-constexpr int SC_MIN_RANGE = 16384;  // staged only for block ranges at least this long
+#ifndef FK_SC_MIN_RANGE
+#define FK_SC_MIN_RANGE 8192
+#endif
+constexpr int SC_MIN_RANGE = FK_SC_MIN_RANGE;  // staged only for block ranges at least this long
 constexpr int SC_KMAX = 4096;  // keys: 3 K-int tables + the stage fit twice per SM
 __global__ void __launch_bounds__(1024, SC_PT <= 8 ? 2 : 1)
     k_scatter_staged(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K, int bpb,
@@ -948,9 +951,10 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
     const char* e = getenv("FK_UPDATE_SCATTER");
     staged_env = (e && e[0] == 'b') ? 0 : 1;
   }
-  // staged only when a block's range spans at least one full sub-tile: short
-  // ranges pay the per-sub-tile scan and barriers without longer runs
-  // (configs 2 and 4: 3.5K points per block, 72 -> 74 and 62 -> 66 us staged)
+  // staged only for block ranges of >= 8K points: shorter ranges pay the
+  // per-sub-tile scan and barriers without longer runs (3.5K-point ranges:
+  // 72 -> 74 us at config 2, 62 -> 66 us at config 4); with the 8K-point
+  // blocks of update_bpb it is 3-4% faster there (profiles/r01_ab_scatter_min_range.txt)
   if (smem_keys && K <= SC_KMAX && staged_env && (N + bpb - 1) / bpb >= SC_MIN_RANGE) {
     const size_t ssm = (3 * K + SC_S) * 4;
     static int attr_dev_mask = 0;  // one-time per device (keeps graph capture free of it)
