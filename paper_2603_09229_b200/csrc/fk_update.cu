@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(1024)
 constexpr int SC_PT = FK_SC_PT;      // points per thread per sub-tile
 constexpr int SC_S = 1024 * SC_PT;   // points per sub-tile
 #ifndef FK_SC_MIN_RANGE
-#define FK_SC_MIN_RANGE 8192
+#define FK_SC_MIN_RANGE 6144
 #endif
 constexpr int SC_MIN_RANGE = FK_SC_MIN_RANGE;  // staged only for block ranges at least this long
 constexpr int SC_KMAX = 4096;  // keys: 3 K-int tables + the stage fit twice per SM
@@ -951,10 +951,12 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
     const char* e = getenv("FK_UPDATE_SCATTER");
     staged_env = (e && e[0] == 'b') ? 0 : 1;
   }
-  // staged only for block ranges of >= 8K points: shorter ranges pay the
+  // staged only for block ranges of >= 6K points: shorter ranges pay the
   // per-sub-tile scan and barriers without longer runs (3.5K-point ranges:
   // 72 -> 74 us at config 2, 62 -> 66 us at config 4); with the 8K-point
-  // blocks of update_bpb it is 3-4% faster there (profiles/r01_ab_scatter_min_range.txt)
+  // blocks of update_bpb it is 3-4% faster there (profiles/r01_ab_scatter_min_range.txt).
+  // update_bpb gives ranges in (4K, 8K] unless the wave cap binds, so the
+  // threshold sits inside that interval rather than at its top.
   if (smem_keys && K <= SC_KMAX && staged_env && (N + bpb - 1) / bpb >= SC_MIN_RANGE) {
     const size_t ssm = (3 * K + SC_S) * 4;
     static int attr_dev_mask = 0;  // one-time per device (keeps graph capture free of it)
