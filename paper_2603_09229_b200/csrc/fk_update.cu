@@ -90,10 +90,26 @@ __device__ __forceinline__ void for_each_id(const int32_t* __restrict__ ids, int
   for (int64_t i = a + 4 * nv + t; i < hi; i += nt) f(i, __ldg(ids + i));
 }
 
+// zero_sums (non-accumulating updates): the blocks also clear the f64 sums
+// for k_segsum, a grid-strided slice each, instead of a separate memset.
 __global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, int64_t B, int64_t N,
                                                int64_t K, int bpb, int32_t* __restrict__ hist,
-                                               int32_t* __restrict__ table) {
+                                               int32_t* __restrict__ table,
+                                               double* __restrict__ zero_sums, int64_t zero_n) {
   extern __shared__ int32_t sh[];
+  if (zero_sums) {
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n2 = zero_n >> 1;  // 16-byte stores when the (caller-owned) buffer allows
+    double2* z2 = reinterpret_cast<double2*>(zero_sums);
+    if ((reinterpret_cast<uintptr_t>(zero_sums) & 15) == 0) {
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += nt)
+        z2[i] = make_double2(0.0, 0.0);
+      if ((zero_n & 1) && blockIdx.x == 0 && threadIdx.x == 0) zero_sums[zero_n - 1] = 0.0;
+    } else {
+      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < zero_n; i += nt)
+        zero_sums[i] = 0.0;
+    }
+  }
   const bool use_smem = K <= HIST_SMEM_KEYS;
   int64_t b, lo, hi;
   range_of(N, bpb, b, lo, hi);
@@ -938,12 +954,13 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   int32_t* table = (int32_t*)w;  // per-block histograms (shared-histogram path)
   cudaError_t e;
   if ((e = cudaMemsetAsync(hist, 0, BK * 4, s)) != cudaSuccess) return e;
-  if (!accumulate && (e = cudaMemsetAsync(sums, 0, BK * d * 8, s)) != cudaSuccess) return e;
+  // sums are cleared inside k_hist (below) unless accumulating
   const int64_t bpb = update_bpb(B, N, num_sms < kMaxSms ? num_sms : kMaxSms);
   const unsigned blocks = (unsigned)(B * bpb);
   const bool smem_keys = K <= HIST_SMEM_KEYS;
   const size_t hsm = smem_keys ? K * 4 : 0;
-  k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist, table);
+  k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist, table, accumulate ? nullptr : sums,
+                                   BK * d);
   const int64_t ch = chunk < 1 ? 1 : (chunk > N ? N : chunk);
   k_scan<<<(unsigned)B, 1024, 0, s>>>(hist, B, N, K, ch, accumulate, off, cursor, counts, merges);
   static int staged_env = -1;  // FK_UPDATE_SCATTER=block: the unstaged block scatter (A/B)
