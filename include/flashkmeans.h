@@ -149,6 +149,15 @@ FK_API fk_status fk_scatter(fk_dtype dt, const void* X, const int32_t* ids, int6
  * each way around the per-iteration NCCL all-reduce of the point-sharded path. */
 FK_API fk_status fk_stats_pack(int32_t unpack, int64_t* counts, double* objective, int32_t* changed,
                                double* red, int64_t BK, int64_t B, void* stream);
+/* The reference's synchronized_merges for one update over GLOBAL counts
+ * (B,K) int64 -- sort_inverse.py:159-165 evaluated on the all-reduced counts,
+ * so a point-sharded run reports the single-process count: each non-empty
+ * key's run [s, e) of its batch element meets floor((e-1)/chunk) -
+ * floor(s/chunk) + 1 update chunks.  *merges = result (accumulate = 0) or
+ * += result.                                                                 */
+FK_API fk_status fk_merges_from_counts(const int64_t* counts, int64_t B, int64_t K,
+                                       int64_t update_chunk, int64_t* merges, int32_t accumulate,
+                                       void* stream);
 
 /* ------------------------------------------------------------- k-means++
  * D^2 seeding of init_centroids(method="kmeanspp") on the device:

@@ -54,6 +54,8 @@ def _declare(L):
     L.fk_scatter.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, P, P, P]
     L.fk_stats_pack.restype = ctypes.c_int
     L.fk_stats_pack.argtypes = [I32, P, P, P, P, I64, I64, P]
+    L.fk_merges_from_counts.restype = ctypes.c_int
+    L.fk_merges_from_counts.argtypes = [P, I64, I64, I64, P, I32, P]
     L.fk_kmeanspp_workspace.restype = SZ
     L.fk_kmeanspp_workspace.argtypes = [I64, I64, I64, I64]
     L.fk_kmeanspp.restype = ctypes.c_int
@@ -71,8 +73,8 @@ EXPORTED = (
     "fk_version", "fk_status_string", "fk_last_cuda_error", "fk_device_supported",
     "fk_assign_workspace", "fk_assign", "fk_update_workspace", "fk_update", "fk_normalize",
     "fk_row_norms", "fk_objective_workspace", "fk_objective", "fk_scatter",
-    "fk_stats_pack", "fk_kmeanspp_workspace", "fk_kmeanspp", "fk_kmeanspp_init", "fk_kmeanspp_sweep",
-    "fk_kmeanspp_select",
+    "fk_stats_pack", "fk_merges_from_counts", "fk_kmeanspp_workspace", "fk_kmeanspp",
+    "fk_kmeanspp_init", "fk_kmeanspp_sweep", "fk_kmeanspp_select",
 )
 
 

@@ -215,6 +215,13 @@ fk_status fk_stats_pack(int32_t unpack, int64_t* counts, double* objective, int3
                                            reinterpret_cast<cudaStream_t>(stream)));
 }
 
+fk_status fk_merges_from_counts(const int64_t* counts, int64_t B, int64_t K, int64_t update_chunk,
+                                int64_t* merges, int32_t accumulate, void* stream) {
+  if (!counts || !merges || B < 1 || K < 1 || update_chunk < 1) return FK_EINVAL;
+  return cuda_status(fk::launch_merges_counts(counts, B, K, update_chunk, merges, accumulate ? 1 : 0,
+                                              reinterpret_cast<cudaStream_t>(stream)));
+}
+
 // ------------------------------------------------------------- k-means++
 size_t fk_kmeanspp_workspace(int64_t B, int64_t N, int64_t K, int64_t d) {
   if (B < 1 || N < 1 || B * N > kMaxPoints || K < 0 || d < 0) return 0;

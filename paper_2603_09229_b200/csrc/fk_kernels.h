@@ -55,6 +55,8 @@ cudaError_t launch_scatter(int dt, const void* X, const int32_t* ids, int64_t B,
 
 cudaError_t launch_stats_pack(int unpack, int64_t* counts, double* obj, int32_t* changed,
                               double* red, int64_t BK, int64_t B, cudaStream_t s);
+cudaError_t launch_merges_counts(const int64_t* counts, int64_t B, int64_t K, int64_t chunk,
+                                 int64_t* merges, int accumulate, cudaStream_t s);
 
 // fk_kmeanspp.cu
 size_t kmeanspp_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d);

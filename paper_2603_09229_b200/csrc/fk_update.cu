@@ -863,6 +863,58 @@ __global__ void k_stats_unpack(const double* __restrict__ red, int64_t* __restri
   else if (i < BK + B) obj[i - BK] = red[i];
   else if (i == BK + B) *changed = red[i] > 0.0 ? 1 : 0;
 }
+// The reference's synchronized_merges for GLOBAL counts (sharded runs): each
+// key's run [s, e) in its batch element's sorted order meets
+// floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks (sort_inverse.py:159-165),
+// s the exclusive prefix of the counts.  One block walks every batch element
+// (B*K is small), so the result is stored, not accumulated.
+__global__ void __launch_bounds__(1024)
+    k_merges_counts(const int64_t* __restrict__ counts, int64_t B, int64_t K, int64_t chunk,
+                    int64_t* __restrict__ merges, int accumulate) {
+  __shared__ int64_t wtot[32];
+  __shared__ unsigned long long wmg[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  unsigned long long mg = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    int64_t carry = 0;
+    for (int64_t base = 0; base < K; base += 1024) {
+      const int64_t k = base + t;
+      const int64_t c = k < K ? counts[b * K + k] : 0;
+      int64_t v = c;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+      }
+      if (lane == 31) wtot[w] = v;
+      __syncthreads();
+      int64_t before = 0, tot = 0;
+      for (int q = 0; q < 32; ++q) {
+        if (q < w) before += wtot[q];
+        tot += wtot[q];
+      }
+      if (c > 0) {
+        const int64_t s0 = carry + before + v - c, e = s0 + c;
+        mg += (unsigned long long)((e - 1) / chunk - s0 / chunk + 1);
+      }
+      carry += tot;
+      __syncthreads();
+    }
+  }
+  for (int o = 16; o; o >>= 1) mg += __shfl_xor_sync(0xffffffffu, mg, o);
+  if (lane == 0) wmg[w] = mg;
+  __syncthreads();
+  if (t == 0) {
+    unsigned long long m = 0;
+    for (int q = 0; q < 32; ++q) m += wmg[q];
+    *merges = accumulate ? *merges + (int64_t)m : (int64_t)m;
+  }
+}
+cudaError_t launch_merges_counts(const int64_t* counts, int64_t B, int64_t K, int64_t chunk,
+                                 int64_t* merges, int accumulate, cudaStream_t s) {
+  k_merges_counts<<<1, 1024, 0, s>>>(counts, B, K, chunk < 1 ? 1 : chunk, merges, accumulate);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_stats_pack(int unpack, int64_t* counts, double* obj, int32_t* changed,
                               double* red, int64_t BK, int64_t B, cudaStream_t s) {
   const int64_t n = BK + B + 1;

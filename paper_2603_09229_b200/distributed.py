@@ -21,7 +21,7 @@ import torch
 import torch.distributed as dist
 
 from .core import Assignments, Centroids, Counters, KMeansConfig, KMeansResult, init_indices
-from .pipeline import LloydEngine
+from .pipeline import LloydEngine, _farthest
 
 __all__ = ["shard_bounds", "make_allreduce", "init_centroids_sharded", "kmeanspp_indices_sharded",
            "reseed_farthest_sharded", "lloyd_run_sharded"]
@@ -135,41 +135,27 @@ def init_centroids_sharded(x_shard: torch.Tensor, total_points: int, lo: int, cl
 def reseed_farthest_sharded(eng: LloydEngine, lo: int, group=None) -> None:
     """reseed_farthest (pipeline.py:76-89) over row shards: each empty cluster, in
     id order, takes the next point by decreasing assigned distance, ties to the
-    lowest GLOBAL index.  Each rank proposes its local top-E (stable sort:
-    distance desc, index asc); the candidates are all-gathered in rank order
-    (= global index order), so one stable sort of the union gives the global
-    order; the rows come from their owners through one all-reduce.  The empty
-    mask is replicated (counts are all-reduced), so every rank reseeds alike."""
+    lowest GLOBAL index (pipeline._farthest: local top-E per rank, all-gathered
+    in rank order); the rows come from their owners through one all-reduce.
+    The empty mask is replicated (counts are all-reduced), so every rank
+    reseeds alike."""
     nxt = eng.cur ^ 1
     em = eng.empty.cpu().numpy()
     if not em.any():
         return
-    world = dist.get_world_size(group)
     n_local, d, dev = eng.N, eng.d, eng.dev
     for b in range(eng.B):
         empties = np.flatnonzero(em[b])
-        E = int(empties.size)
-        if E == 0:
+        if empties.size == 0:
             continue
-        md = eng.mind[b].double()
-        take = min(E, n_local)
-        order = torch.sort(-md, stable=True).indices[:take]
-        cand_d = torch.full((E,), float("-inf"), dtype=torch.float64, device=dev)
-        cand_i = torch.full((E,), -1.0, dtype=torch.float64, device=dev)
-        cand_d[:take] = md[order]
-        cand_i[:take] = (order + lo).double()
-        all_d = torch.empty((world * E,), dtype=torch.float64, device=dev)
-        all_i = torch.empty((world * E,), dtype=torch.float64, device=dev)
-        dist.all_gather(list(all_d.view(world, E).unbind(0)), cand_d, group=group)
-        dist.all_gather(list(all_i.view(world, E).unbind(0)), cand_i, group=group)
-        win = torch.sort(-all_d, stable=True).indices[:E]  # rank order = global index order on ties
-        gidx = all_i[win].long()
-        rows = torch.zeros((E, d), dtype=torch.float64, device=dev)
+        gidx = torch.from_numpy(_farthest(eng.mind[b], int(empties.size), lo,
+                                          group if group is not None else dist.group.WORLD)).to(dev)
+        rows = torch.zeros((gidx.numel(), d), dtype=torch.float64, device=dev)
         mine = (gidx >= lo) & (gidx < lo + n_local)
         if bool(mine.any()):
             rows[mine] = eng.x[b, gidx[mine] - lo].double()
         dist.all_reduce(rows, op=dist.ReduceOp.SUM, group=group)
-        cid = torch.from_numpy(empties).to(dev)
+        cid = torch.from_numpy(empties[: gidx.numel()]).to(dev)
         eng.master[nxt][b, cid] = rows.to(eng.mdtype)
         if eng.operand is not eng.master:
             eng.operand[nxt][b, cid] = rows.to(eng.dtype)
@@ -209,10 +195,9 @@ def lloyd_run_sharded(x_shard: torch.Tensor, total_points: int, lo: int, cfg: KM
         merges = int(eng.merges.item())
     if x_shard.is_cuda:
         torch.cuda.synchronize(x_shard.device)
-    # merges: each rank counted its own shard's segments; the reference count is global
-    mg = torch.tensor([float(merges)], dtype=torch.float64, device=x_shard.device)
-    dist.all_reduce(mg, op=dist.ReduceOp.SUM, group=group)
-    counters.synchronized_merges += int(mg.item())
+    # merges: LloydEngine.exchange re-evaluates the count on the all-reduced
+    # counts, so it is already the single-process (global) figure on every rank
+    counters.synchronized_merges += int(merges)
     return KMeansResult(Centroids(eng.centroids.clone(), check_finite=False),
                         Assignments(eng.ids[slot].clone(), validate=False),
                         history[:iterations].cpu().numpy(), iterations, counters)

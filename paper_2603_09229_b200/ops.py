@@ -271,3 +271,13 @@ def stats_pack(counts: torch.Tensor, obj: torch.Tensor, changed: torch.Tensor, r
     st = N.lib().fk_stats_pack(1 if unpack else 0, counts.data_ptr(), obj.data_ptr(), changed.data_ptr(),
                                red_tail.data_ptr(), BK, B, _stream(dev))
     N.check(st, "fk_stats_pack")
+
+
+def merges_from_counts(counts: torch.Tensor, chunk: int, out: torch.Tensor, accumulate: bool = False) -> None:
+    """The reference's synchronized_merges for one update, from GLOBAL (B,K) int64
+    counts (sharded runs: evaluated after the all-reduce); ``out`` int64 scalar."""
+    dev = _require_cuda(counts, out)
+    B, K = counts.shape
+    st = N.lib().fk_merges_from_counts(counts.data_ptr(), B, K, int(chunk), out.data_ptr(),
+                                       1 if accumulate else 0, _stream(dev))
+    N.check(st, "fk_merges_from_counts")

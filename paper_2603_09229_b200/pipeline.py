@@ -39,7 +39,7 @@ from .flash_assign import TilingConfig
 from .tuner import CacheModel, ProblemShape, heuristic_config
 
 __all__ = ["LloydEngine", "HostStream", "ChunkStream", "PartialStats", "DeviceAssignmentStore",
-           "lloyd_run", "out_of_core_iteration", "chunked_stream_run", "ENGINES"]
+           "lloyd_run", "out_of_core_iteration", "chunked_stream_run", "stream_shard", "ENGINES"]
 
 ENGINES = ("flash", "baseline")
 
@@ -197,6 +197,9 @@ class LloydEngine:
             self.counts.copy_(self.counts_f)
             self.obj.copy_(self.obj_red)
             self.changed.copy_((self.changed_f[0] > 0).to(torch.int32))
+        # the reference's merge count is a function of the GLOBAL sorted order:
+        # re-evaluate it on the reduced counts (each shard counted its own runs)
+        self.be.merges_from_counts(self.counts, self.chunk, self.merges_it)
 
     # ------------------------------------------------- pipelined iteration
     # Split of one iteration into (assign) and (rest) so that the NEXT
@@ -321,9 +324,8 @@ class LloydEngine:
             empties = np.flatnonzero(em[b])
             if empties.size == 0:
                 continue
-            order = torch.sort(-self.mind[b].double(), stable=True).indices
-            rows = order[: empties.size]
-            cid = torch.from_numpy(empties).to(self.dev)
+            rows = torch.from_numpy(_farthest(self.mind[b], int(empties.size), 0)).to(self.dev)
+            cid = torch.from_numpy(empties[: rows.numel()]).to(self.dev)
             self.master[nxt][b, cid] = self.x[b, rows].to(self.mdtype)
             if self.operand is not self.master:
                 self.operand[nxt][b, cid] = self.x[b, rows]
@@ -414,9 +416,16 @@ class HostStream:
     Stands in for the reference's file-backed ChunkStream (pipeline.py:150-234)
     with the same surface (batch, total_points, dims, precision, chunk_points,
     n_chunks, bounds, read_rows).  The array is pinned once so every chunk is a
-    true async DMA (cudaMemcpyAsync from page-locked memory)."""
+    true async DMA (cudaMemcpyAsync from page-locked memory).
 
-    def __init__(self, data, chunk_points: int, pin: bool = True):
+    A rank of a sharded run may hold only its own rows: ``row_offset`` and
+    ``total_points`` place ``data`` (B, n_local, d) at rows [row_offset,
+    row_offset + n_local) of a ``total_points``-row dataset.  Chunk indices and
+    bounds stay global (the chunk grid of the whole dataset); ``stream_shard``
+    gives the rows a rank streams."""
+
+    def __init__(self, data, chunk_points: int, pin: bool = True, row_offset: int = 0,
+                 total_points: int | None = None):
         if int(chunk_points) < 1:
             raise ValueError("chunk_points must be >= 1")
         t = data.data if isinstance(data, DataMatrix) else (
@@ -428,7 +437,12 @@ class HostStream:
         self.host = t.contiguous()
         if pin and not self.host.is_pinned():
             self.host = self.host.pin_memory()
-        self.batch, self.total_points, self.dims = self.host.shape
+        self.batch, n_local, self.dims = self.host.shape
+        self.row_offset = int(row_offset)
+        self.total_points = int(total_points) if total_points is not None else self.row_offset + n_local
+        if self.row_offset < 0 or self.row_offset + n_local > self.total_points:
+            raise ValueError("row_offset/total_points do not contain the local rows")
+        self.row_end = self.row_offset + n_local
         self.chunk_points = min(int(chunk_points), self.total_points)
         self.path = None
 
@@ -456,10 +470,16 @@ class HostStream:
         lo = t * self.chunk_points
         return lo, min(self.total_points, lo + self.chunk_points)
 
+    def has_rows(self, lo: int, hi: int) -> bool:
+        return self.row_offset <= lo and hi <= self.row_end
+
     def view(self, b: int, lo: int, hi: int) -> torch.Tensor:
         if not 0 <= b < self.batch or not 0 <= lo < hi <= self.total_points:
             raise ValueError("row range outside the stream bounds")
-        return self.host[b, lo:hi]
+        if not self.has_rows(lo, hi):
+            raise ValueError(f"rows [{lo}, {hi}) are not held by this shard "
+                             f"[{self.row_offset}, {self.row_end})")
+        return self.host[b, lo - self.row_offset:hi - self.row_offset]
 
     def read_rows(self, b: int, lo: int, hi: int) -> torch.Tensor:
         return self.view(b, lo, hi).clone()
@@ -472,6 +492,20 @@ class HostStream:
 
     def __exit__(self, *exc):
         self.close()
+
+
+def stream_shard(stream, world: int, rank: int) -> tuple[int, int, int, int]:
+    """(chunk_lo, chunk_hi, row_lo, row_hi) a rank streams in a sharded pass:
+    whole chunks of the global chunk grid, rank r taking chunks
+    [r*T//P, (r+1)*T//P).  Every chunk is then processed exactly as in the
+    single-process pass (same rows, same per-chunk update), so the pass
+    statistics and merge count summed over ranks equal the single-process
+    ones."""
+    T = stream.n_chunks
+    c_lo, c_hi = T * rank // world, T * (rank + 1) // world
+    if c_hi <= c_lo:
+        return c_lo, c_hi, 0, 0
+    return c_lo, c_hi, stream.bounds(c_lo)[0], stream.bounds(c_hi - 1)[1]
 
 
 class ChunkStream:
@@ -511,6 +545,9 @@ class ChunkStream:
             raise ValueError(f"chunk index {t} out of range")
         lo = t * self.chunk_points
         return lo, min(self.total_points, lo + self.chunk_points)
+
+    def has_rows(self, lo: int, hi: int) -> bool:
+        return True
 
     def _handle(self):
         if self._f is None:
@@ -587,10 +624,11 @@ class PartialStats:
 class DeviceAssignmentStore:
     """Device-resident stand-in for the reference's FKA1 AssignmentStore
     (fileio.py:189-247): holds this pass's and the previous pass's ids and
-    raises a device changed flag; starts from the 0xFFFFFFFF sentinel."""
+    raises a device changed flag; starts from the 0xFFFFFFFF sentinel.  A
+    sharded pass keeps only its rows [row_offset, row_offset + points)."""
 
-    def __init__(self, batch: int, points: int, device):
-        self.batch, self.points = batch, points
+    def __init__(self, batch: int, points: int, device, row_offset: int = 0):
+        self.batch, self.points, self.row_offset = batch, points, int(row_offset)
         self.ids = [torch.full((batch, points), -1, dtype=torch.int32, device=device) for _ in range(2)]
         self.cur = 0
         self.changed = torch.zeros((), dtype=torch.int32, device=device)
@@ -620,9 +658,9 @@ class DeviceAssignmentStore:
 class _StreamState:
     """Device buffers and streams for the chunk pipeline of one stream shape."""
 
-    def __init__(self, stream, clusters: int, device, keep_mind: bool = False):
+    def __init__(self, stream, clusters: int, device, rows_local: int, keep_mind: bool = False):
         self.dev = device
-        cp, d = stream.chunk_points, stream.dims
+        cp, d, B = stream.chunk_points, stream.dims, stream.batch
         self.buf = [torch.empty((1, cp, d), dtype=stream.dtype, device=device) for _ in range(2)]
         # file-backed sources: two pinned staging buffers filled by a reader thread
         self.staged = not isinstance(stream, HostStream)
@@ -630,153 +668,278 @@ class _StreamState:
             self.stage = [torch.empty((cp, d), dtype=stream.dtype, pin_memory=True) for _ in range(2)]
             self.copied = [torch.cuda.Event() for _ in range(2)]
             self.reader = ThreadPoolExecutor(max_workers=1)
-        # reseed_farthest needs every point's assigned distance of the pass
-        self.mind_all = (torch.empty((stream.batch, stream.total_points), dtype=torch.float32
-                                     if stream.dtype in LOW_PRECISION else stream.dtype, device=device)
-                         if keep_mind else None)
-        self.mind = torch.empty((1, cp), dtype=torch.float32 if stream.dtype in LOW_PRECISION
-                                else stream.dtype, device=device)
+        mdt = torch.float32 if stream.dtype in LOW_PRECISION else stream.dtype
+        # reseed_farthest needs every (local) point's assigned distance of the pass
+        self.mind_all = torch.empty((B, rows_local), dtype=mdt, device=device) if keep_mind else None
+        self.mind = torch.empty((1, cp), dtype=mdt, device=device)
         self.copy_stream = torch.cuda.Stream(device=device)
         self.ready = [torch.cuda.Event() for _ in range(2)]
         self.free = [torch.cuda.Event() for _ in range(2)]
-        B = stream.batch
-        self.sums = torch.zeros((B, clusters, d), dtype=torch.float64, device=device)
+        BK = B * clusters
+        # one packed f64 buffer [sums | counts | objective | changed | merges]: a
+        # sharded pass combines its ranks with ONE all-reduce of it
+        self.red = torch.zeros((BK * d + BK + B + 2,), dtype=torch.float64, device=device)
+        self.sums = self.red[:BK * d].view(B, clusters, d)
+        self.red_tail = self.red[BK * d:-1]
         self.counts = torch.zeros((B, clusters), dtype=torch.int64, device=device)
         self.obj = torch.zeros((B,), dtype=torch.float64, device=device)
-        self.obj_chunk = torch.empty((1,), dtype=torch.float64, device=device)
-        self.merges = torch.zeros((), dtype=torch.int64, device=device)
+        # per-chunk objectives, folded on the host in chunk order after the pass
+        # (pipeline.py:354: obj[b] += float(np.sum(m)) chunk by chunk), so a
+        # sharded pass adds them in the single-process order
+        self.obj_chunks = torch.zeros((B, stream.n_chunks), dtype=torch.float64, device=device)
+        self.obj_host = np.zeros((B,), np.float64)
+        self.merges = torch.zeros((), dtype=torch.int64, device=device)       # all passes
+        self.merges_pass = torch.zeros((), dtype=torch.int64, device=device)  # this pass
 
 
-def _streaming_pass(stream, master: torch.Tensor, operand: torch.Tensor, clusters: int,
-                    chunk: int, counters: Counters, store: DeviceAssignmentStore, st: _StreamState,
-                    new_master: torch.Tensor, new_operand: torch.Tensor | None,
-                    shift2: torch.Tensor, empty: torch.Tensor, allreduce=None):
-    """One pass (pipeline.py:312-373): per-chunk assign + update, then normalize.
+def _group_info(group):
+    if group is None:
+        return 1, 0
+    import torch.distributed as dist
 
-    With ``allreduce`` (multi-GPU, each rank streaming its own row shard) the
-    pass statistics, objective and changed flag are summed across ranks with
-    one packed float64 all-reduce before the (replicated) normalize."""
-    st.sums.zero_()
-    st.counts.zero_()
-    st.obj.zero_()
-    shift2.zero_()
-    store.begin_pass()
-    compute = torch.cuda.current_stream(st.dev)
-    tasks = [(b, t) for b in range(stream.batch) for t in range(stream.n_chunks)]
-    reads = {}
+    return dist.get_world_size(group), dist.get_rank(group)
 
-    def submit_read(i):  # reader thread: wait until staging buffer i&1 was copied out
-        b, t = tasks[i]
-        lo, hi = stream.bounds(t)
-        k = i & 1
-        ev = st.copied[k] if i >= 2 else None
 
-        def job():
-            if ev is not None:
-                ev.synchronize()
-            stream.read_rows_into(b, lo, hi, st.stage[k])
+def _rows_to_device(stream, b: int, idx, device, group=None, row_lo: int = 0,
+                    row_hi: int | None = None) -> torch.Tensor:
+    """Rows ``idx`` (global indices) of batch element b as a (len, d) device
+    tensor in the stream dtype.  In a sharded run each row comes from the rank
+    whose shard holds it, through one f64 all-reduce (exact for every dtype)."""
+    idx = [int(i) for i in idx]
+    if group is None:
+        rows = torch.stack([stream.read_rows(b, i, i + 1)[0] for i in idx]) if idx else \
+            torch.empty((0, stream.dims), dtype=stream.dtype)
+        return rows.to(device)
+    import torch.distributed as dist
 
-        reads[i] = st.reader.submit(job)
+    hi = stream.total_points if row_hi is None else row_hi
+    buf = torch.zeros((len(idx), stream.dims), dtype=torch.float64)
+    for j, i in enumerate(idx):
+        if row_lo <= i < hi:
+            buf[j] = stream.read_rows(b, i, i + 1)[0].double()
+    buf = buf.to(device)
+    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return buf.to(stream.dtype)
 
-    def issue_copy(i):
-        b, t = tasks[i]
-        lo, hi = stream.bounds(t)
-        k = i & 1
-        if st.staged:
-            reads.pop(i).result()
-            src = st.stage[k][: hi - lo]
-        else:
-            src = stream.view(b, lo, hi)
-        with torch.cuda.stream(st.copy_stream):
-            st.copy_stream.wait_event(st.free[k])
-            st.buf[k][0, : hi - lo].copy_(src, non_blocking=True)
-            st.ready[k].record(st.copy_stream)
+
+def _farthest(mind: torch.Tensor, take: int, offset: int, group=None):
+    """The ``take`` points farthest from their centroid, ordered by distance
+    descending then GLOBAL index ascending (reference _farthest_order,
+    pipeline.py:76-81).  ``mind`` holds rows [offset, offset + len).  Sharded:
+    each rank proposes its local top-``take``, the candidates are all-gathered
+    in rank order (= global index order, so a stable sort keeps the lowest
+    index first on ties) and every rank picks the same winners."""
+    dev = mind.device
+    md = mind.double()
+    n = md.numel()
+    k = min(take, n)
+    order = torch.sort(-md, stable=True).indices[:k]
+    cand_d = torch.full((take,), float("-inf"), dtype=torch.float64, device=dev)
+    cand_i = torch.full((take,), -1, dtype=torch.int64, device=dev)
+    cand_d[:k] = md[order]
+    cand_i[:k] = order + offset
+    if group is None:
+        return cand_i[:k].cpu().numpy()
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    all_d = torch.empty((world * take,), dtype=torch.float64, device=dev)
+    all_i = torch.empty((world * take,), dtype=torch.int64, device=dev)
+    dist.all_gather(list(all_d.view(world, take).unbind(0)), cand_d, group=group)
+    dist.all_gather(list(all_i.view(world, take).unbind(0)), cand_i, group=group)
+    win = torch.sort(-all_d, stable=True).indices[:take]
+    got = all_i[win].cpu().numpy()
+    return got[got >= 0]
+
+
+class _StreamRunner:
+    """One streamed Lloyd pass at a time over ``stream`` (pipeline.py:312-373).
+
+    With ``group`` (torch.distributed), rank r streams whole chunks
+    [r*T//P, (r+1)*T//P) of the global chunk grid (``stream_shard``), keeps
+    the ids of its rows device-resident, and the pass statistics, objective,
+    changed flag and merge count are summed across ranks with one packed f64
+    all-reduce before the replicated normalize."""
+
+    def __init__(self, stream, clusters: int, device, chunk: int, group=None,
+                 policy: str = "keep"):
+        self.group = group
+        self.world, self.rank = _group_info(group)
+        self.c_lo, self.c_hi, self.row_lo, self.row_hi = stream_shard(stream, self.world, self.rank)
+        self.stream = stream
+        self.policy = policy
+        self.K = clusters
+        self.chunk = chunk
+        self.dev = device
+        rows_local = self.row_hi - self.row_lo
+        self.st = _StreamState(stream, clusters, device, rows_local,
+                               keep_mind=policy == "reseed_farthest")
+        B, K, d = stream.batch, clusters, stream.dims
+        self.mdt = master_dtype(stream.dtype)
+        self.master = [torch.empty((B, K, d), dtype=self.mdt, device=device) for _ in range(2)]
+        self.lowp = stream.dtype in LOW_PRECISION
+        self.operand = ([torch.empty((B, K, d), dtype=stream.dtype, device=device) for _ in range(2)]
+                        if self.lowp else self.master)
+        self.shift2 = torch.zeros((), dtype=torch.float64, device=device)
+        self.empty = torch.empty((B, K), dtype=torch.uint8, device=device)
+        self.store = DeviceAssignmentStore(B, rows_local, device, row_offset=self.row_lo)
+        self.cur = 0
+
+    def set(self, c: torch.Tensor):
+        self.master[self.cur].copy_(to_device(c, self.dev).to(self.mdt))
+        if self.lowp:
+            self.operand[self.cur].copy_(self.master[self.cur].to(self.stream.dtype))
+
+    def one_pass(self, counters: Counters):
+        """Per-chunk assign + update with the H2D of chunk i+1 overlapping the
+        compute of chunk i, then (sharded: one all-reduce) normalize into the
+        other centroid slot.  Returns (changed, shift)."""
+        st, stream, store = self.st, self.stream, self.store
+        nxt = self.cur ^ 1
+        master, operand = self.master[self.cur], self.operand[self.cur]
+        st.sums.zero_()
+        st.counts.zero_()
+        st.obj.zero_()
+        st.obj_chunks.zero_()
+        st.merges_pass.zero_()
+        self.shift2.zero_()
+        store.begin_pass()
+        compute = torch.cuda.current_stream(st.dev)
+        tasks = [(b, t) for b in range(stream.batch) for t in range(self.c_lo, self.c_hi)]
+        reads = {}
+        r0 = self.row_lo
+
+        def submit_read(i):  # reader thread: wait until staging buffer i&1 was copied out
+            b, t = tasks[i]
+            lo, hi = stream.bounds(t)
+            k = i & 1
+            ev = st.copied[k] if i >= 2 else None
+
+            def job():
+                if ev is not None:
+                    ev.synchronize()
+                stream.read_rows_into(b, lo, hi, st.stage[k])
+
+            reads[i] = st.reader.submit(job)
+
+        def issue_copy(i):
+            b, t = tasks[i]
+            lo, hi = stream.bounds(t)
+            k = i & 1
             if st.staged:
-                st.copied[k].record(st.copy_stream)
-        if st.staged and i + 2 < len(tasks):
-            submit_read(i + 2)
+                reads.pop(i).result()
+                src = st.stage[k][: hi - lo]
+            else:
+                src = stream.view(b, lo, hi)
+            with torch.cuda.stream(st.copy_stream):
+                st.copy_stream.wait_event(st.free[k])
+                st.buf[k][0, : hi - lo].copy_(src, non_blocking=True)
+                st.ready[k].record(st.copy_stream)
+                if st.staged:
+                    st.copied[k].record(st.copy_stream)
+            if st.staged and i + 2 < len(tasks):
+                submit_read(i + 2)
 
-    for k in range(2):  # both buffers start free
-        st.free[k].record(compute)
-    if st.staged:
-        for i in range(min(2, len(tasks))):
-            submit_read(i)
-    if tasks:
-        issue_copy(0)
-    for i, (b, t) in enumerate(tasks):
-        lo, hi = stream.bounds(t)
-        rows = hi - lo
-        k = i & 1
-        compute.wait_event(st.ready[k])
-        xb = st.buf[k][:, :rows]
-        ids_new = store.new[b: b + 1, lo:hi]   # contiguous: one row segment of (B, N)
-        ids_old = store.old[b: b + 1, lo:hi]
-        mind = st.mind[:, :rows] if st.mind_all is None else st.mind_all[b: b + 1, lo:hi]
-        ops.assign(xb, operand[b: b + 1], idx_prev=ids_old, changed=store.changed,
-                   idx_out=ids_new, mind_out=mind)
-        ops.objective(mind, out=st.obj_chunk)
-        st.obj[b: b + 1] += st.obj_chunk
-        ops.update(xb, ids_new, clusters, chunk, accumulate=True, sums=st.sums[b: b + 1],
-                   counts=st.counts[b: b + 1], merges=st.merges)
-        st.free[k].record(compute)
-        counters.elements_streamed += rows
-        if i + 1 < len(tasks):  # host may block on the file read while chunk i computes
-            issue_copy(i + 1)
-    if allreduce is not None:
-        red = torch.cat([st.sums.reshape(-1), st.counts.reshape(-1).double(), st.obj,
-                         store.changed.reshape(1).double()])
-        allreduce(red)
-        n1, n2 = st.sums.numel(), st.counts.numel()
-        st.sums.copy_(red[:n1].view_as(st.sums))
-        st.counts.copy_(red[n1:n1 + n2].view_as(st.counts).to(torch.int64))
-        st.obj.copy_(red[n1 + n2:n1 + n2 + st.obj.numel()])
-        store.changed.copy_((red[-1] > 0).to(torch.int32))
-    ops.normalize(st.sums, st.counts, master, out=new_master, operand_out=new_operand, empty=empty,
-                  shift2=shift2)
-    if st.mind_all is not None:
-        _reseed_from_stream(stream, st, master, new_master, new_operand, empty, shift2)
+        for k in range(2):  # both buffers start free
+            st.free[k].record(compute)
+        if st.staged:
+            for i in range(min(2, len(tasks))):
+                submit_read(i)
+        if tasks:
+            issue_copy(0)
+        streamed = 0
+        for i, (b, t) in enumerate(tasks):
+            lo, hi = stream.bounds(t)
+            rows = hi - lo
+            k = i & 1
+            compute.wait_event(st.ready[k])
+            xb = st.buf[k][:, :rows]
+            ids_new = store.new[b: b + 1, lo - r0:hi - r0]   # contiguous: one row segment of (B, n)
+            ids_old = store.old[b: b + 1, lo - r0:hi - r0]
+            mind = st.mind[:, :rows] if st.mind_all is None else st.mind_all[b: b + 1, lo - r0:hi - r0]
+            ops.assign(xb, operand[b: b + 1], idx_prev=ids_old, changed=store.changed,
+                       idx_out=ids_new, mind_out=mind)
+            ops.objective(mind, out=st.obj_chunks[b, t:t + 1])
+            ops.update(xb, ids_new, self.K, self.chunk, accumulate=True, sums=st.sums[b: b + 1],
+                       counts=st.counts[b: b + 1], merges=st.merges_pass)
+            st.free[k].record(compute)
+            streamed += rows
+            if i + 1 < len(tasks):  # host may block on the file read while chunk i computes
+                issue_copy(i + 1)
+        if self.group is not None:
+            import torch.distributed as dist
+
+            ops.stats_pack(st.counts, st.obj, store.changed, st.red_tail)
+            st.red[-1:].copy_(st.merges_pass)
+            dist.all_reduce(st.red, op=dist.ReduceOp.SUM, group=self.group)
+            ops.stats_pack(st.counts, st.obj, store.changed, st.red_tail, unpack=True)
+            st.merges_pass.copy_(st.red[-1])
+            # each chunk's objective has exactly one contributor: the sum is a gather
+            dist.all_reduce(st.obj_chunks, op=dist.ReduceOp.SUM, group=self.group)
+            streamed = stream.batch * stream.total_points  # every rank reports the whole pass
+        counters.elements_streamed += streamed
+        st.merges += st.merges_pass
+        ops.normalize(st.sums, st.counts, master, out=self.master[nxt],
+                      operand_out=self.operand[nxt] if self.lowp else None, empty=self.empty,
+                      shift2=self.shift2)
+        if st.mind_all is not None:
+            self._reseed(master, self.master[nxt], self.operand[nxt] if self.lowp else None)
+        v = torch.stack([store.changed.to(torch.float64), self.shift2]).cpu()
+        chunk_obj = st.obj_chunks.cpu().numpy()
+        for b in range(stream.batch):  # chunk order, one rounding per chunk (as the reference)
+            acc = 0.0
+            for val in chunk_obj[b]:
+                acc += float(val)
+            st.obj_host[b] = acc
+        return bool(v[0] != 0), math.sqrt(float(v[1]))
+
+    def _reseed(self, master, new_master, new_operand):
+        """reseed_farthest for a streamed pass (pipeline.py:283-309, 366-371): each
+        empty cluster, in id order, takes the next-farthest point of the pass
+        (distance desc, index asc), read back from the source; the shift is
+        recomputed."""
+        em = self.empty.cpu().numpy()
+        if not em.any():
+            return
+        for b in range(self.stream.batch):
+            empties = np.flatnonzero(em[b])
+            if empties.size == 0:
+                continue
+            idx = _farthest(self.st.mind_all[b], int(empties.size), self.row_lo, self.group)
+            rows = _rows_to_device(self.stream, b, idx, self.dev, self.group, self.row_lo, self.row_hi)
+            cid = torch.from_numpy(empties[: len(idx)]).to(self.dev)
+            new_master[b, cid] = rows.to(new_master.dtype)
+            if new_operand is not None:
+                new_operand[b, cid] = rows
+        diff = new_master.double() - master.double()
+        self.shift2.copy_((diff * diff).sum(-1).max())
 
 
-def _reseed_from_stream(stream, st: _StreamState, master, new_master, new_operand, empty, shift2):
-    """reseed_farthest for a streamed pass (pipeline.py:283-309, 366-371): each
-    empty cluster takes the next-farthest point of the pass (distance desc,
-    index asc), read back from the source; the shift is recomputed."""
-    em = empty.cpu().numpy()
-    if not em.any():
-        return
-    for b in range(stream.batch):
-        empties = np.flatnonzero(em[b])
-        if empties.size == 0:
-            continue
-        order = torch.sort(-st.mind_all[b].double(), stable=True).indices[: empties.size].cpu()
-        rows = torch.stack([stream.read_rows(b, int(r), int(r) + 1)[0] for r in order])
-        cid = torch.from_numpy(empties).to(st.dev)
-        rows = rows.to(st.dev)
-        new_master[b, cid] = rows.to(new_master.dtype)
-        if new_operand is not None:
-            new_operand[b, cid] = rows
-    diff = new_master.double() - master.double()
-    shift2.copy_((diff * diff).sum(-1).max())
-
-
-def _init_from_stream(stream, clusters: int, seed: int, method: str, device=None) -> torch.Tensor:
+def _init_from_stream(stream, clusters: int, seed: int, method: str, device=None, group=None,
+                      runner: _StreamRunner | None = None) -> torch.Tensor:
     """Same row draws as the in-core initializer (pipeline.py:456-479); a
     file-backed source reads only the chosen rows (plus, for k-means++, the
-    D^2 sweeps of pipeline.py:420-453, streamed through the device)."""
+    D^2 sweeps of pipeline.py:420-453, streamed through the device).  Sharded:
+    every rank draws the same indices; each row comes from its owner."""
     if method not in INIT_METHODS:
         raise ValueError(f"init method must be one of {INIT_METHODS}")
     if clusters > stream.total_points:
         raise ValueError(f"cannot place {clusters} clusters with only {stream.total_points} points")
-    out = torch.empty((stream.batch, clusters, stream.dims), dtype=stream.dtype)
+    if device is not None:
+        dev = device
+    elif method == "random_distinct" and group is None:
+        dev = torch.device("cpu")  # rows only: stay on the host
+    else:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    r_lo, r_hi = (runner.row_lo, runner.row_hi) if runner is not None else (0, stream.total_points)
+    out = torch.empty((stream.batch, clusters, stream.dims), dtype=stream.dtype, device=dev)
     for b in range(stream.batch):
         rng = np.random.default_rng((seed, b))
         if method == "random_distinct":
             idx = rng.choice(stream.total_points, size=clusters, replace=False)
         else:
-            dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-            idx = _streaming_kmeanspp(stream, b, clusters, rng, dev)
-        for j, i in enumerate(idx):
-            out[b, j] = stream.read_rows(b, int(i), int(i) + 1)[0]
+            idx = _streaming_kmeanspp(stream, b, clusters, rng, dev, group, runner)
+        out[b] = _rows_to_device(stream, b, idx, dev, group, r_lo, r_hi)
     return out
 
 
@@ -786,13 +949,15 @@ def _stream_rows_host(stream, b: int, lo: int, hi: int, buf: torch.Tensor | None
     return stream.read_rows_into(b, lo, hi, buf)
 
 
-def _streaming_kmeanspp(stream, b: int, k: int, rng: np.random.Generator, device) -> np.ndarray:
+def _streaming_kmeanspp(stream, b: int, k: int, rng: np.random.Generator, device, group=None,
+                        runner: _StreamRunner | None = None) -> np.ndarray:
     """k-means++ over a chunk stream (pipeline.py:420-453): the (N,) f64 weight
     table is device-resident, every chunk is swept by fk_kmeanspp_sweep as it
     arrives and each choice() draw is resolved by fk_kmeanspp_select -- the
     same arithmetic as the in-core seeding, so the chosen rows match it (and
     the reference) index for index.  One host read per draw fetches the
-    chosen index (its row is the next sweep's center)."""
+    chosen index (its row is the next sweep's center).  Sharded: each rank
+    sweeps its own chunks and the table slices are all-gathered per draw."""
     from . import ops
 
     n = stream.total_points
@@ -800,17 +965,35 @@ def _streaming_kmeanspp(stream, b: int, k: int, rng: np.random.Generator, device
     idx[0] = rng.integers(n)
     if k == 1:
         return idx
+    world, rank = _group_info(group)
+    if runner is not None:
+        c_lo, c_hi, r_lo, r_hi = runner.c_lo, runner.c_hi, runner.row_lo, runner.row_hi
+    else:
+        c_lo, c_hi, r_lo, r_hi = 0, stream.n_chunks, 0, n
     pp = ops.KmeansppStream(n, k, device)
     buf = None
     if not isinstance(stream, HostStream):
         buf = torch.empty((stream.chunk_points, stream.dims), dtype=stream.dtype).pin_memory()
+    if group is not None:
+        import torch.distributed as dist
+
+        shards = [stream_shard(stream, world, r)[2:] for r in range(world)]
+        maxn = max(max(h - l for l, h in shards), 1)
+        send = torch.zeros((maxn,), dtype=torch.float64, device=device)
+        recv = torch.empty((world * maxn,), dtype=torch.float64, device=device)
 
     def sweep(row: int, first: bool, j: int) -> None:
-        center = stream.read_rows(b, row, row + 1)[0].to(device)
-        for t in range(stream.n_chunks):
+        center = _rows_to_device(stream, b, [row], device, group, r_lo, r_hi)[0]
+        for t in range(c_lo, c_hi):
             lo, hi = stream.bounds(t)
             rows = _stream_rows_host(stream, b, lo, hi, buf).to(device, non_blocking=buf is None)
             pp.sweep(rows, lo, center, first, j)
+        if group is not None:
+            send[: r_hi - r_lo].copy_(pp.m[0, r_lo:r_hi])
+            dist.all_gather(list(recv.view(world, maxn).unbind(0)), send, group=group)
+            for r, (l, h) in enumerate(shards):
+                if h > l and r != rank:
+                    pp.m[0, l:h].copy_(recv[r * maxn:r * maxn + (h - l)])
 
     sweep(int(idx[0]), True, 1)
     for j in range(1, k):
@@ -828,76 +1011,71 @@ def _streaming_kmeanspp(stream, b: int, k: int, rng: np.random.Generator, device
     return idx
 
 
-class _StreamRunner:
-    def __init__(self, stream, clusters: int, device, chunk: int, allreduce=None,
-                 policy: str = "keep"):
-        if policy == "reseed_farthest" and allreduce is not None:
-            raise NotImplementedError("reseed_farthest with sharded streaming needs a global top-k")
-        self.allreduce = allreduce
-        self.stream = stream
-        self.K = clusters
-        self.chunk = chunk
-        self.dev = device
-        self.st = _StreamState(stream, clusters, device, keep_mind=policy == "reseed_farthest")
-        B, K, d = stream.batch, clusters, stream.dims
-        self.mdt = master_dtype(stream.dtype)
-        self.master = [torch.empty((B, K, d), dtype=self.mdt, device=device) for _ in range(2)]
-        self.lowp = stream.dtype in LOW_PRECISION
-        self.operand = ([torch.empty((B, K, d), dtype=stream.dtype, device=device) for _ in range(2)]
-                        if self.lowp else self.master)
-        self.shift2 = torch.zeros((), dtype=torch.float64, device=device)
-        self.empty = torch.empty((B, K), dtype=torch.uint8, device=device)
-        self.store = DeviceAssignmentStore(B, stream.total_points, device)
-        self.cur = 0
-
-    def set(self, c: torch.Tensor):
-        self.master[self.cur].copy_(to_device(c, self.dev).to(self.mdt))
-        if self.lowp:
-            self.operand[self.cur].copy_(self.master[self.cur].to(self.stream.dtype))
-
-    def one_pass(self, counters: Counters):
-        nxt = self.cur ^ 1
-        _streaming_pass(self.stream, self.master[self.cur], self.operand[self.cur], self.K,
-                        self.chunk, counters, self.store, self.st, self.master[nxt],
-                        self.operand[nxt] if self.lowp else None, self.shift2, self.empty,
-                        self.allreduce)
-        v = torch.stack([self.store.changed.to(torch.float64), self.shift2]).cpu()
-        return bool(v[0] != 0), math.sqrt(float(v[1]))
-
-
 def _check_stream_centroids(stream, c: Centroids, clusters: int) -> None:
     if c.batch != stream.batch or c.dims != stream.dims:
         raise ValueError("centroids do not match the stream shape")
     if c.clusters != clusters:
         raise ValueError("centroid count does not match the configuration")
-    if c.precision != stream.precision:
+    # the stream's precision, or (bf16/fp16 data) its f32 master -- what the pass returns
+    if c.precision != stream.precision and c.dtype != master_dtype(stream.dtype):
         raise ValueError("centroid precision does not match the stream")
 
 
+def _stream_device(device):
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        dev = torch.device("cuda", torch.cuda.current_device())
+    elif dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def _cached_runner(stream, clusters: int, dev, chunk: int, policy: str, group) -> _StreamRunner:
+    """Per-stream cache of the pass machinery (device buffers, copy stream,
+    events), so repeated out_of_core_iteration calls allocate nothing."""
+    cache = stream.__dict__.setdefault("_fk_runners", {})
+    key = (clusters, str(dev), chunk, policy, id(group))
+    run = cache.get(key)
+    if run is None:
+        run = _StreamRunner(stream, clusters, dev, chunk, group=group, policy=policy)
+        cache[key] = run
+    return run
+
+
 def out_of_core_iteration(stream, c: Centroids, cfg: KMeansConfig, counters: Counters,
-                          store=None, workers: int | None = None, device=None):
+                          store=None, workers: int | None = None, device=None, group=None):
     """One streaming Lloyd iteration (pipeline.py:385-417): returns (new
     centroids, assignment store, counters); the caller finalizes (or aborts)
     the store.  For an FKM1 ``ChunkStream`` a fresh store is the FKA1
     ``AssignmentStore`` at "<dataset>.fka1" (as in the reference); a
-    host-array stream keeps its ids in a ``DeviceAssignmentStore``."""
+    host-array stream keeps its ids in a ``DeviceAssignmentStore``.
+
+    ``group`` (a torch.distributed process group, e.g. ``dist.group.WORLD``)
+    shards the pass: each rank streams its whole chunks (``stream_shard``)
+    and the statistics are all-reduced once; the returned centroids are
+    replicated and equal the single-process pass (bitwise for f32 data).  The
+    store then holds this rank's rows only (device-resident)."""
     from .fileio import AssignmentStore
 
     _check_stream_centroids(stream, c, cfg.clusters)
-    dev = device or device_of(c.data)
-    if dev.type != "cuda":
-        dev = torch.device("cuda", torch.cuda.current_device())
+    dev = _stream_device(device or device_of(c.data))
     tiling = _resolve_tiling(cfg, stream.total_points, stream.dims, stream.batch, stream.elem_bytes,
                              _workers(workers))
     own_store = store is None
-    if store is None and getattr(stream, "path", None):
+    if store is None and group is None and getattr(stream, "path", None):
         store = AssignmentStore(stream.path + ".fka1", stream.batch, stream.total_points)
     try:
-        run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk,
-                            policy=cfg.empty_cluster_policy)
+        run = _cached_runner(stream, cfg.clusters, dev, tiling.update_chunk, cfg.empty_cluster_policy,
+                             group)
         if isinstance(store, DeviceAssignmentStore):
+            if store.points != run.row_hi - run.row_lo or store.row_offset != run.row_lo:
+                raise ValueError("assignment store does not cover this rank's rows")
             run.store = store
+        elif store is None:  # a fresh pass: sentinel ids, so every point counts as changed
+            run.store = DeviceAssignmentStore(stream.batch, run.row_hi - run.row_lo, dev, run.row_lo)
+        run.cur = 0
         run.set(c.data)
+        merges0 = int(run.st.merges.item())
         run.one_pass(counters)
         if isinstance(store, AssignmentStore):
             ids = run.store.new.cpu()
@@ -907,36 +1085,42 @@ def out_of_core_iteration(stream, c: Centroids, cfg: KMeansConfig, counters: Cou
         if own_store and isinstance(store, AssignmentStore):
             store.abort()
         raise
-    counters.synchronized_merges += int(run.st.merges.item())
-    return (Centroids(run.master[run.cur ^ 1].clone(), check_finite=False),
+    counters.synchronized_merges += int(run.st.merges.item()) - merges0
+    return (Centroids(run.master[1].clone(), check_finite=False),
             store if store is not None else run.store, counters)
 
 
 def chunked_stream_run(stream, cfg: KMeansConfig, assign_path: str | None = None,
                        workers: int | None = None, counters: Counters | None = None,
-                       device=None) -> KMeansResult:
+                       device=None, group=None) -> KMeansResult:
     """Full out-of-core run (pipeline.py:482-530) with the in-core run's decisions.
 
     The final assignments are written as an FKA1 file (atomically) to
     ``assign_path``, default "<dataset>.fka1" for an FKM1 stream; a host-array
-    stream without ``assign_path`` keeps them in memory only."""
+    stream without ``assign_path`` keeps them in memory only.
+
+    ``group`` shards every pass across ranks (see ``out_of_core_iteration``):
+    centroids, objective history, iteration count and counters are the
+    replicated single-process values; ``assignments`` holds this rank's rows
+    [row_lo, row_hi) of ``stream_shard``, and the FKA1 output is one file per
+    rank, "<path>.<rank>-of-<world>"."""
     from .fileio import write_fka1
 
     counters = counters if counters is not None else Counters()
     if cfg.clusters > stream.total_points:
         raise ValueError("more clusters than points in the stream")
-    dev = device or torch.device("cuda", torch.cuda.current_device())
+    dev = _stream_device(device)
     tiling = _resolve_tiling(cfg, stream.total_points, stream.dims, stream.batch, stream.elem_bytes,
                              _workers(workers))
-    run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk,
+    run = _StreamRunner(stream, cfg.clusters, dev, tiling.update_chunk, group=group,
                         policy=cfg.empty_cluster_policy)
-    run.set(_init_from_stream(stream, cfg.clusters, cfg.seed, cfg.init, run.dev))
+    run.set(_init_from_stream(stream, cfg.clusters, cfg.seed, cfg.init, run.dev, group, run))
     history = []
     iterations = 0
     for it in range(1, cfg.max_iters + 1):
         iterations = it
         changed, shift = run.one_pass(counters)
-        history.append(run.st.obj.cpu().numpy().copy())
+        history.append(run.st.obj_host.copy())
         if not changed:
             break
         run.cur ^= 1
@@ -946,6 +1130,8 @@ def chunked_stream_run(stream, cfg: KMeansConfig, assign_path: str | None = None
     a = run.store.read_all()
     path = assign_path or (stream.path + ".fka1" if getattr(stream, "path", None) else None)
     if path:
+        if group is not None:
+            path = f"{path}.{run.rank}-of-{run.world}"
         write_fka1(path, a)
     return KMeansResult(Centroids(run.master[run.cur].clone(), check_finite=False), a,
                         np.array(history), iterations, counters)

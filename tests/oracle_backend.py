@@ -75,3 +75,18 @@ class KmeansppStream:
             self.idx[0, j] = O.choice_cdf(m, total, u)
         else:
             self.halted[0] = j
+
+
+def merges_from_counts(counts, chunk, out, accumulate=False):
+    """Restatement of k_merges_counts (sort_inverse.py:159-165 on global counts)."""
+    c = counts.numpy().astype(np.int64)
+    total = 0
+    for row in c:
+        s = np.concatenate([[0], np.cumsum(row)[:-1]])
+        e = s + row
+        nz = row > 0
+        total += int(((e[nz] - 1) // chunk - s[nz] // chunk + 1).sum())
+    if accumulate:
+        out += total
+    else:
+        out.fill_(total)

@@ -176,7 +176,7 @@ def test_stream_init_matches_in_core(tmp_path, method):
         c_stream = _init_from_stream(s, 7, 11, method)
     idx = init_indices(300, 7, 11, 2, method, x.data.cuda() if method == "kmeanspp" else x.data)
     c_core = torch.stack([x.data[b][torch.from_numpy(idx[b])] for b in range(2)])
-    assert torch.equal(c_stream, c_core)
+    assert torch.equal(c_stream.cpu(), c_core)
 
 
 def test_reference_reads_our_bf16_rejecting_codes(tmp_path, reference):

@@ -129,3 +129,27 @@ def test_wide_rows_integer_grid_bitwise(ops, oracle, d, dtype):
     x = torch.randint(-4, 5, (2, 777, d), generator=g).to(dtype)
     c = torch.randint(-4, 5, (2, 300, d), generator=g).to(dtype)
     check_assign(ops, oracle, x, c, exact=True)
+
+
+def test_config5_shape_fp16_k65536(ops, oracle):
+    """BASELINE config 5's precision and shape per chunk (fp16, K=65536, d=128) at
+    a reduced N: assign under the near-tie rule, then the update of the GPU's
+    own ids -- bit-exact counts and merge count, sums within fp32-accumulation
+    bounds -- through the large-K (global histogram) update path."""
+    g = torch.Generator().manual_seed(5)
+    K, N, d = 65536, 8192, 128
+    centers = torch.rand((1, 4096, d), generator=g) * 20 - 10
+    lab = torch.randint(0, 4096, (1, N), generator=g)
+    x = (torch.gather(centers, 1, lab[..., None].expand(1, N, d)) + torch.randn((1, N, d), generator=g))
+    x = x.to(torch.float16).contiguous()
+    lab_c = torch.randint(0, 4096, (1, K), generator=g)
+    c = (torch.gather(centers, 1, lab_c[..., None].expand(1, K, d))
+         + torch.randn((1, K, d), generator=g)).to(torch.float16).contiguous()
+    check_assign(ops, oracle, x, c, exact=False)
+    ids, _ = ops.assign(x.cuda(), c.cuda())
+    merges = torch.zeros((), dtype=torch.int64, device="cuda")
+    sums, counts = ops.update(x.cuda(), ids, K, 1000, merges=merges)
+    s_ref, c_ref, m_ref = oracle.sort_inverse_update(x.float().numpy(), ids.cpu().numpy(), K, 1000)
+    assert np.array_equal(counts.cpu().numpy(), c_ref)
+    assert int(merges.item()) == m_ref
+    np.testing.assert_allclose(sums.cpu().numpy(), s_ref, rtol=1e-6, atol=1e-4)

@@ -81,7 +81,7 @@ def test_streamed_kmeanspp_matches_in_core(kpp_golden, tmp_path):
             c = _init_from_stream(s, spec["k"], spec["seed"], "kmeanspp", torch.device("cuda", 0))
         gold = kpp_golden[name]
         ref = torch.stack([x[b][torch.from_numpy(gold[b])] for b in range(x.shape[0])])
-        assert torch.equal(c, ref)
+        assert torch.equal(c.cpu(), ref)
     # file-backed stream (FKM1), f32
     spec = CASES["duplicates_f32"]
     x = fk.DataMatrix(torch.from_numpy(make_case(spec)))
@@ -91,7 +91,7 @@ def test_streamed_kmeanspp_matches_in_core(kpp_golden, tmp_path):
         c = _init_from_stream(s, spec["k"], spec["seed"], "kmeanspp", torch.device("cuda", 0))
     gold = kpp_golden["duplicates_f32"]
     ref = torch.stack([x.data[b][torch.from_numpy(gold[b])] for b in range(2)])
-    assert torch.equal(c, ref)
+    assert torch.equal(c.cpu(), ref)
 
 
 def test_lloyd_run_with_kmeanspp_init(kpp_golden):
