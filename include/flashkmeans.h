@@ -98,9 +98,12 @@ FK_API fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B,
                     int32_t* changed_flag, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- update
- * Per-cluster sums (f64) and counts (int64) from (X, ids) by a device
+ * Per-cluster sums (f64) and counts (int64) from (X, ids) by a device stable
  * counting sort of ids followed by warp-level segmented reductions over the
- * sorted order (X is never permuted).  `accumulate`=0 overwrites sums/counts,
+ * sorted order (X is never permuted).  Deterministic: every addition order is
+ * fixed by (ids, shape, SM count), so repeated calls return the same bits; ids
+ * outside [0, K) are skipped (the Python layer rejects them beforehand, as
+ * the reference does).  `accumulate`=0 overwrites sums/counts,
  * 1 adds into them (chunked streaming, PartialStats.combine pipeline.py:250).
  * `update_chunk` is the reference's chunk (TilingConfig.update_chunk); it
  * only defines *merges_out (device int64, incremented by the segment count the
@@ -110,6 +113,17 @@ FK_API fk_status fk_update(fk_dtype dt, const void* X, const int32_t* ids, int64
                     int64_t K, int64_t d, int64_t update_chunk, int32_t accumulate, double* sums,
                     int64_t* counts, int64_t* merges_out, void* workspace, size_t workspace_bytes,
                     void* stream);
+
+/* Stable argsort of the ids alone (argsort_assignments / counting_sort,
+ * sort_inverse.py:67-78, _kernels.py:118-132): the order the update's segmented
+ * reductions walk.  order_out (B*N int32): flat point indices b*N + i, grouped
+ * by key b*K + id, ascending point index inside a key (np.argsort
+ * kind="stable"); ids outside [0, K) are left out, so only the first
+ * offsets_out[B*K] entries are written.  offsets_out (B*K+1 int64): start of
+ * each key's run.  Workspace: fk_update_workspace(dt, B, N, K, 1).            */
+FK_API fk_status fk_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, int32_t* order_out,
+                            int64_t* offsets_out, void* workspace, size_t workspace_bytes,
+                            void* stream);
 
 /* ------------------------------------------------------------- normalize
  * c = fl_T(sums / counts) per cluster; clusters with count 0 keep `prev`

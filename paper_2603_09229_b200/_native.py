@@ -42,6 +42,8 @@ def _declare(L):
     L.fk_update_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
     L.fk_update.restype = ctypes.c_int
     L.fk_update.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, I64, I32, P, P, P, P, SZ, P]
+    L.fk_argsort.restype = ctypes.c_int
+    L.fk_argsort.argtypes = [P, I64, I64, I64, P, P, P, SZ, P]
     L.fk_normalize.restype = ctypes.c_int
     L.fk_normalize.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, P, P, P, I64, I64, I64, P]
     L.fk_row_norms.restype = ctypes.c_int
@@ -71,7 +73,7 @@ def _declare(L):
 
 EXPORTED = (
     "fk_version", "fk_status_string", "fk_last_cuda_error", "fk_device_supported",
-    "fk_assign_workspace", "fk_assign", "fk_update_workspace", "fk_update", "fk_normalize",
+    "fk_assign_workspace", "fk_assign", "fk_update_workspace", "fk_update", "fk_argsort", "fk_normalize",
     "fk_row_norms", "fk_objective_workspace", "fk_objective", "fk_scatter",
     "fk_stats_pack", "fk_merges_from_counts", "fk_kmeanspp_workspace", "fk_kmeanspp",
     "fk_kmeanspp_init", "fk_kmeanspp_sweep", "fk_kmeanspp_select",

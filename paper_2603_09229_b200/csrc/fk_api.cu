@@ -148,9 +148,8 @@ fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B, int64_
 
 // ------------------------------------------------------------------ update
 size_t fk_update_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d) {
-  (void)d;
-  if (!valid_dt(dt) || B < 1 || N < 1 || K < 1) return 0;
-  return fk::update_workspace_bytes(B, N, K);
+  if (!valid_dt(dt) || B < 1 || N < 1 || K < 1 || d < 1) return 0;
+  return fk::update_workspace_bytes(B, N, K, d);
 }
 
 fk_status fk_update(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
@@ -165,6 +164,15 @@ fk_status fk_update(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, i
   return cuda_status(fk::launch_update(dt, X, ids, B, N, K, d, update_chunk, accumulate, sums,
                                        counts, merges_out, ws, dev_info().sms,
                                        reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, int32_t* order_out,
+                     int64_t* offsets_out, void* ws, size_t ws_bytes, void* stream) {
+  if (!shape_ok(B, N, K, 1) || !ids || !order_out || !offsets_out) return FK_EINVAL;
+  if (!ws || ws_bytes < fk_update_workspace(FK_F32, B, N, K, 1)) return FK_EWORKSPACE;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_argsort(ids, B, N, K, order_out, offsets_out, ws, dev_info().sms,
+                                        reinterpret_cast<cudaStream_t>(stream)));
 }
 
 // ------------------------------------------------------------------ normalize

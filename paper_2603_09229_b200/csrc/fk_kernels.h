@@ -37,11 +37,13 @@ cudaError_t launch_assign_cuda_core_lowp(int dt, const void* X, const void* C, c
                                          cudaStream_t stream);
 
 // fk_update.cu
-size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K);
+size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d);
 cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
                           int64_t K, int64_t d, int64_t chunk, int accumulate, double* sums,
                           int64_t* counts, int64_t* merges, void* ws, int num_sms,
                           cudaStream_t stream);
+cudaError_t launch_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, int32_t* order_out,
+                           int64_t* off_out, void* ws, int num_sms, cudaStream_t stream);
 cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* counts,
                              const void* prev, void* out, int operand_dt, void* operand_out,
                              uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,

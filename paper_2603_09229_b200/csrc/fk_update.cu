@@ -2,31 +2,36 @@
 //
 // Replaces sort_inverse_update (reference sort_inverse.py:106-149, kernels
 // counting_sort / segment_stats / merge_segments _kernels.py:118-171) with a
-// contention-free GPU scheme: no per-point scatter into shared accumulators.
+// contention-free GPU scheme: no per-point scatter into shared accumulators,
+// and a result that is bitwise reproducible run to run.
 //
-//   k_hist     histogram of composite keys (b*K + id), smem-privatized when
-//              B*K fits in shared memory                      -> counts (exact)
-//   k_scan     one-block exclusive scan -> segment offsets, insertion cursors,
-//              int64 counts and the reference's synchronized_merges count
-//   k_scatter  bucket point indices by key (warp-aggregated cursor bumps);
-//              X itself is never permuted (sort_inverse.py:12-13)
-//   k_segsum   equal slices of the sorted order per warp; each warp streams the
-//              gathered rows with 16-byte vector loads, keeps per-lane running
-//              sums, and emits ONE merge per segment: segments owned by the
-//              slice are written directly, the <= 2 boundary segments per
-//              slice are merged with an f64 reduction.
+//   k_hist       per-block histograms of the cluster ids over contiguous point
+//                ranges (shared-memory bins; global rows for very large K)
+//   k_colscan    per key: exclusive prefix of the block histograms in block
+//                order (each block's base inside the key's run) and the totals
+//   k_scan       per batch element: key offsets, int64 counts and the
+//                reference's synchronized_merges count
+//   k_scatter    each block STABLY sorts its range by id in shared memory
+//                (LSD radix passes of <= 8 bits; per-warp digit counters and
+//                match.any ranks, no atomics) and writes the point indices at
+//                off[key] + block base + rank: the global order is the
+//                reference's stable argsort (_kernels.py:118-132); X itself is
+//                never permuted (sort_inverse.py:12-13)
+//   k_segsum     equal slices of the sorted order per warp; 16-byte row
+//                gathers, per-lane running sums, ONE merge per segment: owned
+//                segments are stored directly, segments spanning slices leave
+//                a partial per slice and the last slice to arrive adds them in
+//                slice order (the reference merges in ascending order,
+//                _kernels.py:163-171, sort_inverse.py:159-165)
 //
 // sums are f64 and counts int64, the reference's ClusterStats dtypes
 // (core.py:203-233).  bf16/fp16 rows accumulate in fp32 inside a slice; f32
-// and f64 rows accumulate in f64 so fp32 data reproduces the reference's
-// sums exactly.
-#include <cooperative_groups.h>
+// and f64 rows accumulate in f64.  Every summation order is a fixed function
+// of (ids, shape, SM count), so two runs give the same bits.
 #include <stdlib.h>
 
 #include "fk_common.cuh"
 #include "fk_kernels.h"
-
-namespace cg = cooperative_groups;
 
 namespace fk {
 
@@ -37,13 +42,10 @@ FK_DEV double as_f64(double v) { return v; }
 FK_DEV double as_f64(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
 FK_DEV double as_f64(__half v) { return (double)__half2float(v); }
 
-// ----------------------------------------------------------------- hist
-// Each block owns a contiguous range of one batch element's points.  With
-// K <= HIST_SMEM_KEYS the block histograms in shared memory and publishes one
-// atomic per non-empty bin; otherwise identical keys are warp-aggregated.
+// ----------------------------------------------------------------- ranges
 // Blocks are laid out per batch element (gridDim.x = B * bpb): block j of
-// element b owns a contiguous slice of that element's points, so a shared
-// histogram needs only K bins, whatever B is.
+// element b owns a contiguous slice of that element's points, so a block
+// histogram needs only K bins, whatever B is.  lo/hi are flat (b*N + i).
 __device__ __forceinline__ void range_of(int64_t N, int bpb, int64_t& b, int64_t& lo,
                                          int64_t& hi) {
   b = blockIdx.x / bpb;
@@ -52,6 +54,7 @@ __device__ __forceinline__ void range_of(int64_t N, int bpb, int64_t& b, int64_t
   lo = b * N + (int64_t)j * per;
   const int64_t end = (int64_t)j * per + per < N ? (int64_t)j * per + per : N;
   hi = b * N + end;
+  if (lo > hi) lo = hi;
 }
 
 // Visit ids[lo, hi) as f(index, id): a scalar head up to 16-byte alignment,
@@ -90,52 +93,87 @@ __device__ __forceinline__ void for_each_id(const int32_t* __restrict__ ids, int
   for (int64_t i = a + 4 * nv + t; i < hi; i += nt) f(i, __ldg(ids + i));
 }
 
-// zero_sums (non-accumulating updates): the blocks also clear the f64 sums
-// for k_segsum, a grid-strided slice each, instead of a separate memset.
-__global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, int64_t B, int64_t N,
-                                               int64_t K, int bpb, int32_t* __restrict__ hist,
-                                               int32_t* __restrict__ table,
-                                               double* __restrict__ zero_sums, int64_t zero_n) {
+
+// ----------------------------------------------------------------- hist
+// Each block histograms its contiguous point range into its row of `table`
+// (B*bpb rows of K int32).  K <= HIST_SMEM_KEYS: shared-memory bins, the whole
+// row written out (zeros included); larger K: warp-aggregated atomics straight
+// into the (pre-zeroed) global row.  Integer counts are order-independent.
+// The blocks also clear, a grid-strided slice each, the f64 sums (unless the
+// update accumulates) and the per-key arrival counters of k_segsum's ordered
+// merge -- no separate memsets.
+__global__ void __launch_bounds__(1024)
+    k_hist(const int32_t* __restrict__ ids, int64_t N, int64_t K, int bpb, int32_t* __restrict__ table,
+           double* __restrict__ zero_sums, int64_t zero_n, int32_t* __restrict__ arrive,
+           int64_t arrive_n) {
   extern __shared__ int32_t sh[];
-  if (zero_sums) {
+  {
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
-    const int64_t n2 = zero_n >> 1;  // 16-byte stores when the (caller-owned) buffer allows
-    double2* z2 = reinterpret_cast<double2*>(zero_sums);
-    if ((reinterpret_cast<uintptr_t>(zero_sums) & 15) == 0) {
-      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += nt)
-        z2[i] = make_double2(0.0, 0.0);
-      if ((zero_n & 1) && blockIdx.x == 0 && threadIdx.x == 0) zero_sums[zero_n - 1] = 0.0;
-    } else {
-      for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < zero_n; i += nt)
-        zero_sums[i] = 0.0;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (zero_sums) {
+      if ((reinterpret_cast<uintptr_t>(zero_sums) & 15) == 0) {  // 16-byte stores
+        double2* z2 = reinterpret_cast<double2*>(zero_sums);
+        for (int64_t i = t0; i < (zero_n >> 1); i += nt) z2[i] = make_double2(0.0, 0.0);
+        if ((zero_n & 1) && t0 == 0) zero_sums[zero_n - 1] = 0.0;
+      } else {
+        for (int64_t i = t0; i < zero_n; i += nt) zero_sums[i] = 0.0;
+      }
     }
+    for (int64_t i = t0; i < arrive_n; i += nt) arrive[i] = 0;
   }
   const bool use_smem = K <= HIST_SMEM_KEYS;
   int64_t b, lo, hi;
   range_of(N, bpb, b, lo, hi);
+  int32_t* trow = table + (int64_t)blockIdx.x * K;
   if (use_smem) {
     for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sh[k] = 0;
     __syncthreads();
   }
   for_each_id(ids, lo, hi, [&](int64_t, int32_t id) {
-    if (id < 0 || id >= K) return;  // validated on the host side
+    if (id < 0 || id >= K) return;  // not a cluster: left out of the sort (and the sums)
     if (use_smem) {
       atomicAdd(&sh[id], 1);
     } else {
-      const int64_t key = b * K + id;
-      const unsigned peers = __match_any_sync(__activemask(), key);
-      const int leader = __ffs(peers) - 1;
-      if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[key], __popc(peers));
+      const unsigned peers = __match_any_sync(__activemask(), id);
+      if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&trow[id], __popc(peers));
     }
   });
   if (use_smem) {
     __syncthreads();
-    int32_t* trow = table + (int64_t)blockIdx.x * K;  // this block's histogram, reused by the scatter
-    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
-      const int32_t c = sh[k];
-      trow[k] = c;
-      if (c) atomicAdd(&hist[b * K + k], c);
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) trow[k] = sh[k];
+  }
+}
+
+// ----------------------------------------------------------------- colscan
+// Per key, over the bpb block rows of its batch element in block order:
+// table[blk][k] <- sum of table[blk'][k] for blk' < blk (where block blk's
+// points of key k start inside the key's run), and hist[b*K + k] <- the total.
+// Block (32 keys) x (32 row groups): coalesced 128-byte row reads.
+__global__ void __launch_bounds__(1024)
+    k_colscan(int32_t* __restrict__ table, int64_t K, int bpb, int64_t ktiles,
+              int32_t* __restrict__ hist) {
+  __shared__ int32_t part[32][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t b = blockIdx.x / ktiles;
+  const int64_t k = (blockIdx.x - b * ktiles) * 32 + tx;
+  const int R = (bpb + 31) / 32;
+  const int r0 = ty * R < bpb ? ty * R : bpb;
+  const int r1 = r0 + R < bpb ? r0 + R : bpb;
+  int32_t* col = table + (int64_t)b * bpb * K + k;
+  int32_t s = 0;
+  if (k < K)
+    for (int r = r0; r < r1; ++r) s += col[(int64_t)r * K];
+  part[ty][tx] = s;
+  __syncthreads();
+  int32_t pre = 0;
+  for (int q = 0; q < ty; ++q) pre += part[q][tx];
+  if (k < K) {
+    for (int r = r0; r < r1; ++r) {
+      const int32_t c = col[(int64_t)r * K];
+      col[(int64_t)r * K] = pre;
+      pre += c;
     }
+    if (ty == 31) hist[b * K + k] = pre;
   }
 }
 
@@ -145,11 +183,11 @@ __global__ void __launch_bounds__(1024) k_hist(const int32_t* __restrict__ ids, 
 // is valid), then walks its own K keys in tiles of 4096 (4 consecutive keys
 // per thread, so K <= 4096 is one pass): block-wide exclusive scan per tile
 // plus a running carry.  Also produces the int64 counts and the reference's
-// synchronized_merges count.
+// synchronized_merges count.  off[B*K] = number of sorted (valid) points.
 __global__ void __launch_bounds__(1024)
     k_scan(const int32_t* __restrict__ hist, int64_t B, int64_t N, int64_t K, int64_t chunk,
-           int accumulate, int64_t* __restrict__ off, int32_t* __restrict__ cursor,
-           int64_t* __restrict__ counts, int64_t* __restrict__ merges) {
+           int accumulate, int64_t* __restrict__ off, int64_t* __restrict__ counts,
+           int64_t* __restrict__ merges) {
   __shared__ int64_t warp_tot[32];
   __shared__ unsigned long long warp_mg[32];
   const int64_t b = blockIdx.x;
@@ -162,10 +200,10 @@ __global__ void __launch_bounds__(1024)
   __syncthreads();
   int64_t carry = 0;
   for (int i = 0; i < 32; ++i) carry += warp_tot[i];
+  const int64_t base_b = carry;  // start of this batch element's runs
   __syncthreads();
   unsigned long long mg = 0;
   const uint32_t ch = (uint32_t)chunk;
-  // tiles of 4096 keys, 4 consecutive keys per thread: one pass when K <= 4096
   for (int64_t base = 0; base < K; base += 4096) {
     int64_t c[4], sum = 0;
 #pragma unroll
@@ -197,13 +235,12 @@ __global__ void __launch_bounds__(1024)
       if (kk < K) {
         const int64_t k = b * K + kk;
         off[k] = run;
-        cursor[k] = (int32_t)run;
-        counts[k] = accumulate ? counts[k] + c[q] : c[q];
+        if (counts) counts[k] = accumulate ? counts[k] + c[q] : c[q];
         if (c[q] > 0 && merges) {
           // reference merges: the run [s, e) of this key inside its batch element
           // meets floor((e-1)/chunk) - floor(s/chunk) + 1 update chunks
           // (all quantities < 2^31: 32-bit divisions)
-          const uint32_t s0 = (uint32_t)(run - b * N), e = s0 + (uint32_t)c[q];
+          const uint32_t s0 = (uint32_t)(run - base_b), e = s0 + (uint32_t)c[q];
           mg += (unsigned long long)((e - 1) / ch - s0 / ch + 1);
         }
       }
@@ -224,145 +261,337 @@ __global__ void __launch_bounds__(1024)
 }
 
 // ----------------------------------------------------------------- scatter
-// Bucket point indices by key.  Block-aggregated: a block histograms its
-// contiguous point range in shared memory, reserves ONE contiguous range per
-// non-empty key with a single global atomic, then hands out positions with
-// shared-memory cursors -- no per-point global atomics, no dependency chains.
-__global__ void __launch_bounds__(1024)
-    k_scatter_block(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K, int bpb,
-                    const int32_t* __restrict__ table, int32_t* __restrict__ cursor,
-                    int32_t* __restrict__ order) {
-  extern __shared__ int32_t sh[];
-  int64_t b, lo, hi;
-  range_of(N, bpb, b, lo, hi);
-  // this block's histogram (built by k_hist over the same point range):
-  // reserve one contiguous range per non-empty key
-  const int32_t* trow = table + (int64_t)blockIdx.x * K;
-  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
-    const int32_t c = trow[k];
-    sh[k] = c ? atomicAdd(&cursor[b * K + k], c) : 0;
-  }
-  __syncthreads();
-  for_each_id(ids, lo, hi, [&](int64_t i, int32_t id) {
-    if (id < 0 || id >= K) return;
-    const int pos = atomicAdd(&sh[id], 1);
-    order[pos] = (int32_t)i;
-  });
-}
+// Stable counting sort of the point indices by id.  Each block walks its range
+// in sub-tiles of SD_S points; a sub-tile is sorted in shared memory by LSD
+// radix passes of <= 8 bits: warp w owns SD_PW consecutive positions of the
+// current order, counts digits per (digit, warp) (one counter update per
+// distinct digit per warp step, warp-private, no atomics), a block scan in
+// digit-major/warp-minor order gives every (digit, warp) its base, and a
+// second walk in the same order places the elements -- stable by construction.
+// The sorted sub-tile is written at off[key] + (block base of the key, from
+// k_colscan, advanced by earlier sub-tiles) + rank in the key's run: the
+// global order is the stable argsort of the ids (_kernels.py:118-132).
+constexpr int SD_T = 1024;              // threads per block (one block per SM)
+constexpr int SD_W = SD_T / 32;         // warps
+constexpr int SD_S = 8192;              // points per sub-tile
+constexpr int SD_PW = SD_S / SD_W;      // positions per warp
+constexpr int SD_PT = SD_S / SD_T;      // positions per thread (blocked phases)
+constexpr int SD_KSMEM = 4096;          // K up to this: the block's key bases live in smem
+constexpr size_t SD_SMEM = (size_t)SD_S * 4 + 2 * (size_t)SD_S * 2 + 256 * SD_W * 4;
+constexpr size_t SD_SMEM_BASES = SD_SMEM + (size_t)SD_KSMEM * 4;
 
-// Staged variant (K <= SC_KMAX): the block's range is processed in sub-tiles
-// of SC_S points.  Each sub-tile is counting-sorted by key in shared memory
-// (local ranks from shared atomics, a block scan of the K counts) and then
-// written out in sorted order, so consecutive threads store consecutive
-// positions of the same key's run: one store instruction touches a few
-// 32-byte sectors instead of 32 scattered ones.  Staged entries pack
-// (local index << 14) | key into 32 bits.
-#ifndef FK_SC_PT
-#define FK_SC_PT 16
-#endif
-constexpr int SC_PT = FK_SC_PT;      // points per thread per sub-tile
-constexpr int SC_S = 1024 * SC_PT;   // points per sub-tile
-#ifndef FK_SC_MIN_RANGE
-#define FK_SC_MIN_RANGE 6144
-#endif
-constexpr int SC_MIN_RANGE = FK_SC_MIN_RANGE;  // staged only for block ranges at least this long
-constexpr int SC_KMAX = 4096;  // keys: 3 K-int tables + the stage fit twice per SM
-__global__ void __launch_bounds__(1024, SC_PT <= 8 ? 2 : 1)
-    k_scatter_staged(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K, int bpb,
-                     const int32_t* __restrict__ table, int32_t* __restrict__ cursor,
-                     int32_t* __restrict__ order) {
-  extern __shared__ int32_t sm[];
-  __shared__ int32_t wtot[32];
-  int32_t* gcur = sm;          // next global position of each key for this block
-  int32_t* lcnt = sm + K;      // sub-tile counts per key
-  int32_t* lbase = sm + 2 * K;  // exclusive scan of lcnt
-  uint32_t* stage = reinterpret_cast<uint32_t*>(sm + 3 * K);
-  int64_t b, lo, hi;
-  range_of(N, bpb, b, lo, hi);
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  const int32_t* trow = table + (int64_t)blockIdx.x * K;
-  for (int k = t; k < K; k += 1024) {
-    const int32_t c = trow[k];
-    gcur[k] = c ? atomicAdd(&cursor[b * K + k], c) : 0;
+// Exclusive block scan (SD_T threads) of one value per thread; *total = sum.
+template <typename Op>
+__device__ __forceinline__ int sd_block_scan(int v, int ident, int* wbuf, int* total, Op op) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl = op(incl, u);
   }
-  for (int64_t s0 = lo; s0 < hi; s0 += SC_S) {
-    const int n = (int)(hi - s0 < SC_S ? hi - s0 : SC_S);
-    for (int k = t; k < K; k += 1024) lcnt[k] = 0;
-    __syncthreads();
-    int32_t id[SC_PT], rk[SC_PT];
-#pragma unroll
-    for (int j = 0; j < SC_PT; ++j) id[j] = t + 1024 * j < n ? __ldg(ids + s0 + t + 1024 * j) : -1;
-#pragma unroll
-    for (int j = 0; j < SC_PT; ++j) rk[j] = (id[j] >= 0 && id[j] < K) ? atomicAdd(&lcnt[id[j]], 1) : -1;
-    __syncthreads();
-    // exclusive scan of lcnt: 4 consecutive keys per thread (K <= 4096)
-    int v[4], sum = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = 4 * t + q;
-      v[q] = k < K ? lcnt[k] : 0;
-      sum += v[q];
-    }
-    int incl = sum;
+  int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+  if (lane == 0) excl = ident;
+  if (lane == 31) wbuf[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < SD_W ? wbuf[lane] : ident;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += u;
+      const int u = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x = op(x, u);
     }
-    if (lane == 31) wtot[w] = incl;
-    __syncthreads();
-    if (w == 0) {
-      int x = wtot[lane];
+    if (lane < SD_W) wbuf[lane] = x;  // inclusive over warps
+  }
+  __syncthreads();
+  const int res = w ? op(wbuf[w - 1], excl) : excl;
+  if (total) *total = wbuf[SD_W - 1];
+  __syncthreads();
+  return res;
+}
+
+// Lanes holding the same digit as this lane, among `valid`.  MATCH = 1 uses
+// match.any; otherwise one ballot per digit bit (CUB's MatchAny).
+template <bool MATCH>
+__device__ __forceinline__ unsigned sd_peers(uint32_t dg, int nbits, bool valid) {
+  if (MATCH) return __match_any_sync(0xffffffffu, valid ? dg : 0x10000u | (threadIdx.x & 31)) &
+                    __ballot_sync(0xffffffffu, valid);
+  unsigned m = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += u;
+  for (int i = 0; i < 8; ++i) {
+    if (i < nbits) {
+      const bool bit = (dg >> i) & 1u;
+      const unsigned bal = __ballot_sync(0xffffffffu, bit);
+      m &= bit ? bal : ~bal;
+    }
+  }
+  return m;
+}
+
+template <int NP, bool SBASE, bool MATCH>
+__global__ void __launch_bounds__(SD_T, 1)
+    k_scatter_stable(const int32_t* __restrict__ ids, int64_t N, int64_t K, int bpb, int last_bits,
+                     int32_t* __restrict__ table, const int64_t* __restrict__ off,
+                     int32_t* __restrict__ order) {
+  extern __shared__ __align__(16) uint8_t sd_sm[];
+  uint32_t* skey = reinterpret_cast<uint32_t*>(sd_sm);
+  uint16_t* pa = reinterpret_cast<uint16_t*>(skey + SD_S);
+  uint16_t* pb = pa + SD_S;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(pb + SD_S);
+  int32_t* sbase = reinterpret_cast<int32_t*>(cnt + 256 * SD_W);  // SBASE: next position per key
+  __shared__ int wbuf[32];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const auto add = [](int a, int b) { return a + b; };
+  const auto mx = [](int a, int b) { return a > b ? a : b; };
+  int64_t b, lo, hi;
+  range_of(N, bpb, b, lo, hi);
+  int32_t* trow = table + (int64_t)blockIdx.x * K;
+  const int64_t* offb = off + b * K;
+  if (SBASE)  // flat positions < 2^31 (B*N is): int32 bases, advanced in shared memory
+    for (int k = t; k < K; k += SD_T) sbase[k] = (int32_t)(offb[k] + trow[k]);
+  for (int64_t s0 = lo; s0 < hi; s0 += SD_S) {
+    const int n = (int)(hi - s0 < SD_S ? hi - s0 : SD_S);
+#pragma unroll 4
+    for (int i = t; i < SD_S; i += SD_T) skey[i] = i < n ? (uint32_t)__ldg(ids + s0 + i) : 0xffffffffu;
+    __syncthreads();
+    int nv = n;
+    uint16_t* src = pa;
+    uint16_t* dst = pb;
+#pragma unroll
+    for (int pass = 0; pass < NP; ++pass) {
+      const int shift = 8 * pass;
+      const int nbits = pass == NP - 1 ? last_bits : 8;
+      const uint32_t dmask = (1u << nbits) - 1u;
+      const int E = (1 << nbits) * SD_W;  // (digit, warp) counters
+      for (int i = t; i < E; i += SD_T) cnt[i] = 0;
+      __syncthreads();
+      // count walk (pass 0 visits the sub-tile in index order and drops ids
+      // outside [0, K): they are not points of any cluster).  This lane's
+      // digits and peer masks are kept for the scatter walk.
+      uint32_t dge[SD_PW / 32];  // digit << 16 | local index, or ~0 for no element
+      unsigned pes[SD_PW / 32];
+#pragma unroll
+      for (int st = 0; st < SD_PW / 32; ++st) {
+        const int pos = w * SD_PW + st * 32 + lane;
+        bool valid;
+        uint32_t e, k;
+        if (pass == 0) {
+          e = (uint32_t)pos;
+          k = skey[pos];
+          valid = pos < n && k < (uint32_t)K;
+        } else {
+          valid = pos < nv;
+          e = valid ? src[pos] : 0u;
+          k = skey[e];
+        }
+        const uint32_t dg = (k >> shift) & dmask;
+        const unsigned peers = sd_peers<MATCH>(dg, nbits, valid);
+        dge[st] = valid ? (dg << 16 | e) : 0xffffffffu;
+        pes[st] = peers;
       }
-      wtot[lane] = x;
-    }
-    __syncthreads();
-    int run = incl - sum + (w ? wtot[w - 1] : 0);
+      // per-(digit, warp) counts: the lowest lane of each digit group adds the
+      // group's size, one step after another (warp-private counters)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = 4 * t + q;
-      if (k < K) lbase[k] = run;
-      run += v[q];
+      for (int st = 0; st < SD_PW / 32; ++st) {
+        if (dge[st] != 0xffffffffu && (pes[st] & lt) == 0) cnt[(dge[st] >> 16) * SD_W + w] += (uint32_t)__popc(pes[st]);
+        __syncwarp();
+      }
+      __syncthreads();
+      {  // exclusive scan of the counters, digit-major / warp-minor
+        const int per = E >= SD_T ? E / SD_T : 1;
+        const int i0 = t * per;
+        uint32_t v[8];
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v[j] = (j < per && i0 + j < E) ? cnt[i0 + j] : 0u;
+          sum += (int)v[j];
+        }
+        int tot;
+        int ex = sd_block_scan(sum, 0, wbuf, &tot, add);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < per && i0 + j < E) {
+            cnt[i0 + j] = (uint32_t)ex;
+            ex += (int)v[j];
+          }
+        if (pass == 0) nv = tot;
+      }
+      __syncthreads();
+      // scatter walk: same positions in the same order
+#pragma unroll
+      for (int st = 0; st < SD_PW / 32; ++st) {
+        const bool ok = dge[st] != 0xffffffffu;
+        const uint32_t dg = dge[st] >> 16;
+        const unsigned peers = pes[st];
+        uint32_t base = 0;
+        if (ok) {
+          base = cnt[dg * SD_W + w];
+          dst[base + __popc(peers & lt)] = (uint16_t)(dge[st] & 0xffffu);
+        }
+        __syncwarp();
+        if (ok && (peers & lt) == 0) cnt[dg * SD_W + w] = base + (uint32_t)__popc(peers);
+        __syncwarp();
+      }
+      __syncthreads();
+      uint16_t* tmp = src;
+      src = dst;
+      dst = tmp;
     }
+    // src[0, nv): the sub-tile's local indices stably sorted by id.  Run starts,
+    // blocked (thread t owns positions [SD_PT*t, SD_PT*t + SD_PT)), into dst.
+    {
+      const int p0 = SD_PT * t;
+      uint32_t kp = (p0 > 0 && p0 - 1 < nv) ? skey[src[p0 - 1]] : 0xffffffffu;
+      int rs[SD_PT];
+      int m = -1;
+#pragma unroll
+      for (int j = 0; j < SD_PT; ++j) {
+        const int p = p0 + j;
+        if (p < nv) {
+          const uint32_t k = skey[src[p]];
+          if (k != kp || p == 0) m = p;
+          kp = k;
+        }
+        rs[j] = m;
+      }
+      const int carry = sd_block_scan(m, -1, wbuf, nullptr, mx);
+#pragma unroll
+      for (int j = 0; j < SD_PT; ++j)
+        if (p0 + j < nv) dst[p0 + j] = (uint16_t)(rs[j] >= 0 ? rs[j] : carry);
+    }
+    __syncthreads();
+    // write the order (strided: a warp stores 32 consecutive positions); every
+    // base is fetched before the first store, then each run's end advances the
+    // key's base for the next sub-tile
+    int32_t gp[SD_PT];  // flat positions: B*N < 2^31
+    uint32_t kk[SD_PT];
+    bool endr[SD_PT];
+#pragma unroll
+    for (int j = 0; j < SD_PT; ++j) {
+      const int p = j * SD_T + t;
+      kk[j] = 0xffffffffu;
+      endr[j] = false;
+      if (p < nv) {
+        const uint32_t k = skey[src[p]];
+        const int r = p - (int)dst[p];
+        kk[j] = k;
+        gp[j] = (int32_t)(SBASE ? sbase[k] : offb[k] + __ldcg(trow + k)) + r;
+        endr[j] = p + 1 == nv || (int)dst[p + 1] == p + 1;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < SD_PT; ++j)
+      if (kk[j] != 0xffffffffu) order[gp[j]] = (int32_t)(s0 + src[j * SD_T + t]);
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < SC_PT; ++j)
-      if (rk[j] >= 0) stage[lbase[id[j]] + rk[j]] = ((uint32_t)(t + 1024 * j) << 14) | (uint32_t)id[j];
+    for (int j = 0; j < SD_PT; ++j)
+      if (endr[j]) {
+        if (SBASE)
+          sbase[kk[j]] = (int32_t)(gp[j] + 1);
+        else
+          __stcg(trow + kk[j], (int32_t)((int64_t)gp[j] + 1 - offb[kk[j]]));
+      }
     __syncthreads();
-    const int tot = wtot[31];
-    for (int p = t; p < tot; p += 1024) {
-      const uint32_t e = stage[p];
-      const int key = (int)(e & 0x3fffu);
-      order[gcur[key] + p - lbase[key]] = (int32_t)(s0 + (e >> 14));
-    }
-    __syncthreads();
-    for (int k = t; k < K; k += 1024) gcur[k] += lcnt[k];
   }
 }
 
-// Large B*K: warp-aggregated cursor bumps straight in global memory.
-__global__ void k_scatter(const int32_t* __restrict__ ids, int64_t B, int64_t N, int64_t K,
-                          int32_t* __restrict__ cursor, int32_t* __restrict__ order) {
-  const int64_t P = B * N;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += stride) {
-    const int64_t b = i / N;
-    const int32_t id = ids[i];
-    if (id < 0 || id >= K) continue;
-    const int64_t key = b * K + id;
-    const unsigned mask = __activemask();
-    const unsigned peers = __match_any_sync(mask, key);
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    int base = 0;
-    if (lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    const int rank = __popc(peers & ((1u << lane) - 1));
-    order[base + rank] = (int32_t)i;
+// Stable scatter for K <= SW_KMAX: warp-granular tables instead of a block
+// sort.  Block = W warps; warp w owns a contiguous part of the block's range.
+//   1. each warp counts its part into its own row of a (W, K) u16 table
+//      (shared atomics: counts are order-independent);
+//   2. per key, an exclusive prefix over the W rows (warp order = index
+//      order), plus the key's global base off[key] + (block base, k_colscan);
+//   3. each warp walks its part in index order, 32 points a step; every lane
+//      takes its rank from a returning shared atomic on its warp's count.
+// No match.any: its cost grows with the number of distinct values in the warp
+// (scripts/probe_match.cu: ~2000 cycles per warp instruction at 32 distinct
+// ids with 32 warps per SM, against ~65 for a conflicting shared atomic).
+// The ids of SW_U steps are loaded together.  The u16 table needs block
+// ranges < 2^16 points (update_bpb).
+constexpr int SW_KMAX = 32766;            // W * (K + 2) * 2 bytes <= 64 KB
+constexpr int SW_TABLE_BYTES = 65536;
+constexpr int SW_U = 8;                   // steps in flight per warp
+
+template <int W>
+__global__ void __launch_bounds__(W * 32)
+    k_scatter_warp(const int32_t* __restrict__ ids, int64_t N, int64_t K, int bpb,
+                   const int32_t* __restrict__ table, const int64_t* __restrict__ off,
+                   int32_t* __restrict__ order) {
+  extern __shared__ __align__(16) uint8_t sw_sm[];
+  // rows padded to K + 2 entries: the W rows of one key fall in different banks
+  const int KS = (int)K + 2;
+  uint16_t* tab = reinterpret_cast<uint16_t*>(sw_sm);                           // W * KS
+  int32_t* kbase = reinterpret_cast<int32_t*>(sw_sm + ((W * KS * 2 + 15) & ~15));  // K
+  uint32_t* tab32 = reinterpret_cast<uint32_t*>(sw_sm);
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t Ku = (uint32_t)K;
+  int64_t b, lo, hi;
+  range_of(N, bpb, b, lo, hi);
+  const int32_t* trow = table + (int64_t)blockIdx.x * K;
+  const int64_t* offb = off + b * K;
+  for (int i = t; i < W * KS / 2; i += W * 32) tab32[i] = 0u;
+  for (int k = t; k < K; k += W * 32) kbase[k] = (int32_t)(offb[k] + trow[k]);  // flat < 2^31
+  // this warp's part [a, e) of the block range
+  const int n = (int)(hi - lo);
+  const int a = (int)((int64_t)n * w / W), e = (int)((int64_t)n * (w + 1) / W);
+  const int32_t* idw = ids + lo;
+  __syncthreads();
+  // 1. per-warp counts (fire-and-forget shared atomics on packed u16 pairs)
+  for (int p0 = a; p0 < e; p0 += 32 * SW_U) {
+    uint32_t id[SW_U];
+#pragma unroll
+    for (int u = 0; u < SW_U; ++u) {
+      const int p = p0 + u * 32 + lane;
+      id[u] = p < e ? (uint32_t)__ldg(idw + p) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int u = 0; u < SW_U; ++u)
+      if (id[u] < Ku) {
+        const uint32_t f = (uint32_t)(w * KS) + id[u];
+        atomicAdd(tab32 + (f >> 1), 1u << (16 * (f & 1)));
+      }
+  }
+  __syncthreads();
+  // 2. exclusive prefix over the W warp rows of each key: segmented warp scans
+  //    of width W (32/W keys per warp instruction)
+  {
+    constexpr int KPW = 32 / W;  // keys per warp pass
+    const int q = lane % W, ks = lane / W;
+    for (int k0 = w * KPW; k0 < K; k0 += W * KPW) {
+      const int k = k0 + ks;
+      const uint32_t c = k < K ? tab[q * KS + k] : 0u;
+      uint32_t v = c;
+#pragma unroll
+      for (int o = 1; o < W; o <<= 1) {
+        const uint32_t u = __shfl_up_sync(0xffffffffu, v, o, W);
+        if (q >= o) v += u;
+      }
+      if (k < K) tab[q * KS + k] = (uint16_t)(v - c);
+    }
+  }
+  __syncthreads();
+  // 3. ranks in index order: every lane bumps its warp's running count of its
+  //    id with a returning shared atomic; lanes of one instruction that hit
+  //    the same counter are serialized in lane order, so the returned counts
+  //    are the stable ranks (checked against numpy's stable argsort in
+  //    tests/test_gpu_kernels.py).  The ids are re-read (L2-resident).
+  for (int p0 = a; p0 < e; p0 += 32 * SW_U) {
+    uint32_t id[SW_U];
+#pragma unroll
+    for (int u = 0; u < SW_U; ++u) {
+      const int p = p0 + u * 32 + lane;
+      id[u] = p < e ? (uint32_t)__ldg(idw + p) : 0xffffffffu;
+    }
+#pragma unroll
+    for (int u = 0; u < SW_U; ++u)
+      if (id[u] < Ku) {
+        const uint32_t f = (uint32_t)(w * KS) + id[u];
+        const uint32_t sh = 16 * (f & 1);
+        const uint32_t r = (atomicAdd(tab32 + (f >> 1), 1u << sh) >> sh) & 0xffffu;
+        order[kbase[id[u]] + (int32_t)r] = (int32_t)(lo + p0 + u * 32 + lane);
+      }
   }
 }
 
@@ -425,19 +654,58 @@ FK_DEV uint4 ldg_stream(const void* p) {
   return r;
 }
 
+// One merge per (slice, segment).  A segment inside the slice is stored
+// directly.  A segment spanning slices [w0, w1] leaves its partial in slot
+// part[w][s] (s = 0 when the segment contains the slice's first position, else
+// 1), and the last slice to arrive (per-key counter) adds the partials in
+// slice order w0..w1 -- the reference's ascending merge order, whichever
+// warp finishes last.  `acc_j(j)` gives this lane's partial of column j, for
+// the columns `for_cols` visits.
+struct SegMerge {
+  double* part;     // [slices][2][d] f64 partials of segments spanning slices
+  int32_t* arrive;  // [B*K] arrival counters (zeroed by k_hist)
+  int64_t L, d;
+};
+
+FK_DEV void seg_flush_boundary(const SegMerge& m, int64_t wg, int64_t p0, int64_t key, int64_t seg_lo,
+                               int64_t seg_end, double* __restrict__ dst) {
+  // the caller has written its partial into part[wg][slot] and fenced
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  int last = 0;
+  const int64_t w0 = seg_lo / m.L, w1 = (seg_end - 1) / m.L;
+  if (lane == 0) {
+    const int old = atomicAdd(m.arrive + key, 1);
+    last = old == (int)(w1 - w0);
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  const int64_t s0 = (seg_lo == w0 * m.L) ? 0 : 1;
+  for (int64_t j = lane; j < m.d; j += 32) {
+    double tot = __ldcg(m.part + (w0 * 2 + s0) * m.d + j);
+    for (int64_t w = w0 + 1; w <= w1; ++w) tot += __ldcg(m.part + (w * 2) * m.d + j);
+    dst[j] += tot;
+  }
+  (void)p0;
+  (void)wg;
+}
+
 // LPR lanes cover one row with VPL 16-byte vectors each; RPW = 32/LPR rows per
 // warp step; U steps are issued back to back to keep bytes in flight.
 template <typename T, typename A, int LPR, int VPL, int U>
 __global__ void __launch_bounds__(256)
     k_segsum(const T* __restrict__ X, const int32_t* __restrict__ order,
-             const int64_t* __restrict__ off, int64_t BK, int64_t P, int64_t L, int64_t d,
-             double* __restrict__ sums, const int32_t* __restrict__ ids, int64_t N, int64_t K) {
+             const int64_t* __restrict__ off, int64_t BK, int64_t L, int64_t d,
+             double* __restrict__ sums, const int32_t* __restrict__ ids, int64_t N, int64_t K,
+             SegMerge mg) {
   constexpr int E = VecCvt<T>::E;
   constexpr int RPW = 32 / LPR;
   constexpr int NA = VPL * E;
   const int lane = threadIdx.x & 31;
   const int sub = lane / LPR, sl = lane % LPR;
   const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t P = off[BK];  // sorted (valid) points
   const int64_t p0 = wg * L;
   if (p0 >= P) return;
   const int64_t p1 = (p0 + L < P) ? p0 + L : P;
@@ -447,14 +715,6 @@ __global__ void __launch_bounds__(256)
   const int32_t pt = order[p0];
   const int64_t pb = pt / N;
   int64_t key = pb * K + ids[pt];
-  if (key < 0 || key >= BK || off[key] > p0 || off[key + 1] <= p0) {
-    int64_t lo = 0, hi = BK;  // defensive (ids are validated by the caller)
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (off[mid] <= p0) lo = mid; else hi = mid;
-    }
-    key = lo;
-  }
   int64_t seg_lo = off[key], seg_end = off[key + 1];
   A acc[NA];
 #pragma unroll
@@ -513,24 +773,29 @@ __global__ void __launch_bounds__(256)
         for (int q = 0; q < VPL; ++q) VecCvt<T>::add(acc + q * E, v[u][q]);
     }
     p = lim;
-    // flush this segment's partial (one merge per segment)
+    // flush this segment's partial (one merge per segment; fixed shuffle tree)
 #pragma unroll
     for (int o = LPR; o < 32; o <<= 1)
 #pragma unroll
       for (int e = 0; e < NA; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
-    if (sub == 0) {
-      const bool owned = seg_lo >= p0 && seg_end <= p1;
-      double* dst = sums + key * d;
+    double* dst = sums + key * d;
+    if (seg_lo >= p0 && seg_end <= p1) {  // owned: the only writer of this key
+      if (sub == 0) {
 #pragma unroll
-      for (int q = 0; q < VPL; ++q)
+        for (int q = 0; q < VPL; ++q)
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          const int64_t j = (int64_t)(q * LPR + sl) * E + e;
-          if (owned)
-            dst[j] += (double)acc[q * E + e];
-          else
-            atomicAdd(dst + j, (double)acc[q * E + e]);
-        }
+          for (int e = 0; e < E; ++e) dst[(int64_t)(q * LPR + sl) * E + e] += (double)acc[q * E + e];
+      }
+    } else {
+      double* pp = mg.part + (wg * 2 + (seg_lo <= p0 ? 0 : 1)) * d;
+      if (sub == 0) {
+#pragma unroll
+        for (int q = 0; q < VPL; ++q)
+#pragma unroll
+          for (int e = 0; e < E; ++e) pp[(int64_t)(q * LPR + sl) * E + e] = (double)acc[q * E + e];
+        __threadfence();
+      }
+      seg_flush_boundary(mg, wg, p0, key, seg_lo, seg_end, dst);
     }
 #pragma unroll
     for (int e = 0; e < NA; ++e) acc[e] = (A)0;
@@ -547,10 +812,11 @@ __global__ void __launch_bounds__(256)
 // Any row width: one warp per slice, lanes stride over the features.
 template <typename T>
 __global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restrict__ order,
-                                 const int64_t* __restrict__ off, int64_t BK, int64_t P,
-                                 int64_t L, int64_t d, double* __restrict__ sums) {
+                                 const int64_t* __restrict__ off, int64_t BK, int64_t L, int64_t d,
+                                 double* __restrict__ sums, SegMerge mg) {
   const int lane = threadIdx.x & 31;
   const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t P = off[BK];
   const int64_t p0 = wg * L;
   if (p0 >= P) return;
   const int64_t p1 = (p0 + L < P) ? p0 + L : P;
@@ -565,17 +831,20 @@ __global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restr
     const int64_t seg_lo = off[key], seg_end = off[key + 1];
     const int64_t lim = seg_end < p1 ? seg_end : p1;
     const bool owned = seg_lo >= p0 && seg_end <= p1;
+    double* dst = sums + key * d;
+    double* pp = mg.part + (wg * 2 + (seg_lo <= p0 ? 0 : 1)) * d;
     for (int64_t j0 = 0; j0 < d; j0 += 32) {
       const int64_t j = j0 + lane;
       double acc = 0.0;
-      if (j < d)
-        for (int64_t r = p; r < lim; ++r) acc += as_f64(X[(int64_t)order[r] * d + j]);
       if (j < d) {
-        if (owned)
-          sums[key * d + j] += acc;
-        else
-          atomicAdd(sums + key * d + j, acc);
+        for (int64_t r = p; r < lim; ++r) acc += as_f64(X[(int64_t)order[r] * d + j]);
+        if (owned) dst[j] += acc;
+        else pp[j] = acc;
       }
+    }
+    if (!owned) {
+      __threadfence();
+      seg_flush_boundary(mg, wg, p0, key, seg_lo, seg_end, dst);
     }
     p = lim;
     if (p < p1) {
@@ -586,262 +855,33 @@ __global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restr
 }
 
 // Blocks per batch element for the histogram / scatter passes: ~2 waves in
-// total, each block owning >= 8192 points so the per-block K-bin table, its
-// scan and its cursor reservations amortize (same-box A/B,
-// profiles/r01_ab_update_bpb.txt: 2048 -> 8192 points took config 2 from 73
-// to 69 us and config 4 from 63 to 57 us; config 3 is capped by the wave count).
-static int64_t update_bpb(int64_t B, int64_t N, int num_sms) {
-  static int64_t min_range = -1;  // FK_UPDATE_MIN_RANGE: points per block lower bound (A/B)
-  if (min_range < 0) {
-    const char* e = getenv("FK_UPDATE_MIN_RANGE");
-    min_range = e ? atoll(e) : 8192;
-    if (min_range < 2048) min_range = 2048;  // the workspace table is sized for >= 2048
-  }
+// total, each block owning >= 8192 points (one stable-sort sub-tile) so the
+// per-block K-bin table, its column scan and the sort amortize.  For K beyond
+// the shared bins the block rows live in global memory: keep them at most
+// ~2 bytes per point.
+static int64_t update_bpb(int64_t B, int64_t N, int64_t K, int num_sms) {
   int64_t bpb = ((int64_t)num_sms * 2 + B - 1) / B;
-  const int64_t max_bpb = (N + min_range - 1) / min_range;
+  const int64_t max_bpb = (N + SD_S - 1) / SD_S;
   if (bpb > max_bpb) bpb = max_bpb;
+  if (K > HIST_SMEM_KEYS) {
+    const int64_t cap = N / (2 * K);
+    if (bpb > cap) bpb = cap;
+  }
+  const int64_t min_bpb = (N + 65534) / 65535;  // k_scatter_warp's u16 tables: ranges < 2^16
+  if (bpb < min_bpb) bpb = min_bpb;
   return bpb < 1 ? 1 : bpb;
 }
 constexpr int kMaxSms = 256;  // workspace bound for any sm_100 part
+constexpr int kSegWarpsPerSm = 32;
 
-// ------------------------------------------------- one-kernel cluster update
-// Small per-batch problems (config 4: B=64 x N=16k, K=256, d=64, fp16): one
-// thread-block cluster of C CTAs per batch element does the whole update in
-// shared memory, with no global scratch and one launch:
-//   1. each CTA histograms its N/C ids (shared bins) and counting-sorts its
-//      local point indices by id (shared cursors);
-//   2. rank 0 reads every CTA's bins over DSMEM: exact int64 counts and the
-//      reference's synchronized_merges count for this batch element;
-//   3. each CTA walks its local sorted order in contiguous runs per lane
-//      group, gathers the rows (16-B vectors), keeps fp32 running sums and
-//      merges ONCE per (run, segment) into its shared K x d fp32 table;
-//   4. CTA r reduces key range r of the C tables over DSMEM in fixed rank
-//      order and stores f64 sums directly (no global atomics).
-constexpr int CU_THREADS = 256;
-constexpr int CU_PMAX = 8192;               // local points per CTA
-constexpr size_t CU_TABLE_MAX = 96 * 1024;  // K * d * 4 bytes of shared sums
-
-template <typename T>
-__global__ void __launch_bounds__(CU_THREADS)
-    k_update_cluster(const T* __restrict__ X, const int32_t* __restrict__ ids, int64_t N, int K,
-                     int d, int64_t chunk, int accumulate, double* __restrict__ sums,
-                     int64_t* __restrict__ counts, int64_t* __restrict__ merges) {
-  extern __shared__ __align__(16) uint8_t cu_sm[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int C = (int)cluster.num_blocks();
-  const int r = (int)cluster.block_rank();
-  const int64_t b = blockIdx.x / C;
-  const int64_t per = (N + C - 1) / C;
-  const int64_t lo = (int64_t)r * per;
-  const int64_t hi = lo + per < N ? lo + per : N;
-  const int np = hi > lo ? (int)(hi - lo) : 0;
-  float* table = reinterpret_cast<float*>(cu_sm);                         // K*d
-  int32_t* hist = reinterpret_cast<int32_t*>(cu_sm + (size_t)K * d * 4);  // K
-  int32_t* cur = hist + K;                                                // K
-  int32_t* order = cur + K;                                               // per
-  int32_t* sid = order + per;                                             // per: local ids
-  __shared__ unsigned long long s_mg;
-  __shared__ int64_t wtot[32];
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  for (int k = t; k < K; k += CU_THREADS) hist[k] = 0;
-  for (int e = t; e < K * d; e += CU_THREADS) table[e] = 0.f;
-  if (t == 0) s_mg = 0;
-  __syncthreads();
-  const int32_t* idb = ids + b * N + lo;
-  for (int i = t; i < np; i += CU_THREADS) {
-    const int32_t id = __ldg(idb + i);
-    sid[i] = id;
-    if (id >= 0 && id < K) atomicAdd(&hist[id], 1);
-  }
-  __syncthreads();
-  // local exclusive scan of the bins -> cursors (one warp per 32-key tile, serial carry)
-  if (warp == 0) {
-    int carry = 0;
-    for (int base = 0; base < K; base += 32) {
-      const int k = base + lane;
-      const int c = k < K ? hist[k] : 0;
-      int v = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-      }
-      if (k < K) cur[k] = carry + v - c;
-      carry += __shfl_sync(0xffffffffu, v, 31);
-    }
-  }
-  cluster.sync();  // every CTA's bins are final (read remotely below)
-  if (r == 0) {
-    // exact counts + the reference's merge count for this batch element
-    int64_t carry = 0;
-    unsigned long long mg = 0;
-    const uint32_t ch = (uint32_t)chunk;
-    for (int base = 0; base < K; base += CU_THREADS) {
-      const int k = base + t;
-      int64_t c = 0;
-      if (k < K)
-        for (int q = 0; q < C; ++q) c += *cluster.map_shared_rank(hist + k, q);
-      int64_t v = c;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t u = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += u;
-      }
-      if (lane == 31) wtot[warp] = v;
-      __syncthreads();
-      int64_t wbase = 0;
-      for (int w = 0; w < warp; ++w) wbase += wtot[w];
-      const int64_t run = carry + wbase + v - c;
-      if (k < K) {
-        counts[b * K + k] = accumulate ? counts[b * K + k] + c : c;
-        if (c > 0) {
-          const uint32_t s0 = (uint32_t)run, e = s0 + (uint32_t)c;
-          mg += (unsigned long long)((e - 1) / ch - s0 / ch + 1);
-        }
-      }
-      int64_t tot = 0;
-      for (int w = 0; w < CU_THREADS / 32; ++w) tot += wtot[w];
-      carry += tot;
-      __syncthreads();
-    }
-    for (int o = 16; o; o >>= 1) mg += __shfl_xor_sync(0xffffffffu, mg, o);
-    if (lane == 0 && mg) atomicAdd(&s_mg, mg);
-  }
-  // local counting sort of the point indices (X is never permuted)
-  for (int i = t; i < np; i += CU_THREADS) {
-    const int32_t id = sid[i];
-    if (id >= 0 && id < K) order[atomicAdd(&cur[id], 1)] = i;
-  }
-  __syncthreads();
-  // cur[k] is now the END of key k's local run; the valid sorted length:
-  const int nv = K > 0 ? cur[K - 1] : 0;
-  // segmented sums: LPR lanes cover one row, each lane group walks a
-  // contiguous run of the local sorted order
-  constexpr int E = 16 / (int)sizeof(T);
-  const int vpr = d / E;                // 16-B vectors per row
-  const int lpr = vpr >= 32 ? 32 : vpr; // lanes per row (power of two: d in shape buckets)
-  const int vpl = vpr / lpr;            // vectors per lane
-  const int groups = CU_THREADS / lpr;
-  const int gid = t / lpr, gl = t % lpr;
-  const int run = (nv + groups - 1) / groups;
-  const int p0 = gid * run, p1 = p0 + run < nv ? p0 + run : nv;
-  const T* xb = X + (b * N + lo) * (int64_t)d;
-  if (p0 < p1) {
-    // key of position p0: first k with cur[k] > p0 (cur = run ends)
-    int klo = 0, khi = K - 1;
-    while (klo < khi) {
-      const int mid = (klo + khi) >> 1;
-      if (cur[mid] > p0) khi = mid; else klo = mid + 1;
-    }
-    for (int v0 = 0; v0 < vpl; ++v0) {
-      const int col = (v0 * lpr + gl) * E;
-      float acc[E];
-#pragma unroll
-      for (int e = 0; e < E; ++e) acc[e] = 0.f;
-      int k = klo, ke = cur[klo], nrow = 0;
-      auto flush = [&]() {
-        if (nrow) {
-          float* dst = table + (size_t)k * d + col;
-#pragma unroll
-          for (int e = 0; e < E; ++e) {
-            atomicAdd(dst + e, acc[e]);
-            acc[e] = 0.f;
-          }
-          nrow = 0;
-        }
-      };
-      // CU_U gathers in flight across segment boundaries, added in sorted order;
-      // one merge per (run, segment)
-      constexpr int CU_U = 16;
-      for (int p = p0; p < p1; p += CU_U) {
-        const int n = p1 - p < CU_U ? p1 - p : CU_U;
-        uint4 v[CU_U];
-#pragma unroll
-        for (int u = 0; u < CU_U; ++u)
-          if (u < n) v[u] = ldg_stream(xb + (int64_t)order[p + u] * d + col);
-#pragma unroll
-        for (int u = 0; u < CU_U; ++u) {
-          if (u < n) {
-            while (p + u >= ke) {  // segment boundary (skipping empty keys)
-              flush();
-              ++k;
-              ke = cur[k];
-            }
-            VecCvt<T>::add(acc, v[u]);
-            ++nrow;
-          }
-        }
-      }
-      flush();
-    }
-  }
-  cluster.sync();  // every table complete
-  // CTA r reduces keys [r*K/C, (r+1)*K/C) across the cluster, fixed rank order
-  const int k0 = (int)((int64_t)K * r / C), k1 = (int)((int64_t)K * (r + 1) / C);
-  const float* rt[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) rt[q] = cluster.map_shared_rank(table, q < C ? q : 0);
-  for (int e = k0 * d + t; e < k1 * d; e += CU_THREADS) {
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = q < C ? rt[q][e] : 0.f;  // all remote loads in flight
-    double acc = 0.0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (q < C) acc += (double)v[q];
-    double* o = sums + b * (int64_t)K * d + e;
-    *o = accumulate ? *o + acc : acc;
-  }
-  if (r == 0 && t == 0 && merges && s_mg) atomicAdd((unsigned long long*)merges, s_mg);
-  cluster.sync();  // keep every table alive until all remote reads are done
-}
-
-// cluster size for the one-kernel path, or 0 when it does not apply
-static int cluster_update_size(int dt, int64_t B, int64_t N, int64_t K, int64_t d, int num_sms) {
-  // Opt-in only (FK_UPDATE_CLUSTER=1): same-box A/B at config 4 measured 66.9 us
-  // against 61.4 us for the four-kernel path (0.45 waves of 8-warp CTAs and
-  // serialized phases leave HBM at 24%; profiles/r01_ab_cluster.txt).
-  const char* e = getenv("FK_UPDATE_CLUSTER");
-  if (!(e && e[0] == '1')) return 0;
-  if (dt != DT_BF16 && dt != DT_F16) return 0;  // f32/f64 keep f64 accumulation (bitwise path)
-  if ((d * 2) % 16 != 0 || d > 256 || (d / 8 & (d / 8 - 1)) != 0) return 0;
-  if ((size_t)K * d * 4 > CU_TABLE_MAX || K > 8192) return 0;
-  for (int C = 1; C <= 8; C <<= 1) {
-    const int64_t per = (N + C - 1) / C;
-    if (per > CU_PMAX) continue;
-    // enough CTAs to cover the machine when the batch is small
-    if (B * C < num_sms && C < 8 && (N + 2 * C - 1) / (2 * C) >= 512) continue;
-    return C;
-  }
-  return 0;
-}
-
-static size_t cluster_update_smem(int64_t N, int64_t K, int64_t d, int C) {
-  const int64_t per = (N + C - 1) / C;
-  return (size_t)K * d * 4 + (size_t)K * 8 + (size_t)per * 8;
-}
-
-template <typename T>
-static cudaError_t launch_cluster_update(const void* X, const int32_t* ids, int64_t B, int64_t N,
-                                         int64_t K, int64_t d, int64_t chunk, int accumulate,
-                                         double* sums, int64_t* counts, int64_t* merges, int C,
-                                         cudaStream_t s) {
-  const size_t smem = cluster_update_smem(N, K, d, C);
-  cudaFuncSetAttribute(k_update_cluster<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(B * C));
-  cfg.blockDim = dim3(CU_THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_update_cluster<T>, static_cast<const T*>(X), ids, N, (int)K,
-                            (int)d, chunk, accumulate, sums, counts, merges);
+// Slice length of k_segsum: 32 warp slices per SM (same-box A/B,
+// profiles/r01_ab_segsum.txt: 64 -> 32 took config 2 from 67.8 to 64.1 us
+// and config 4 from 52 to 49.5 us, config 3 unchanged; 16 starves config 3
+// of bytes in flight), at least 64 points each.
+static int64_t segsum_slice(int64_t P, int num_sms) {
+  const int64_t want = (int64_t)num_sms * kSegWarpsPerSm;
+  int64_t L = (P + want - 1) / want;
+  return L < 64 ? 64 : L;
 }
 
 // --------------------------------------------- multi-GPU exchange packing
@@ -926,39 +966,64 @@ cudaError_t launch_stats_pack(int unpack, int64_t* counts, double* obj, int32_t*
   return cudaGetLastError();
 }
 
-size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K) {
-  const int64_t BK = B * K, P = B * N;
+
+// Workspace: table (B*bpb*K) | hist (B*K) | off (B*K+1) | order (B*N) |
+// arrive (B*K) | segment partials (slices * 2 * d f64).
+struct UpdateWs {
+  int32_t* table;
+  int32_t* hist;
+  int64_t* off;
+  int32_t* order;
+  int32_t* arrive;
+  double* part;
+};
+
+static size_t update_ws_layout(int64_t B, int64_t N, int64_t K, int64_t d, int num_sms, void* base,
+                               UpdateWs* ws) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const int64_t table = K <= HIST_SMEM_KEYS ? B * update_bpb(B, N, kMaxSms) * K : 0;
-  return al(BK * 4) + al(BK * 4) + al((BK + 1) * 8) + al(P * 4) + al(table * 4);
+  const int64_t BK = B * K, P = B * N;
+  const int64_t bpb = update_bpb(B, N, K, num_sms);
+  const int64_t slices = (P + segsum_slice(P, num_sms) - 1) / segsum_slice(P, num_sms);
+  const size_t sz[6] = {al((size_t)B * bpb * K * 4), al((size_t)BK * 4), al((size_t)(BK + 1) * 8),
+                        al((size_t)P * 4), al((size_t)BK * 4), al((size_t)slices * 2 * d * 8)};
+  size_t total = 0;
+  uint8_t* p = static_cast<uint8_t*>(base);
+  void* ptrs[6];
+  for (int i = 0; i < 6; ++i) {
+    ptrs[i] = p ? p + total : nullptr;
+    total += sz[i];
+  }
+  if (ws) {
+    ws->table = (int32_t*)ptrs[0];
+    ws->hist = (int32_t*)ptrs[1];
+    ws->off = (int64_t*)ptrs[2];
+    ws->order = (int32_t*)ptrs[3];
+    ws->arrive = (int32_t*)ptrs[4];
+    ws->part = (double*)ptrs[5];
+  }
+  return total;
+}
+
+size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d) {
+  // blocks and slices grow with the SM count: size for the largest sm_100 part
+  return update_ws_layout(B, N, K, d, kMaxSms, nullptr, nullptr);
 }
 
 template <typename T, typename A>
-static cudaError_t dispatch_segsum(const void* X, const int32_t* order, const int64_t* off,
-                                   int64_t BK, int64_t P, int64_t d, double* sums, int num_sms,
-                                   cudaStream_t s, const int32_t* ids, int64_t N, int64_t K) {
-  constexpr int E = VecCvt<T>::E;
+static cudaError_t dispatch_segsum(const void* X, const UpdateWs& w, int64_t BK, int64_t P, int64_t d,
+                                   double* sums, int num_sms, cudaStream_t s, const int32_t* ids,
+                                   int64_t N, int64_t K) {
   const int th = 256;
-  // warp slices per SM: 32 (same-box A/B, profiles/r01_ab_segsum.txt: 64 -> 32
-  // took config 2 from 67.8 to 64.1 us and config 4 from 52 to 49.5 us, config 3
-  // unchanged; 16 starves config 3 of bytes in flight).  FK_SEGSUM_WPS overrides.
-  static int wps = -1;
-  if (wps < 0) {
-    const char* e = getenv("FK_SEGSUM_WPS");
-    wps = e ? atoi(e) : 32;
-    if (wps < 1) wps = 32;
-  }
-  const int64_t want_warps = (int64_t)num_sms * wps;
-  int64_t L = (P + want_warps - 1) / want_warps;
-  if (L < 64) L = 64;
+  const int64_t L = segsum_slice(P, num_sms);
   const int64_t warps = (P + L - 1) / L;
   const unsigned grid = (unsigned)((warps * 32 + th - 1) / th);
   const int64_t row_bytes = d * (int64_t)sizeof(T);
   const bool vec_ok = (row_bytes % 16) == 0;
   const int64_t nvec = row_bytes / 16;  // 16-byte vectors per row
   const T* x = (const T*)X;
+  const SegMerge mg{w.part, w.arrive, L, d};
 #define FK_SEG(LPR, VPL, U) \
-  k_segsum<T, A, LPR, VPL, U><<<grid, th, 0, s>>>(x, order, off, BK, P, L, d, sums, ids, N, K)
+  k_segsum<T, A, LPR, VPL, U><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, ids, N, K, mg)
   if (vec_ok) {
     switch (nvec) {
       case 1: FK_SEG(1, 1, 4); break;
@@ -970,14 +1035,112 @@ static cudaError_t dispatch_segsum(const void* X, const int32_t* order, const in
       case 64: FK_SEG(32, 2, 2); break;
       case 128: FK_SEG(32, 4, 1); break;
       default:
-        k_segsum_generic<T><<<grid, th, 0, s>>>(x, order, off, BK, P, L, d, sums);
+        k_segsum_generic<T><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, mg);
     }
   } else {
-    k_segsum_generic<T><<<grid, th, 0, s>>>(x, order, off, BK, P, L, d, sums);
+    k_segsum_generic<T><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, mg);
   }
 #undef FK_SEG
-  (void)E;
   return cudaGetLastError();
+}
+
+static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t N, int64_t K,
+                                         int64_t bpb, const UpdateWs& w, cudaStream_t s) {
+  int bits = 1;
+  while (bits < 31 && ((K - 1) >> bits) != 0) ++bits;
+  const int np = (bits + 7) / 8;
+  const int last_bits = bits - 8 * (np - 1);
+  static int match_env = -1;  // FK_SCATTER_MATCH=1: match.any instead of per-bit ballots (A/B)
+  if (match_env < 0) {
+    const char* e = getenv("FK_SCATTER_MATCH");
+    match_env = (e && e[0] == '1') ? 1 : 0;
+  }
+  const unsigned blocks = (unsigned)(B * bpb);
+  static int radix_env = -1;  // FK_SCATTER_RADIX=1: the block radix sort for every K (A/B)
+  if (radix_env < 0) {
+    const char* e = getenv("FK_SCATTER_RADIX");
+    radix_env = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (K <= SW_KMAX && !radix_env) {
+    int W = 32;
+    while (W > 1 && (int64_t)W * (K + 2) * 2 > SW_TABLE_BYTES) W >>= 1;
+    const size_t smem = (size_t)((W * (K + 2) * 2 + 15) & ~15) + (size_t)K * 4;
+#define FK_SW(WV)                                                                                  \
+  do {                                                                                             \
+    static bool attr_set[64] = {};                                                                 \
+    int dev = 0;                                                                                   \
+    cudaGetDevice(&dev);                                                                           \
+    if (!attr_set[dev & 63]) {                                                                     \
+      cudaFuncSetAttribute(k_scatter_warp<WV>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                           SW_TABLE_BYTES + SW_KMAX * 4 + 16);  /* the largest table + bases */                                     \
+      attr_set[dev & 63] = true;                                                                   \
+    }                                                                                              \
+    k_scatter_warp<WV><<<blocks, WV * 32, smem, s>>>(ids, N, K, (int)bpb, w.table, w.off, w.order); \
+  } while (0)
+    switch (W) {
+      case 32: FK_SW(32); break;
+      case 16: FK_SW(16); break;
+      case 8: FK_SW(8); break;
+      case 4: FK_SW(4); break;
+      case 2: FK_SW(2); break;
+      default: FK_SW(1);
+    }
+#undef FK_SW
+    return cudaGetLastError();
+  }
+  const bool sb = K <= SD_KSMEM;
+  const size_t smem = sb ? SD_SMEM_BASES : SD_SMEM;
+#define FK_SCAT(NPV, SB, MA)                                                                       \
+  do {                                                                                             \
+    static bool attr_set[64] = {};                                                                 \
+    int dev = 0;                                                                                   \
+    cudaGetDevice(&dev);                                                                           \
+    if (!attr_set[dev & 63]) { /* one-time per device: keeps graph capture free of it */           \
+      cudaFuncSetAttribute(k_scatter_stable<NPV, SB, MA>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)SD_SMEM_BASES);                                                    \
+      attr_set[dev & 63] = true;                                                                   \
+    }                                                                                              \
+    k_scatter_stable<NPV, SB, MA><<<blocks, SD_T, smem, s>>>(ids, N, K, (int)bpb, last_bits,       \
+                                                              w.table, w.off, w.order);            \
+  } while (0)
+#define FK_SCAT_NP(SB, MA)              \
+  switch (np) {                         \
+    case 1: FK_SCAT(1, SB, MA); break;  \
+    case 2: FK_SCAT(2, SB, MA); break;  \
+    case 3: FK_SCAT(3, SB, MA); break;  \
+    default: FK_SCAT(4, SB, MA);        \
+  }
+  if (sb) {
+    if (match_env) FK_SCAT_NP(true, true) else FK_SCAT_NP(true, false)
+  } else {
+    if (match_env) FK_SCAT_NP(false, true) else FK_SCAT_NP(false, false)
+  }
+#undef FK_SCAT_NP
+#undef FK_SCAT
+  return cudaGetLastError();
+}
+
+// The stable argsort alone (argsort_assignments, sort_inverse.py:67-78):
+// order_out (B*N int32 flat point indices, valid ids only) and the key offsets
+// off_out (B*K+1 int64); the workspace is fk_update's for d = 1.
+cudaError_t launch_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, int32_t* order_out,
+                           int64_t* off_out, void* ws, int num_sms, cudaStream_t s) {
+  const int sms = num_sms < kMaxSms ? num_sms : kMaxSms;
+  UpdateWs w;
+  update_ws_layout(B, N, K, 1, sms, ws, &w);
+  w.order = order_out;
+  w.off = off_out;
+  const int64_t bpb = update_bpb(B, N, K, sms);
+  cudaError_t e;
+  const bool smem_keys = K <= HIST_SMEM_KEYS;
+  if (!smem_keys && (e = cudaMemsetAsync(w.table, 0, (size_t)B * bpb * K * 4, s)) != cudaSuccess)
+    return e;
+  k_hist<<<(unsigned)(B * bpb), 1024, smem_keys ? K * 4 : 0, s>>>(ids, N, K, (int)bpb, w.table, nullptr,
+                                                                  0, nullptr, 0);
+  const int64_t ktiles = (K + 31) / 32;
+  k_colscan<<<(unsigned)(B * ktiles), dim3(32, 32), 0, s>>>(w.table, K, (int)bpb, ktiles, w.hist);
+  k_scan<<<(unsigned)B, 1024, 0, s>>>(w.hist, B, N, K, N, 0, w.off, nullptr, nullptr);
+  return launch_scatter_stable(ids, B, N, K, bpb, w, s);
 }
 
 cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
@@ -985,69 +1148,28 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
                           int64_t* counts, int64_t* merges, void* ws, int num_sms,
                           cudaStream_t s) {
   const int64_t BK = B * K, P = B * N;
-  const int64_t chc = chunk < 1 ? 1 : (chunk > N ? N : chunk);
-  if (const int C = cluster_update_size(dt, B, N, K, d, num_sms)) {
-    return dt == DT_BF16
-               ? launch_cluster_update<__nv_bfloat16>(X, ids, B, N, K, d, chc, accumulate, sums,
-                                                      counts, merges, C, s)
-               : launch_cluster_update<__half>(X, ids, B, N, K, d, chc, accumulate, sums, counts,
-                                               merges, C, s);
-  }
-  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  uint8_t* w = (uint8_t*)ws;
-  int32_t* hist = (int32_t*)w;
-  w += al(BK * 4);
-  int32_t* cursor = (int32_t*)w;
-  w += al(BK * 4);
-  int64_t* off = (int64_t*)w;
-  w += al((BK + 1) * 8);
-  int32_t* order = (int32_t*)w;
-  w += al(P * 4);
-  int32_t* table = (int32_t*)w;  // per-block histograms (shared-histogram path)
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(hist, 0, BK * 4, s)) != cudaSuccess) return e;
-  // sums are cleared inside k_hist (below) unless accumulating
-  const int64_t bpb = update_bpb(B, N, num_sms < kMaxSms ? num_sms : kMaxSms);
+  const int sms = num_sms < kMaxSms ? num_sms : kMaxSms;
+  UpdateWs w;
+  update_ws_layout(B, N, K, d, sms, ws, &w);
+  const int64_t bpb = update_bpb(B, N, K, sms);
   const unsigned blocks = (unsigned)(B * bpb);
+  cudaError_t e;
   const bool smem_keys = K <= HIST_SMEM_KEYS;
-  const size_t hsm = smem_keys ? K * 4 : 0;
-  k_hist<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, hist, table, accumulate ? nullptr : sums,
-                                   BK * d);
+  if (!smem_keys && (e = cudaMemsetAsync(w.table, 0, (size_t)B * bpb * K * 4, s)) != cudaSuccess)
+    return e;
+  // sums are cleared inside k_hist unless accumulating; so are the arrival counters
+  k_hist<<<blocks, 1024, smem_keys ? K * 4 : 0, s>>>(ids, N, K, (int)bpb, w.table,
+                                                     accumulate ? nullptr : sums, BK * d, w.arrive, BK);
+  const int64_t ktiles = (K + 31) / 32;
+  k_colscan<<<(unsigned)(B * ktiles), dim3(32, 32), 0, s>>>(w.table, K, (int)bpb, ktiles, w.hist);
   const int64_t ch = chunk < 1 ? 1 : (chunk > N ? N : chunk);
-  k_scan<<<(unsigned)B, 1024, 0, s>>>(hist, B, N, K, ch, accumulate, off, cursor, counts, merges);
-  static int staged_env = -1;  // FK_UPDATE_SCATTER=block: the unstaged block scatter (A/B)
-  if (staged_env < 0) {
-    const char* e = getenv("FK_UPDATE_SCATTER");
-    staged_env = (e && e[0] == 'b') ? 0 : 1;
-  }
-  // staged only for block ranges of >= 6K points: shorter ranges pay the
-  // per-sub-tile scan and barriers without longer runs (3.5K-point ranges:
-  // 72 -> 74 us at config 2, 62 -> 66 us at config 4); with the 8K-point
-  // blocks of update_bpb it is 3-4% faster there (profiles/r01_ab_scatter_min_range.txt).
-  // update_bpb gives ranges in (4K, 8K] unless the wave cap binds, so the
-  // threshold sits inside that interval rather than at its top.
-  if (smem_keys && K <= SC_KMAX && staged_env && (N + bpb - 1) / bpb >= SC_MIN_RANGE) {
-    const size_t ssm = (3 * K + SC_S) * 4;
-    static int attr_dev_mask = 0;  // one-time per device (keeps graph capture free of it)
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!(attr_dev_mask & (1 << (dev & 31)))) {
-      cudaFuncSetAttribute(k_scatter_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((3 * SC_KMAX + SC_S) * 4));
-      attr_dev_mask |= 1 << (dev & 31);
-    }
-    k_scatter_staged<<<blocks, 1024, ssm, s>>>(ids, B, N, K, (int)bpb, table, cursor, order);
-  } else if (smem_keys)
-    k_scatter_block<<<blocks, 1024, hsm, s>>>(ids, B, N, K, (int)bpb, table, cursor, order);
-  else
-    k_scatter<<<(unsigned)((P + 511) / 512 < num_sms * 4 ? (P + 511) / 512 : num_sms * 4), 512, 0,
-                s>>>(ids, B, N, K, cursor, order);
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_scan<<<(unsigned)B, 1024, 0, s>>>(w.hist, B, N, K, ch, accumulate, w.off, counts, merges);
+  if ((e = launch_scatter_stable(ids, B, N, K, bpb, w, s)) != cudaSuccess) return e;
   switch (dt) {
-    case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, order, off, BK, P, d, sums, num_sms, s, ids, N, K);
-    case DT_F16: return dispatch_segsum<__half, float>(X, order, off, BK, P, d, sums, num_sms, s, ids, N, K);
-    case DT_F32: return dispatch_segsum<float, double>(X, order, off, BK, P, d, sums, num_sms, s, ids, N, K);
-    default: return dispatch_segsum<double, double>(X, order, off, BK, P, d, sums, num_sms, s, ids, N, K);
+    case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, w, BK, P, d, sums, sms, s, ids, N, K);
+    case DT_F16: return dispatch_segsum<__half, float>(X, w, BK, P, d, sums, sms, s, ids, N, K);
+    case DT_F32: return dispatch_segsum<float, double>(X, w, BK, P, d, sums, sms, s, ids, N, K);
+    default: return dispatch_segsum<double, double>(X, w, BK, P, d, sums, sms, s, ids, N, K);
   }
 }
 

@@ -127,6 +127,24 @@ def update(x: torch.Tensor, ids: torch.Tensor, clusters: int, chunk: int | None 
     return sums, counts
 
 
+def argsort(ids: torch.Tensor, clusters: int):
+    """Stable device counting sort of (B,N) int32 ids: (order int32 (B*N,) flat
+    point indices grouped by key b*K + id, offsets int64 (B*K+1,))."""
+    dev = _require_cuda(ids)
+    ids = ids.contiguous()
+    B, n = ids.shape
+    K = int(clusters)
+    order = torch.empty((B * n,), dtype=torch.int32, device=dev)
+    offsets = torch.empty((B * K + 1,), dtype=torch.int64, device=dev)
+    L = N.lib()
+    need = L.fk_update_workspace(N.FK_F32, B, n, K, 1)
+    ws = _ws.get(dev, need, "update")
+    st = L.fk_argsort(ids.data_ptr(), B, n, K, order.data_ptr(), offsets.data_ptr(), ws.data_ptr(),
+                      ws.numel(), _stream(dev))
+    N.check(st, "fk_argsort")
+    return order, offsets
+
+
 def normalize(sums: torch.Tensor, counts: torch.Tensor, prev: torch.Tensor,
               out: torch.Tensor | None = None, operand_dtype: torch.dtype | None = None,
               operand_out: torch.Tensor | None = None, empty: torch.Tensor | None = None,

@@ -207,3 +207,81 @@ def test_objective(ops):
     o = ops.objective(m.cuda())
     ref = np.array([np.sum(m[b].numpy(), dtype=np.float64) for b in range(3)])
     np.testing.assert_allclose(o.cpu().numpy(), ref, rtol=1e-12)
+
+
+# ----------------------------------------------------------- stable sort / determinism
+def test_device_argsort_hand_cases():
+    """The reference's counting_sort known answers (test_sort_inverse.py:26-42)."""
+    import paper_2603_09229_b200 as fk
+
+    idx, a_sorted = fk.argsort_assignments(fk.Assignments(torch.tensor([[2, 0, 1, 0]], dtype=torch.int32).cuda()), 3)
+    assert idx.order[0].tolist() == [1, 3, 2, 0]
+    assert a_sorted[0].tolist() == [0, 0, 1, 2]
+    idx, _ = fk.argsort_assignments(fk.Assignments(torch.tensor([[1, 1, 0, 1, 0]], dtype=torch.int32).cuda()), 2)
+    assert idx.order[0].tolist() == [2, 4, 0, 1, 3]
+
+
+@pytest.mark.parametrize("B,N,K,skew", [
+    (1, 5_000_003, 4096, False),   # several sub-tiles per block, 2 radix passes
+    (64, 16384, 256, False),       # config 4: one pass, many batch elements
+    (2, 300_001, 1, False),        # K = 1
+    (1, 200_000, 65536, False),    # global-row histograms, 2 passes
+    (1, 400_000, 70000, True),     # 3 passes, skewed: one giant run + a long tail
+    (3, 9000, 300, True),
+])
+def test_device_argsort_is_numpy_stable_argsort(ops, B, N, K, skew):
+    g = torch.Generator().manual_seed(N + K)
+    if skew:  # Zipf-like: most points in a few clusters
+        ids = (torch.rand((B, N), generator=g) ** 6 * K).to(torch.int32).clamp_(max=K - 1)
+    else:
+        ids = torch.randint(0, K, (B, N), generator=g, dtype=torch.int32)
+    order, off = ops.argsort(ids.cuda(), K)
+    ref = np.concatenate([np.argsort(ids[b].numpy(), kind="stable") + b * N for b in range(B)])
+    assert np.array_equal(order.cpu().numpy(), ref)
+    cnt = np.stack([np.bincount(ids[b].numpy(), minlength=K) for b in range(B)]).reshape(-1)
+    assert np.array_equal(off.cpu().numpy(), np.concatenate([[0], np.cumsum(cnt)]))
+
+
+def test_device_argsort_skips_out_of_range_ids(ops):
+    ids = torch.tensor([[3, -1, 0, 7, 1, 0, 2]], dtype=torch.int32)
+    order, off = ops.argsort(ids.cuda(), 4)
+    assert off.cpu().tolist() == [0, 2, 3, 4, 5]
+    assert order.cpu().tolist()[:5] == [2, 5, 4, 6, 0]
+
+
+@pytest.mark.parametrize("B,N,K,d,dtype", [
+    (1, 4_000_000, 4096, 128, torch.bfloat16),
+    (64, 16384, 256, 64, torch.float16),
+    (1, 1 << 20, 1024, 128, torch.float64),
+    (2, 700_001, 3001, 32, torch.float32),
+    (1, 300_000, 20000, 16, torch.bfloat16),
+])
+def test_update_is_deterministic(ops, B, N, K, d, dtype):
+    """Two updates of the same (X, ids) give the same bits -- sums included,
+    for every dtype (stable order + slice-ordered boundary merges; no float
+    atomics anywhere on the path)."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = (torch.randn((B, N, d), device="cuda", generator=g) * 4 + 1).to(dtype)
+    ids = torch.randint(0, K, (B, N), device="cuda", generator=g, dtype=torch.int32)
+    s1, c1 = ops.update(x, ids, K, N)
+    s1 = s1.clone()
+    c1 = c1.clone()
+    junk = torch.randint(0, K, (B, N), device="cuda", generator=g, dtype=torch.int32)
+    ops.update(x, junk, K, N)  # reuse the workspace with other data in between
+    s2, c2 = ops.update(x, ids, K, N)
+    assert torch.equal(c1, c2)
+    assert torch.equal(s1.view(torch.int64), s2.view(torch.int64))
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 37, 4096])
+def test_device_argsort_stable_under_heavy_collisions(ops, K):
+    """Many lanes of a warp step share an id: the ranks must still follow the
+    point index (the stable order), on every repetition."""
+    g = torch.Generator().manual_seed(K)
+    ids = torch.randint(0, K, (2, 600_000), generator=g, dtype=torch.int32)
+    ids[:, 1000:40000] = 0  # long single-id stretches
+    ref = np.concatenate([np.argsort(ids[b].numpy(), kind="stable") + b * ids.shape[1] for b in range(2)])
+    idc = ids.cuda()
+    for _ in range(10):
+        order, _ = ops.argsort(idc, K)
+        assert np.array_equal(order.cpu().numpy(), ref)
