@@ -90,12 +90,20 @@ FK_API int fk_device_supported(int device);
  *               is OR-ed with 1 if any id differs from idx_prev
  *               (the lloyd_run repeat test, pipeline.py:137)
  * FK_F32/FK_F64 always run the exact mirror (bitwise equal to the
- * reference); FK_BF16/FK_F16 run the tcgen05 kernel for d <= 128 and a
- * CUDA-core kernel otherwise.                                                */
+ * reference); FK_BF16/FK_F16 run the tcgen05 kernel for d <= 256 (rows of
+ * 16-byte multiples) and a CUDA-core kernel otherwise.
+ * bias      : optional (FK_BF16/FK_F16 only) the tensor-core bias operand of C,
+ *             (B, fk_assign_bias_rows(K), 16) bf16 = [hi, mid, lo, 0...] split of
+ *             ||c||^2/2, as written by fk_normalize(bias_out) or fk_assign_bias;
+ *             NULL computes it inside the call (one extra pass over C).          */
 FK_API size_t fk_assign_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d);
-FK_API fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B, int64_t N, int64_t K,
-                    int64_t d, int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
-                    int32_t* changed_flag, void* workspace, size_t workspace_bytes, void* stream);
+FK_API int64_t fk_assign_bias_rows(int64_t K);
+FK_API fk_status fk_assign_bias(fk_dtype dt, const void* C, int64_t B, int64_t K, int64_t d,
+                                void* bias_out, void* stream);
+FK_API fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B,
+                           int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
+                           const int32_t* idx_prev, int32_t* changed_flag, void* workspace,
+                           size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------- update
  * Per-cluster sums (f64) and counts (int64) from (X, ids) by a device stable
@@ -136,7 +144,10 @@ FK_API fk_status fk_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K,
 FK_API fk_status fk_normalize(fk_dtype master_dt, const double* sums, const int64_t* counts,
                        const void* prev, void* out, fk_dtype operand_dt, void* operand_out,
                        uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K, int64_t d,
-                       void* stream);
+                       void* bias_out, void* stream);
+/* bias_out (optional, with a bf16/fp16 operand_out): also write the next
+ * assign's bias operand of operand_out (see fk_assign), bitwise what
+ * fk_assign_bias would compute.                                              */
 
 /* Exact row norms in the data precision (f32/f64), core.row_norms semantics. */
 FK_API fk_status fk_row_norms(fk_dtype dt, const void* M, int64_t rows, int64_t d, void* out,
@@ -147,6 +158,19 @@ FK_API fk_status fk_row_norms(fk_dtype dt, const void* M, int64_t rows, int64_t 
  * reduction; for f32 min_dists every f64 partial is exact in practice, so it
  * equals numpy's np.sum(m, dtype=float64) bit for bit.                      */
 FK_API size_t fk_objective_workspace(int64_t B, int64_t N);
+/* The two halves of fk_objective for the device-resident loop:
+ * fk_objective_partials writes B * ceil(N / 8192) fixed-order partials;
+ * fk_loop_tail (one launch at the end of an iteration) reduces them into
+ * objective[b] (bitwise fk_objective's result) and, when history is given,
+ * into history[*history_row * B + b] (then ++*history_row: the row index
+ * lives on the device so a replayed CUDA graph fills successive rows); it
+ * copies [*changed, *max_shift2, *merges] into flags_out[3] (f64) and clears
+ * the three for the next iteration.                                          */
+FK_API fk_status fk_objective_partials(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N,
+                                       double* partials, void* stream);
+FK_API fk_status fk_loop_tail(const double* partials, int64_t B, int64_t N, double* objective,
+                              double* history, int64_t* history_row, int32_t* changed,
+                              double* max_shift2, int64_t* merges, double* flags_out, void* stream);
 FK_API fk_status fk_objective(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N, double* out,
                        void* workspace, size_t workspace_bytes, void* stream);
 

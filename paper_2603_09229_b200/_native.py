@@ -36,8 +36,12 @@ def _declare(L):
     L.fk_device_supported.argtypes = [ctypes.c_int]
     L.fk_assign_workspace.restype = SZ
     L.fk_assign_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
+    L.fk_assign_bias_rows.restype = I64
+    L.fk_assign_bias_rows.argtypes = [I64]
+    L.fk_assign_bias.restype = ctypes.c_int
+    L.fk_assign_bias.argtypes = [ctypes.c_int, P, I64, I64, I64, P, P]
     L.fk_assign.restype = ctypes.c_int
-    L.fk_assign.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]
+    L.fk_assign.argtypes = [ctypes.c_int, P, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]
     L.fk_update_workspace.restype = SZ
     L.fk_update_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
     L.fk_update.restype = ctypes.c_int
@@ -45,7 +49,11 @@ def _declare(L):
     L.fk_argsort.restype = ctypes.c_int
     L.fk_argsort.argtypes = [P, I64, I64, I64, P, P, P, SZ, P]
     L.fk_normalize.restype = ctypes.c_int
-    L.fk_normalize.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, P, P, P, I64, I64, I64, P]
+    L.fk_normalize.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, P, P, P, I64, I64, I64, P, P]
+    L.fk_objective_partials.restype = ctypes.c_int
+    L.fk_objective_partials.argtypes = [ctypes.c_int, P, I64, I64, P, P]
+    L.fk_loop_tail.restype = ctypes.c_int
+    L.fk_loop_tail.argtypes = [P, I64, I64, P, P, P, P, P, P, P, P]
     L.fk_row_norms.restype = ctypes.c_int
     L.fk_row_norms.argtypes = [ctypes.c_int, P, I64, I64, P, P]
     L.fk_objective_workspace.restype = SZ
@@ -73,8 +81,9 @@ def _declare(L):
 
 EXPORTED = (
     "fk_version", "fk_status_string", "fk_last_cuda_error", "fk_device_supported",
-    "fk_assign_workspace", "fk_assign", "fk_update_workspace", "fk_update", "fk_argsort", "fk_normalize",
-    "fk_row_norms", "fk_objective_workspace", "fk_objective", "fk_scatter",
+    "fk_assign_workspace", "fk_assign_bias_rows", "fk_assign_bias", "fk_assign", "fk_update_workspace",
+    "fk_update", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
+    "fk_objective_partials", "fk_loop_tail", "fk_scatter",
     "fk_stats_pack", "fk_merges_from_counts", "fk_kmeanspp_workspace", "fk_kmeanspp",
     "fk_kmeanspp_init", "fk_kmeanspp_sweep", "fk_kmeanspp_select",
 )

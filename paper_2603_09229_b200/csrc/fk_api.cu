@@ -98,8 +98,17 @@ size_t fk_assign_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t
   return al256((size_t)B * N * es) + al256((size_t)B * K * es);
 }
 
-fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B, int64_t N, int64_t K,
-                    int64_t d, int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+int64_t fk_assign_bias_rows(int64_t K) { return K < 1 ? 0 : fk::assign_tc_kpad(K); }
+
+fk_status fk_assign_bias(fk_dtype dt, const void* C, int64_t B, int64_t K, int64_t d, void* bias_out,
+                         void* stream) {
+  if (!is_lowp(dt) || !C || !bias_out || B < 1 || K < 1 || d < 1) return FK_EINVAL;
+  return cuda_status(fk::launch_cn_ext(dt, C, B, K, d, fk::assign_tc_kpad(K), bias_out,
+                                       reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B, int64_t N,
+                    int64_t K, int64_t d, int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
                     int32_t* changed_flag, void* ws, size_t ws_bytes, void* stream) {
   if (!valid_dt(dt) || !shape_ok(B, N, K, d)) return FK_EINVAL;
   if (!X || !C || !idx_out || !mind_out) return FK_EINVAL;
@@ -116,7 +125,10 @@ fk_status fk_assign(fk_dtype dt, const void* X, const void* C, int64_t B, int64_
       const int fmt = dt == FK_BF16 ? 1 : 0;
       void* ext = nullptr;
       fk_status st;
-      if (fk::assign_tc_uses_ext(fmt)) {
+      if (fk::assign_tc_uses_ext(fmt) && bias) {
+        ext = const_cast<void*>(bias);  // precomputed by fk_normalize / fk_assign_bias
+        st = FK_OK;
+      } else if (fk::assign_tc_uses_ext(fmt)) {
         ext = reinterpret_cast<uint8_t*>(ws) + al256((size_t)B * kpad * 4);
         st = cuda_status(fk::launch_cn_ext(dt, C, B, K, d, kpad, ext, s));
       } else {
@@ -179,12 +191,32 @@ fk_status fk_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, int32_
 fk_status fk_normalize(fk_dtype master_dt, const double* sums, const int64_t* counts,
                        const void* prev, void* out, fk_dtype operand_dt, void* operand_out,
                        uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K, int64_t d,
-                       void* stream) {
+                       void* bias_out, void* stream) {
   if (master_dt != FK_F32 && master_dt != FK_F64) return FK_EINVAL;
   if (operand_out && !valid_dt(operand_dt)) return FK_EINVAL;
   if (!sums || !counts || !prev || !out || B < 1 || K < 1 || d < 1) return FK_EINVAL;
+  if (bias_out && !(operand_out && is_lowp(operand_dt))) return FK_EINVAL;
   return cuda_status(fk::launch_normalize(master_dt, sums, counts, prev, out, operand_dt,
-                                          operand_out, empty_mask, max_shift2, B, K, d,
+                                          operand_out, empty_mask, max_shift2, B, K, d, bias_out,
+                                          fk::assign_tc_kpad(K),
+                                          reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_objective_partials(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N,
+                                double* partials, void* stream) {
+  if (!valid_dt(mind_dt) || !mind || !partials || B < 1 || N < 1) return FK_EINVAL;
+  return cuda_status(fk::launch_objective_partials(mind_dt == FK_F64 ? 1 : 0, mind, B, N, partials,
+                                                   reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_loop_tail(const double* partials, int64_t B, int64_t N, double* objective,
+                       double* history, int64_t* history_row, int32_t* changed, double* max_shift2,
+                       int64_t* merges, double* flags_out, void* stream) {
+  if (!partials || !objective || !changed || !max_shift2 || !merges || !flags_out || B < 1 || N < 1)
+    return FK_EINVAL;
+  if (history && !history_row) return FK_EINVAL;
+  return cuda_status(fk::launch_loop_tail(partials, B, N, objective, history, history_row, changed,
+                                          max_shift2, merges, flags_out,
                                           reinterpret_cast<cudaStream_t>(stream)));
 }
 

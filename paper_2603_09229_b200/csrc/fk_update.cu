@@ -105,8 +105,10 @@ __device__ __forceinline__ void for_each_id(const int32_t* __restrict__ ids, int
 __global__ void __launch_bounds__(1024)
     k_hist(const int32_t* __restrict__ ids, int64_t N, int64_t K, int bpb, int32_t* __restrict__ table,
            double* __restrict__ zero_sums, int64_t zero_n, int32_t* __restrict__ arrive,
-           int64_t arrive_n) {
+           int64_t arrive_n, int32_t* __restrict__ inval) {
   extern __shared__ int32_t sh[];
+  __shared__ int32_t s_bad;
+  if (threadIdx.x == 0) s_bad = 0;
   {
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -125,12 +127,15 @@ __global__ void __launch_bounds__(1024)
   int64_t b, lo, hi;
   range_of(N, bpb, b, lo, hi);
   int32_t* trow = table + (int64_t)blockIdx.x * K;
-  if (use_smem) {
+  if (use_smem)
     for (int64_t k = threadIdx.x; k < K; k += blockDim.x) sh[k] = 0;
-    __syncthreads();
-  }
+  __syncthreads();
+  int bad = 0;
   for_each_id(ids, lo, hi, [&](int64_t, int32_t id) {
-    if (id < 0 || id >= K) return;  // not a cluster: left out of the sort (and the sums)
+    if (id < 0 || id >= K) {  // not a cluster: left out of the sort (and the sums)
+      ++bad;
+      return;
+    }
     if (use_smem) {
       atomicAdd(&sh[id], 1);
     } else {
@@ -138,10 +143,12 @@ __global__ void __launch_bounds__(1024)
       if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&trow[id], __popc(peers));
     }
   });
-  if (use_smem) {
-    __syncthreads();
+  for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&s_bad, bad);
+  __syncthreads();
+  if (use_smem)
     for (int64_t k = threadIdx.x; k < K; k += blockDim.x) trow[k] = sh[k];
-  }
+  if (inval && threadIdx.x == 0) inval[blockIdx.x] = s_bad;
 }
 
 // ----------------------------------------------------------------- colscan
@@ -510,34 +517,133 @@ __global__ void __launch_bounds__(SD_T, 1)
 // ids with 32 warps per SM, against ~65 for a conflicting shared atomic).
 // The ids of SW_U steps are loaded together.  The u16 table needs block
 // ranges < 2^16 points (update_bpb).
-constexpr int SW_KMAX = 32766;            // W * (K + 2) * 2 bytes <= 64 KB
+constexpr int SW_KMAX = 16384;            // W * (K + 2) * 2 bytes <= 64 KB, + K * 8 bytes of bases
 constexpr int SW_TABLE_BYTES = 65536;
 constexpr int SW_U = 8;                   // steps in flight per warp
+constexpr int SW_COLS_BPB = 16;           // up to this many blocks per batch element: no k_colscan
 
-template <int W>
+// Exclusive scan, in place, of n int32 values in shared memory by the whole
+// block (T threads, contiguous chunks per thread); returns the total.
+template <int T>
+__device__ int sw_block_scan(int32_t* v, int n, int32_t* wsum) {
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  constexpr int NW = T / 32;
+  const int per = (n + T - 1) / T;
+  const int i0 = t * per < n ? t * per : n;
+  const int i1 = i0 + per < n ? i0 + per : n;
+  int sum = 0;
+  for (int i = i0; i < i1; ++i) sum += v[i];
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < NW ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += u;
+    }
+    if (lane < NW) wsum[lane] = x;
+  }
+  __syncthreads();
+  int run = incl - sum + (w ? wsum[w - 1] : 0);
+  const int total = wsum[NW - 1];
+  for (int i = i0; i < i1; ++i) {
+    const int c = v[i];
+    v[i] = run;
+    run += c;
+  }
+  __syncthreads();
+  return total;
+}
+
+// COLS: the block also does the column prefix over its batch element's bpb
+// block rows (small bpb; otherwise k_colscan did it and wrote the totals to
+// `hist`).  Every block then derives the key offsets of its batch element
+// itself (exclusive scan of the totals + the batch element's base, b*N minus
+// the ids outside [0, K) of earlier elements); block 0 of each batch element
+// also publishes off[], the int64 counts and the reference merge count -- no
+// separate scan kernel.
+template <int W, bool COLS>
 __global__ void __launch_bounds__(W * 32)
     k_scatter_warp(const int32_t* __restrict__ ids, int64_t N, int64_t K, int bpb,
-                   const int32_t* __restrict__ table, const int64_t* __restrict__ off,
+                   const int32_t* __restrict__ table, const int32_t* __restrict__ hist,
+                   const int32_t* __restrict__ inval, int64_t B, int64_t chunk, int accumulate,
+                   int64_t* __restrict__ off, int64_t* __restrict__ counts, int64_t* __restrict__ merges,
                    int32_t* __restrict__ order) {
   extern __shared__ __align__(16) uint8_t sw_sm[];
   // rows padded to K + 2 entries: the W rows of one key fall in different banks
   const int KS = (int)K + 2;
   uint16_t* tab = reinterpret_cast<uint16_t*>(sw_sm);                           // W * KS
   int32_t* kbase = reinterpret_cast<int32_t*>(sw_sm + ((W * KS * 2 + 15) & ~15));  // K
+  int32_t* kpre = kbase + K;                                                      // K
   uint32_t* tab32 = reinterpret_cast<uint32_t*>(sw_sm);
+  __shared__ int32_t wsum[32];
+  __shared__ unsigned long long s_bad, s_mg;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t Ku = (uint32_t)K;
   int64_t b, lo, hi;
   range_of(N, bpb, b, lo, hi);
+  const int j = (int)(blockIdx.x - b * bpb);
   const int32_t* trow = table + (int64_t)blockIdx.x * K;
-  const int64_t* offb = off + b * K;
+  if (t == 0) {
+    s_bad = 0;
+    s_mg = 0;
+  }
   for (int i = t; i < W * KS / 2; i += W * 32) tab32[i] = 0u;
-  for (int k = t; k < K; k += W * 32) kbase[k] = (int32_t)(offb[k] + trow[k]);  // flat < 2^31
+  // block base inside each key's run (kbase) and the key totals (kpre)
+  for (int k = t; k < K; k += W * 32) {
+    if (COLS) {
+      const int32_t* col = table + (int64_t)b * bpb * K + k;
+      int32_t run = 0, tot = 0;
+      for (int r = 0; r < bpb; ++r) {
+        const int32_t c = col[(int64_t)r * K];
+        run += r < j ? c : 0;
+        tot += c;
+      }
+      kbase[k] = run;
+      kpre[k] = tot;
+    } else {
+      kbase[k] = trow[k];
+      kpre[k] = hist[b * K + k];
+    }
+  }
+  {  // batch base: b*N minus the invalid ids of the earlier batch elements
+    unsigned long long bad = 0;
+    for (int64_t i = t; i < b * bpb; i += W * 32) bad += (unsigned long long)inval[i];
+    for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    __syncthreads();
+    if (lane == 0 && bad) atomicAdd(&s_bad, bad);
+  }
+  // key offsets relative to the batch element: exclusive prefix of the totals
+  const int32_t total = sw_block_scan<W * 32>(kpre, (int)K, wsum);
+  const int64_t base_b = b * N - (int64_t)s_bad;
+  if (j == 0) {  // publish off / counts / merges for this batch element
+    unsigned long long mg = 0;
+    const uint32_t ch = (uint32_t)chunk;
+    for (int k = t; k < K; k += W * 32) {
+      const int32_t s0 = kpre[k];
+      const int32_t c = (k + 1 < K ? kpre[k + 1] : total) - s0;
+      off[b * K + k] = base_b + s0;
+      if (counts) counts[b * K + k] = accumulate ? counts[b * K + k] + c : c;
+      if (c > 0) mg += (unsigned long long)(((uint32_t)(s0 + c) - 1) / ch - (uint32_t)s0 / ch + 1);
+    }
+    if (b == B - 1 && t == 0) off[B * K] = base_b + total;
+    for (int o = 16; o; o >>= 1) mg += __shfl_xor_sync(0xffffffffu, mg, o);
+    if (lane == 0 && mg) atomicAdd(&s_mg, mg);
+  }
+  for (int k = t; k < K; k += W * 32) kbase[k] += (int32_t)(base_b + kpre[k]);  // flat < 2^31
   // this warp's part [a, e) of the block range
   const int n = (int)(hi - lo);
   const int a = (int)((int64_t)n * w / W), e = (int)((int64_t)n * (w + 1) / W);
   const int32_t* idw = ids + lo;
   __syncthreads();
+  if (j == 0 && merges && t == 0 && s_mg) atomicAdd((unsigned long long*)merges, s_mg);
   // 1. per-warp counts (fire-and-forget shared atomics on packed u16 pairs)
   for (int p0 = a; p0 < e; p0 += 32 * SW_U) {
     uint32_t id[SW_U];
@@ -976,6 +1082,7 @@ struct UpdateWs {
   int32_t* order;
   int32_t* arrive;
   double* part;
+  int32_t* inval;
 };
 
 static size_t update_ws_layout(int64_t B, int64_t N, int64_t K, int64_t d, int num_sms, void* base,
@@ -984,12 +1091,13 @@ static size_t update_ws_layout(int64_t B, int64_t N, int64_t K, int64_t d, int n
   const int64_t BK = B * K, P = B * N;
   const int64_t bpb = update_bpb(B, N, K, num_sms);
   const int64_t slices = (P + segsum_slice(P, num_sms) - 1) / segsum_slice(P, num_sms);
-  const size_t sz[6] = {al((size_t)B * bpb * K * 4), al((size_t)BK * 4), al((size_t)(BK + 1) * 8),
-                        al((size_t)P * 4), al((size_t)BK * 4), al((size_t)slices * 2 * d * 8)};
+  const size_t sz[7] = {al((size_t)B * bpb * K * 4), al((size_t)BK * 4), al((size_t)(BK + 1) * 8),
+                        al((size_t)P * 4),           al((size_t)BK * 4), al((size_t)slices * 2 * d * 8),
+                        al((size_t)B * bpb * 4)};
   size_t total = 0;
   uint8_t* p = static_cast<uint8_t*>(base);
-  void* ptrs[6];
-  for (int i = 0; i < 6; ++i) {
+  void* ptrs[7];
+  for (int i = 0; i < 7; ++i) {
     ptrs[i] = p ? p + total : nullptr;
     total += sz[i];
   }
@@ -1000,6 +1108,7 @@ static size_t update_ws_layout(int64_t B, int64_t N, int64_t K, int64_t d, int n
     ws->order = (int32_t*)ptrs[3];
     ws->arrive = (int32_t*)ptrs[4];
     ws->part = (double*)ptrs[5];
+    ws->inval = (int32_t*)ptrs[6];
   }
   return total;
 }
@@ -1044,8 +1153,20 @@ static cudaError_t dispatch_segsum(const void* X, const UpdateWs& w, int64_t BK,
   return cudaGetLastError();
 }
 
+static bool scatter_is_warp(int64_t K) {
+  static int radix_env = -1;  // FK_SCATTER_RADIX=1: the block radix sort for every K (A/B)
+  if (radix_env < 0) {
+    const char* e = getenv("FK_SCATTER_RADIX");
+    radix_env = (e && e[0] == '1') ? 1 : 0;
+  }
+  return K <= SW_KMAX && !radix_env;
+}
+
+// The stable scatter.  The warp-table kernel also does the key scan (off,
+// counts, merges); the radix kernel needs k_scan to have run.
 static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t N, int64_t K,
-                                         int64_t bpb, const UpdateWs& w, cudaStream_t s) {
+                                         int64_t bpb, const UpdateWs& w, int64_t chunk, int accumulate,
+                                         int64_t* counts, int64_t* merges, cudaStream_t s) {
   int bits = 1;
   while (bits < 31 && ((K - 1) >> bits) != 0) ++bits;
   const int np = (bits + 7) / 8;
@@ -1056,26 +1177,31 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
     match_env = (e && e[0] == '1') ? 1 : 0;
   }
   const unsigned blocks = (unsigned)(B * bpb);
-  static int radix_env = -1;  // FK_SCATTER_RADIX=1: the block radix sort for every K (A/B)
-  if (radix_env < 0) {
-    const char* e = getenv("FK_SCATTER_RADIX");
-    radix_env = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (K <= SW_KMAX && !radix_env) {
+  if (scatter_is_warp(K)) {
     int W = 32;
     while (W > 1 && (int64_t)W * (K + 2) * 2 > SW_TABLE_BYTES) W >>= 1;
-    const size_t smem = (size_t)((W * (K + 2) * 2 + 15) & ~15) + (size_t)K * 4;
-#define FK_SW(WV)                                                                                  \
+    const size_t smem = (size_t)((W * (K + 2) * 2 + 15) & ~15) + (size_t)K * 8;
+    const bool cols = bpb <= SW_COLS_BPB;
+#define FK_SW2(WV, CV)                                                                             \
   do {                                                                                             \
     static bool attr_set[64] = {};                                                                 \
     int dev = 0;                                                                                   \
     cudaGetDevice(&dev);                                                                           \
-    if (!attr_set[dev & 63]) {                                                                     \
-      cudaFuncSetAttribute(k_scatter_warp<WV>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                           SW_TABLE_BYTES + SW_KMAX * 4 + 16);  /* the largest table + bases */                                     \
+    if (!attr_set[dev & 63]) { /* the largest table + bases */                                     \
+      cudaFuncSetAttribute(k_scatter_warp<WV, CV>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
+                           SW_TABLE_BYTES + SW_KMAX * 8 + 16);                                     \
       attr_set[dev & 63] = true;                                                                   \
     }                                                                                              \
-    k_scatter_warp<WV><<<blocks, WV * 32, smem, s>>>(ids, N, K, (int)bpb, w.table, w.off, w.order); \
+    k_scatter_warp<WV, CV><<<blocks, WV * 32, smem, s>>>(ids, N, K, (int)bpb, w.table, w.hist,     \
+                                                         w.inval, B, chunk, accumulate, w.off,     \
+                                                         counts, merges, w.order);                 \
+  } while (0)
+#define FK_SW(WV)        \
+  do {                   \
+    if (cols)            \
+      FK_SW2(WV, true);  \
+    else                 \
+      FK_SW2(WV, false); \
   } while (0)
     switch (W) {
       case 32: FK_SW(32); break;
@@ -1086,6 +1212,7 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
       default: FK_SW(1);
     }
 #undef FK_SW
+#undef FK_SW2
     return cudaGetLastError();
   }
   const bool sb = K <= SD_KSMEM;
@@ -1120,6 +1247,21 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
   return cudaGetLastError();
 }
 
+// After k_hist: the column prefix (k_colscan, unless the warp scatter does it
+// itself), the key scan (inside the warp scatter; k_scan for the radix one)
+// and the stable scatter.
+static cudaError_t launch_sort_passes(const int32_t* ids, int64_t B, int64_t N, int64_t K, int64_t bpb,
+                                      const UpdateWs& w, int64_t chunk, int accumulate, int64_t* counts,
+                                      int64_t* merges, cudaStream_t s) {
+  const bool warp = scatter_is_warp(K);
+  if (!(warp && bpb <= SW_COLS_BPB)) {
+    const int64_t ktiles = (K + 31) / 32;
+    k_colscan<<<(unsigned)(B * ktiles), dim3(32, 32), 0, s>>>(w.table, K, (int)bpb, ktiles, w.hist);
+  }
+  if (!warp) k_scan<<<(unsigned)B, 1024, 0, s>>>(w.hist, B, N, K, chunk, accumulate, w.off, counts, merges);
+  return launch_scatter_stable(ids, B, N, K, bpb, w, chunk, accumulate, counts, merges, s);
+}
+
 // The stable argsort alone (argsort_assignments, sort_inverse.py:67-78):
 // order_out (B*N int32 flat point indices, valid ids only) and the key offsets
 // off_out (B*K+1 int64); the workspace is fk_update's for d = 1.
@@ -1136,11 +1278,8 @@ cudaError_t launch_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, 
   if (!smem_keys && (e = cudaMemsetAsync(w.table, 0, (size_t)B * bpb * K * 4, s)) != cudaSuccess)
     return e;
   k_hist<<<(unsigned)(B * bpb), 1024, smem_keys ? K * 4 : 0, s>>>(ids, N, K, (int)bpb, w.table, nullptr,
-                                                                  0, nullptr, 0);
-  const int64_t ktiles = (K + 31) / 32;
-  k_colscan<<<(unsigned)(B * ktiles), dim3(32, 32), 0, s>>>(w.table, K, (int)bpb, ktiles, w.hist);
-  k_scan<<<(unsigned)B, 1024, 0, s>>>(w.hist, B, N, K, N, 0, w.off, nullptr, nullptr);
-  return launch_scatter_stable(ids, B, N, K, bpb, w, s);
+                                                                  0, nullptr, 0, w.inval);
+  return launch_sort_passes(ids, B, N, K, bpb, w, N, 0, nullptr, nullptr, s);
 }
 
 cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
@@ -1159,12 +1298,11 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
     return e;
   // sums are cleared inside k_hist unless accumulating; so are the arrival counters
   k_hist<<<blocks, 1024, smem_keys ? K * 4 : 0, s>>>(ids, N, K, (int)bpb, w.table,
-                                                     accumulate ? nullptr : sums, BK * d, w.arrive, BK);
-  const int64_t ktiles = (K + 31) / 32;
-  k_colscan<<<(unsigned)(B * ktiles), dim3(32, 32), 0, s>>>(w.table, K, (int)bpb, ktiles, w.hist);
+                                                     accumulate ? nullptr : sums, BK * d, w.arrive, BK,
+                                                     w.inval);
   const int64_t ch = chunk < 1 ? 1 : (chunk > N ? N : chunk);
-  k_scan<<<(unsigned)B, 1024, 0, s>>>(w.hist, B, N, K, ch, accumulate, w.off, counts, merges);
-  if ((e = launch_scatter_stable(ids, B, N, K, bpb, w, s)) != cudaSuccess) return e;
+  if ((e = launch_sort_passes(ids, B, N, K, bpb, w, ch, accumulate, counts, merges, s)) != cudaSuccess)
+    return e;
   switch (dt) {
     case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, w, BK, P, d, sums, sms, s, ids, N, K);
     case DT_F16: return dispatch_segsum<__half, float>(X, w, BK, P, d, sums, sms, s, ids, N, K);
@@ -1176,11 +1314,24 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
 // ----------------------------------------------------------------- normalize
 constexpr int NORM_RW = 4;  // centroid rows per warp in k_normalize
 
+FK_DEV float op_to_f32(float v) { return v; }
+FK_DEV float op_to_f32(double v) { return (float)v; }
+FK_DEV float op_to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+FK_DEV float op_to_f32(__half v) { return __half2float(v); }
+
+// c = fl(s / n) per cluster (empty clusters keep prev bitwise), the rounded MMA
+// operand, the empty mask and max ||c_new - c_prev||^2 -- and, for a bf16/fp16
+// operand, the tensor-core bias operand of the NEXT assign: the [hi, mid, lo]
+// bf16 split of ||c||^2 / 2 of the rounded row, with exactly the arithmetic of
+// k_cn_ext (lane-strided fmaf over the columns in increasing order, then an
+// xor-shuffle tree), so precomputing it here leaves the assignment bitwise
+// unchanged and saves the assign its own pass over C.
 template <typename TM, typename TO>
 __global__ void __launch_bounds__(256)
     k_normalize(const double* __restrict__ sums, const int64_t* __restrict__ counts,
                 const TM* __restrict__ prev, TM* __restrict__ out, TO* __restrict__ operand,
-                uint8_t* __restrict__ empty, double* max_shift2, int64_t BK, int64_t d) {
+                uint8_t* __restrict__ empty, double* max_shift2, int64_t BK, int64_t d,
+                __nv_bfloat16* __restrict__ bias, int64_t K, int64_t kpad) {
   __shared__ double wmax[8];
   // NORM_RW rows per warp, every load of a pass (64 columns of each row) issued
   // before the first division so the latencies overlap, and 4x fewer blocks
@@ -1191,10 +1342,12 @@ __global__ void __launch_bounds__(256)
   const int lane = threadIdx.x & 31;
   int64_t cnt[RW];
   double sh[RW];
+  float nrm[RW];
 #pragma unroll
   for (int q = 0; q < RW; ++q) {
     cnt[q] = row0 + q < BK ? counts[row0 + q] : 0;
     sh[q] = 0.0;
+    nrm[q] = 0.f;
   }
   for (int64_t j0 = 0; j0 < d; j0 += 32 * NR) {
     double sv[RW][NR];
@@ -1219,7 +1372,12 @@ __global__ void __launch_bounds__(256)
           TM nv = pv[q][r];
           if (cnt[q] > 0) nv = (TM)(sv[q][r] / (double)cnt[q]);  // correctly rounded, as numpy
           out[o] = nv;
-          if (operand) operand[o] = (TO)(float)nv;
+          if (operand) {
+            const TO ov = (TO)(float)nv;
+            operand[o] = ov;
+            const float f = op_to_f32(ov);
+            nrm[q] = fmaf(f, f, nrm[q]);
+          }
           const double df = (double)nv - (double)pv[q][r];
           sh[q] += df * df;
         }
@@ -1229,6 +1387,23 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int q = 0; q < RW; ++q)
       if (row0 + q < BK) empty[row0 + q] = cnt[q] > 0 ? 0 : 1;
+  }
+  if (bias) {
+#pragma unroll
+    for (int q = 0; q < RW; ++q) {
+      float acc = nrm[q];
+      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (row0 + q < BK && lane < 16) {
+        const int64_t b = (row0 + q) / K, k = row0 + q - b * K;
+        const float v = 0.5f * acc;
+        const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+        const float r1 = v - __bfloat162float(hi);
+        const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+        bias[(b * kpad + k) * 16 + lane] =
+            lane == 0 ? hi : lane == 1 ? mid : lane == 2 ? lo : __float2bfloat16(0.f);
+      }
+    }
   }
   if (max_shift2) {
     double m = 0.0;
@@ -1252,38 +1427,41 @@ __global__ void __launch_bounds__(256)
 template <typename TM>
 static cudaError_t norm_dispatch(int operand_dt, const double* sums, const int64_t* counts,
                                  const void* prev, void* out, void* operand_out, uint8_t* empty,
-                                 double* ms2, int64_t BK, int64_t d, cudaStream_t s) {
+                                 double* ms2, int64_t BK, int64_t d, void* bias, int64_t K,
+                                 int64_t kpad, cudaStream_t s) {
   const int th = 256;
   const int64_t rows_per_block = (th / 32) * NORM_RW;
   const unsigned grid = (unsigned)((BK + rows_per_block - 1) / rows_per_block);
   const TM* pv = (const TM*)prev;
   TM* ov = (TM*)out;
+  __nv_bfloat16* bz = (__nv_bfloat16*)bias;
   if (!operand_out)
-    k_normalize<TM, float><<<grid, th, 0, s>>>(sums, counts, pv, ov, nullptr, empty, ms2, BK, d);
+    k_normalize<TM, float><<<grid, th, 0, s>>>(sums, counts, pv, ov, nullptr, empty, ms2, BK, d,
+                                               nullptr, K, kpad);
   else if (operand_dt == DT_BF16)
-    k_normalize<TM, __nv_bfloat16><<<grid, th, 0, s>>>(sums, counts, pv, ov,
-                                                      (__nv_bfloat16*)operand_out, empty, ms2, BK, d);
+    k_normalize<TM, __nv_bfloat16><<<grid, th, 0, s>>>(sums, counts, pv, ov, (__nv_bfloat16*)operand_out,
+                                                       empty, ms2, BK, d, bz, K, kpad);
   else if (operand_dt == DT_F16)
     k_normalize<TM, __half><<<grid, th, 0, s>>>(sums, counts, pv, ov, (__half*)operand_out, empty,
-                                               ms2, BK, d);
+                                               ms2, BK, d, bz, K, kpad);
   else if (operand_dt == DT_F32)
     k_normalize<TM, float><<<grid, th, 0, s>>>(sums, counts, pv, ov, (float*)operand_out, empty,
-                                              ms2, BK, d);
+                                              ms2, BK, d, nullptr, K, kpad);
   else
     k_normalize<TM, double><<<grid, th, 0, s>>>(sums, counts, pv, ov, (double*)operand_out, empty,
-                                               ms2, BK, d);
+                                               ms2, BK, d, nullptr, K, kpad);
   return cudaGetLastError();
 }
 
 cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* counts,
                              const void* prev, void* out, int operand_dt, void* operand_out,
                              uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,
-                             int64_t d, cudaStream_t s) {
+                             int64_t d, void* bias_out, int64_t bias_kpad, cudaStream_t s) {
   if (master_dt == DT_F64)
     return norm_dispatch<double>(operand_dt, sums, counts, prev, out, operand_out, empty_mask,
-                                 max_shift2, B * K, d, s);
+                                 max_shift2, B * K, d, bias_out, K, bias_kpad, s);
   return norm_dispatch<float>(operand_dt, sums, counts, prev, out, operand_out, empty_mask,
-                              max_shift2, B * K, d, s);
+                              max_shift2, B * K, d, bias_out, K, bias_kpad, s);
 }
 
 // ----------------------------------------------------------------- objective
@@ -1323,6 +1501,73 @@ __global__ void k_obj_final(const double* part, int64_t B, int64_t nblk, double*
     __syncthreads();
   }
   if (threadIdx.x == 0) out[b] = red[0];
+}
+
+// End of one device-resident Lloyd iteration, one launch (LloydEngine): the
+// objective partials reduced in k_obj_final's fixed order into obj[b] and the
+// history row hist[(*it) * B + b] (*it advanced: the row index lives on the
+// device, so a replayed CUDA graph writes successive rows); flags = [changed,
+// max shift^2, merges] for the one host read; the three accumulators cleared
+// for the next iteration.
+__global__ void __launch_bounds__(1024)
+    k_loop_tail(const double* __restrict__ part, int64_t B, int64_t nblk, double* __restrict__ obj,
+                double* __restrict__ hist, int64_t* __restrict__ hist_it, int32_t* changed,
+                double* shift2, int64_t* merges, double* __restrict__ flags) {
+  // warp w reduces batch elements b = w, w + 32, ...: k_obj_final's 256-slot
+  // tree (slot t sums part[t], part[t+256], ... in order; then pairs t, t+s
+  // for s = 128 .. 1), lane l holding slots l + 32j -- the same additions, so
+  // the same double
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t row = hist ? *hist_it : 0;
+  for (int64_t b = w; b < B; b += 32) {
+    double v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      double acc = 0.0;
+      for (int64_t i = lane + 32 * j; i < nblk; i += 256) acc += part[b * nblk + i];
+      v[j] = acc;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) v[j] += v[j + 4];  // s = 128
+#pragma unroll
+    for (int j = 0; j < 2; ++j) v[j] += v[j + 2];  // s = 64
+    v[0] += v[1];                                  // s = 32
+    double x = v[0];
+    for (int s = 16; s; s >>= 1) x += __shfl_down_sync(0xffffffffu, x, s);
+    if (lane == 0) {
+      obj[b] = x;
+      if (hist) hist[row * B + b] = x;
+    }
+  }
+  __syncthreads();  // every warp read *hist_it before it moves
+  if (threadIdx.x == 0) {
+    if (hist) *hist_it = row + 1;
+    flags[0] = (double)*changed;
+    flags[1] = *shift2;
+    flags[2] = (double)*merges;
+    *changed = 0;
+    *shift2 = 0.0;
+    *merges = 0;
+  }
+}
+
+cudaError_t launch_objective_partials(int mind_is_f64, const void* mind, int64_t B, int64_t N,
+                                      double* part, cudaStream_t s) {
+  const int64_t nblk = (N + OBJ_BLOCK - 1) / OBJ_BLOCK;
+  dim3 grid((unsigned)nblk, (unsigned)B);
+  if (mind_is_f64)
+    k_obj_partial<double><<<grid, 256, 0, s>>>((const double*)mind, B, N, nblk, part);
+  else
+    k_obj_partial<float><<<grid, 256, 0, s>>>((const float*)mind, B, N, nblk, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loop_tail(const double* part, int64_t B, int64_t N, double* obj, double* hist,
+                             int64_t* hist_it, int32_t* changed, double* shift2, int64_t* merges,
+                             double* flags, cudaStream_t s) {
+  const int64_t nblk = (N + OBJ_BLOCK - 1) / OBJ_BLOCK;
+  k_loop_tail<<<1, 1024, 0, s>>>(part, B, nblk, obj, hist, hist_it, changed, shift2, merges, flags);
+  return cudaGetLastError();
 }
 
 size_t objective_workspace_bytes(int64_t B, int64_t N) {

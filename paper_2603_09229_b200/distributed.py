@@ -159,6 +159,7 @@ def reseed_farthest_sharded(eng: LloydEngine, lo: int, group=None) -> None:
         eng.master[nxt][b, cid] = rows.to(eng.mdtype)
         if eng.operand is not eng.master:
             eng.operand[nxt][b, cid] = rows.to(eng.dtype)
+    eng._refresh_bias(nxt)
     diff = eng.master[nxt].double() - eng.master[eng.cur].double()
     eng.shift2.copy_((diff * diff).sum(-1).max())
 

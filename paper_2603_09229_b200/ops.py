@@ -60,14 +60,29 @@ def _require_cuda(*ts):
     return dev
 
 
+def assign_bias(c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """The tensor-core bias operand of bf16/fp16 centroids (B,K,d): (B, kpad, 16)
+    bf16 [hi, mid, lo] split of ||c||^2/2 (rows >= K: +inf).  ``assign`` takes
+    it to skip its own pass over C; ``normalize(bias_out=)`` writes the next one."""
+    dev = _require_cuda(c)
+    c = c.contiguous()
+    B, K, d = c.shape
+    if out is None:
+        out = torch.empty((B, N.lib().fk_assign_bias_rows(K), 16), dtype=torch.bfloat16, device=dev)
+    N.check(N.lib().fk_assign_bias(fk_dtype(c.dtype), c.data_ptr(), B, K, d, out.data_ptr(), _stream(dev)),
+            "fk_assign_bias")
+    return out
+
+
 def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = None,
            changed: torch.Tensor | None = None, idx_out: torch.Tensor | None = None,
-           mind_out: torch.Tensor | None = None):
+           mind_out: torch.Tensor | None = None, bias: torch.Tensor | None = None):
     """Nearest centroid per point: (ids int32 (B,N), min_dists (B,N)).
 
     min_dists is in the data dtype for float32/float64 data and float32 for
     bfloat16/float16 data.  If ``idx_prev`` is given, ``changed`` (int32
-    device scalar) is OR-ed with 1 when any id differs.
+    device scalar) is OR-ed with 1 when any id differs.  ``bias`` (bf16/fp16
+    only): the precomputed ``assign_bias(c)``.
     """
     dev = _require_cuda(x, c)
     if x.dim() != 3 or c.dim() != 3 or x.shape[0] != c.shape[0] or x.shape[2] != c.shape[2]:
@@ -87,7 +102,8 @@ def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = Non
     L = N.lib()
     need = L.fk_assign_workspace(dt, B, n, K, d)
     ws = _ws.get(dev, need, "assign")
-    st = L.fk_assign(dt, x.data_ptr(), c.data_ptr(), B, n, K, d, idx_out.data_ptr(),
+    st = L.fk_assign(dt, x.data_ptr(), c.data_ptr(), None if bias is None else bias.data_ptr(),
+                     B, n, K, d, idx_out.data_ptr(),
                      mind_out.data_ptr(), None if idx_prev is None else idx_prev.data_ptr(),
                      None if changed is None else changed.data_ptr(),
                      None if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
@@ -148,7 +164,7 @@ def argsort(ids: torch.Tensor, clusters: int):
 def normalize(sums: torch.Tensor, counts: torch.Tensor, prev: torch.Tensor,
               out: torch.Tensor | None = None, operand_dtype: torch.dtype | None = None,
               operand_out: torch.Tensor | None = None, empty: torch.Tensor | None = None,
-              shift2: torch.Tensor | None = None):
+              shift2: torch.Tensor | None = None, bias_out: torch.Tensor | None = None):
     """c = sums/counts (empty clusters keep ``prev`` bitwise).
 
     ``prev``/``out`` are float32 or float64 masters; ``operand_out`` gets the
@@ -172,7 +188,7 @@ def normalize(sums: torch.Tensor, counts: torch.Tensor, prev: torch.Tensor,
                               out.data_ptr(), odt,
                               None if operand_out is None else operand_out.data_ptr(),
                               empty.data_ptr(), None if shift2 is None else shift2.data_ptr(),
-                              B, K, d, _stream(dev))
+                              B, K, d, None if bias_out is None else bias_out.data_ptr(), _stream(dev))
     N.check(st, "fk_normalize")
     return out, operand_out, empty
 
@@ -190,6 +206,31 @@ def objective(mind: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tens
                         ws.data_ptr(), ws.numel(), _stream(dev))
     N.check(st, "fk_objective")
     return out
+
+
+OBJ_BLOCK = 8192  # elements per objective partial (fk_objective_partials)
+
+
+def objective_partials(mind: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+    """Fixed-order f64 partial sums of (B,N) min_dists into out (B * ceil(N/8192),)."""
+    dev = _require_cuda(mind, out)
+    B, n = mind.shape
+    N.check(N.lib().fk_objective_partials(fk_dtype(mind.dtype), mind.data_ptr(), B, n, out.data_ptr(),
+                                          _stream(dev)), "fk_objective_partials")
+    return out
+
+
+def loop_tail(partials: torch.Tensor, B: int, n: int, obj: torch.Tensor, changed: torch.Tensor,
+              shift2: torch.Tensor, merges: torch.Tensor, flags: torch.Tensor,
+              history: torch.Tensor | None = None, history_row: torch.Tensor | None = None) -> None:
+    """One launch at the end of an iteration: objective (+ history row), the
+    [changed, shift^2, merges] flags, and the accumulators cleared."""
+    dev = _require_cuda(partials, obj, changed, shift2, merges, flags)
+    N.check(N.lib().fk_loop_tail(partials.data_ptr(), B, n, obj.data_ptr(),
+                                 None if history is None else history.data_ptr(),
+                                 None if history_row is None else history_row.data_ptr(),
+                                 changed.data_ptr(), shift2.data_ptr(), merges.data_ptr(),
+                                 flags.data_ptr(), _stream(dev)), "fk_loop_tail")
 
 
 def row_norms(m: torch.Tensor) -> torch.Tensor:

@@ -113,6 +113,23 @@ class LloydEngine:
         # only for the single-device CUDA path (the NCCL all-reduce stays eager)
         self.use_graphs = backend is None and allreduce is None and self.x.is_cuda
         self._graphs: dict = {}
+        # single-device CUDA path: the end of an iteration is one fk_loop_tail
+        # launch (objective, history row, flags, cleared accumulators), and the
+        # tensor-core bias operand of the next centroids comes out of normalize
+        self.fused = backend is None and allreduce is None
+        self.bias = None
+        if self.fused:
+            from .ops import OBJ_BLOCK
+
+            self._part = torch.empty((B * -(-N // OBJ_BLOCK),), dtype=torch.float64, device=dev)
+            self._flags_d = torch.zeros(3, dtype=torch.float64, device=dev)
+            self._hist = None
+            self._hist_row = torch.zeros((), dtype=torch.int64, device=dev)
+            if self.dtype in LOW_PRECISION:
+                kpad = ops.N.lib().fk_assign_bias_rows(K)
+                self.bias = [torch.zeros((B, kpad, 16), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+                for bz in self.bias:  # padding columns: +inf bias (normalize writes rows < K only)
+                    bz[:, K:, 0] = float("inf")
 
     # -------------------------------------------------------------- state
     def set_centroids(self, c: torch.Tensor) -> None:
@@ -120,7 +137,22 @@ class LloydEngine:
         self.master[self.cur].copy_(c.to(self.mdtype))
         if self.operand is not self.master:
             self.operand[self.cur].copy_(self.master[self.cur].to(self.dtype))
+        self._refresh_bias(self.cur)
         self.it = 0
+
+    def _refresh_bias(self, slot: int) -> None:
+        """Recompute the bias operand of operand[slot] (after a host-side edit)."""
+        if self.bias is not None:
+            ops.assign_bias(self.operand[slot], out=self.bias[slot])
+
+    def _assign_kw(self, csrc: int) -> dict:
+        return {} if self.bias is None else {"bias": self.bias[csrc]}
+
+    def _normalize(self, nxt: int) -> None:
+        kw = {} if self.bias is None else {"bias_out": self.bias[nxt]}
+        self.be.normalize(self.sums, self.counts, self.master[self.cur], out=self.master[nxt],
+                          operand_out=None if self.operand is self.master else self.operand[nxt],
+                          empty=self.empty, shift2=self.shift2, **kw)
 
     @property
     def centroids(self) -> torch.Tensor:
@@ -133,8 +165,8 @@ class LloydEngine:
     # -------------------------------------------------------------- phases
     def assign(self, out_slot: int, compare: bool):
         self.be.assign(self.x, self.operand[self.cur], idx_prev=self.ids[out_slot ^ 1] if compare else None,
-                   changed=self.changed if compare else None, idx_out=self.ids[out_slot],
-                   mind_out=self.mind)
+                       changed=self.changed if compare else None, idx_out=self.ids[out_slot],
+                       mind_out=self.mind, **self._assign_kw(self.cur))
 
     def iterate(self, history_row: torch.Tensor | None = None):
         """One Lloyd iteration, fully on the device.
@@ -175,10 +207,7 @@ class LloydEngine:
                    merges=self.merges_it)
         if self.allreduce is not None:
             self.exchange()
-        nxt = self.cur ^ 1
-        self.be.normalize(self.sums, self.counts, self.master[self.cur], out=self.master[nxt],
-                          operand_out=None if self.operand is self.master else self.operand[nxt],
-                          empty=self.empty, shift2=self.shift2)
+        self._normalize(self.cur ^ 1)
 
     def exchange(self) -> None:
         """Combine the point shards: pack [counts | objective | changed] behind the
@@ -226,28 +255,46 @@ class LloydEngine:
     def enq_assign(self, slot: int, compare: bool, csrc: int) -> None:
         """Queue iteration work part 1: assignment into ids[slot] against operand[csrc]."""
         def fn():
-            self.changed.zero_()
+            if not self.fused:  # the fused tail leaves `changed` cleared
+                self.changed.zero_()
             self.be.assign(self.x, self.operand[csrc],
                            idx_prev=self.ids[slot ^ 1] if compare else None,
                            changed=self.changed if compare else None, idx_out=self.ids[slot],
-                           mind_out=self.mind)
+                           mind_out=self.mind, **self._assign_kw(csrc))
         self._graph(("a", slot, compare, csrc), fn)
 
     def enq_rest(self, slot: int, history_row: torch.Tensor | None = None, timers=None) -> None:
         """Queue part 2: objective, update, shard exchange, normalize into the
         other centroid slot, then an async copy of [changed, shift2, merges]
-        to pinned host memory (read by wait_flags)."""
+        to pinned host memory (read by wait_flags).  On the single-device path
+        the objective, the history row (``run``'s history, row index kept on
+        the device), the flags and the cleared accumulators are one
+        fk_loop_tail launch."""
         if not hasattr(self, "_flags_h"):
-            self._flags_d = torch.zeros(3, dtype=torch.float64, device=self.dev)
+            if not self.fused:
+                self._flags_d = torch.zeros(3, dtype=torch.float64, device=self.dev)
             self._flags_h = torch.zeros(3, dtype=torch.float64).pin_memory() if self.x.is_cuda \
                 else torch.zeros(3, dtype=torch.float64)
             self._flags_ev = torch.cuda.Event() if self.x.is_cuda else None
+        nxt = self.cur ^ 1
+
+        def fn_fused():
+            ops.objective_partials(self.mind, self._part)
+            if timers is not None:  # bench: live per-kernel timing (eager only)
+                timers[0].record()
+            self.be.update(self.x, self.ids[slot], self.K, self.chunk, sums=self.sums,
+                           counts=self.counts, merges=self.merges_it)
+            if timers is not None:
+                timers[1].record()
+            self._normalize(nxt)
+            ops.loop_tail(self._part, self.B, self.N, self.obj, self.changed, self.shift2, self.merges_it,
+                          self._flags_d, self._hist, None if self._hist is None else self._hist_row)
 
         def fn():
             self.shift2.zero_()
             self.merges_it.zero_()
             self.be.objective(self.mind, out=self.obj)
-            if timers is not None:  # bench: live per-kernel timing (eager only)
+            if timers is not None:
                 timers[0].record()
             self.be.update(self.x, self.ids[slot], self.K, self.chunk, sums=self.sums,
                            counts=self.counts, merges=self.merges_it)
@@ -255,22 +302,24 @@ class LloydEngine:
                 timers[1].record()
             if self.allreduce is not None:
                 self.exchange()
-            nxt = self.cur ^ 1
-            self.be.normalize(self.sums, self.counts, self.master[self.cur], out=self.master[nxt],
-                              operand_out=None if self.operand is self.master else self.operand[nxt],
-                              empty=self.empty, shift2=self.shift2)
+            self._normalize(nxt)
             self._flags_d[0].copy_(self.changed)
             self._flags_d[1].copy_(self.shift2)
             self._flags_d[2].copy_(self.merges_it)
+        body = fn_fused if self.fused else fn
         if timers is not None:
-            fn()
+            body()
         else:
-            self._graph(("r", slot, self.cur), fn)
+            hp = None if self._hist_ptr() is None else self._hist_ptr()
+            self._graph(("r", slot, self.cur, hp), body)
         if history_row is not None:
             history_row.copy_(self.obj)
         self._flags_h.copy_(self._flags_d, non_blocking=True)
         if self._flags_ev is not None:
             self._flags_ev.record()
+
+    def _hist_ptr(self):
+        return None if not self.fused or self._hist is None else self._hist.data_ptr()
 
     def wait_flags(self):
         """(changed, shift, merges of this iteration) once its flags reached the host."""
@@ -287,11 +336,17 @@ class LloydEngine:
         merges = 0
         slot = 0
         it = 0
+        if self.fused:  # the loop tail writes history rows through a device row index
+            self._hist = history
+            self._hist_row.zero_()
+            self.changed.zero_()
+            self.shift2.zero_()
+            self.merges_it.zero_()
         self.enq_assign(0, False, self.cur)
         while it < max_iters:
             it += 1
             slot = (it - 1) & 1
-            self.enq_rest(slot, None if history is None else history[it - 1])
+            self.enq_rest(slot, None if (history is None or self.fused) else history[it - 1])
             spec = it < max_iters
             if spec:  # assume the commit: next assign against the new centroids
                 self.enq_assign(slot ^ 1, True, self.cur ^ 1)
@@ -303,6 +358,8 @@ class LloydEngine:
             if shift <= shift_tol:
                 break
         self.it = it
+        if self.fused:
+            self._hist = None
         return it, slot, merges
 
     def poll(self):
@@ -329,6 +386,7 @@ class LloydEngine:
             self.master[nxt][b, cid] = self.x[b, rows].to(self.mdtype)
             if self.operand is not self.master:
                 self.operand[nxt][b, cid] = self.x[b, rows]
+        self._refresh_bias(nxt)
         diff = self.master[nxt].double() - self.master[self.cur].double()
         self.shift2.copy_((diff * diff).sum(-1).max())
 
@@ -400,7 +458,15 @@ def _lloyd_baseline(x: DataMatrix, cfg: KMeansConfig, counters: Counters) -> KMe
         if prev is not None and torch.equal(prev.values, a.values):
             break
         stats = scatter_update(xc, a, cfg.clusters, counters)
-        new_c, _ = normalize(stats, c, cfg.empty_cluster_policy)
+        new_c, empties = normalize(stats, c, cfg.empty_cluster_policy)
+        if cfg.empty_cluster_policy == "reseed_farthest" and any(empties):
+            # _reseed_in_core (pipeline.py:84-89): next-farthest point per empty cluster
+            data = new_c.data.clone()
+            for b, cids in enumerate(empties):
+                if cids:
+                    rows = torch.from_numpy(_farthest(mind[b], len(cids), 0)).to(data.device)
+                    data[b, torch.tensor(cids[: rows.numel()], device=data.device)] = xc.data[b, rows].to(data.dtype)
+            new_c = Centroids(data, check_finite=False)
         diff = new_c.data.double() - c.data.double()
         shift = float((diff * diff).sum(-1).max().sqrt())
         prev, c = a, new_c

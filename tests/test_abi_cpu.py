@@ -49,13 +49,13 @@ def test_version_and_status_strings():
 def test_validation_before_any_launch():
     L = _native.lib()
     # B = 0
-    st = L.fk_assign(_native.FK_BF16, 16, 16, 0, 10, 4, 8, 16, 16, None, None, None, 0, None)
+    st = L.fk_assign(_native.FK_BF16, 16, 16, None, 0, 10, 4, 8, 16, 16, None, None, None, 0, None)
     assert st == _native.FK_EINVAL
     # null output pointers
-    st = L.fk_assign(_native.FK_F32, 16, 16, 1, 10, 4, 8, None, None, None, None, None, 0, None)
+    st = L.fk_assign(_native.FK_F32, 16, 16, None, 1, 10, 4, 8, None, None, None, None, None, 0, None)
     assert st == _native.FK_EINVAL
     # idx_prev without a changed flag
-    st = L.fk_assign(_native.FK_F32, 16, 16, 1, 10, 4, 8, 16, 16, 16, None, None, 0, None)
+    st = L.fk_assign(_native.FK_F32, 16, 16, None, 1, 10, 4, 8, 16, 16, 16, None, None, 0, None)
     assert st == _native.FK_EINVAL
     # bad dtype
     st = L.fk_update(9, 16, 16, 1, 10, 4, 8, 5, 0, 16, 16, None, 16, 1 << 20, None)
@@ -67,8 +67,14 @@ def test_validation_before_any_launch():
     st = L.fk_update(_native.FK_F32, 16, 16, 1, 10, 4, 8, 5, 0, 16, 16, None, 16, 1, None)
     assert st == _native.FK_EWORKSPACE
     # normalize master must be f32/f64
-    st = L.fk_normalize(_native.FK_BF16, 16, 16, 16, 16, 0, None, None, None, 1, 4, 8, None)
+    st = L.fk_normalize(_native.FK_BF16, 16, 16, 16, 16, 0, None, None, None, 1, 4, 8, None, None)
     assert st == _native.FK_EINVAL
+    # a bias operand needs a bf16/fp16 operand
+    st = L.fk_normalize(_native.FK_F32, 16, 16, 16, 16, 0, None, None, None, 1, 4, 8, 16, None)
+    assert st == _native.FK_EINVAL
+    # bias of f32 centroids
+    assert L.fk_assign_bias(_native.FK_F32, 16, 1, 4, 8, 16, None) == _native.FK_EINVAL
+    assert L.fk_assign_bias_rows(300) == 512 and L.fk_assign_bias_rows(256) == 256
 
 
 def test_workspace_queries():

@@ -285,3 +285,25 @@ def test_device_argsort_stable_under_heavy_collisions(ops, K):
     for _ in range(10):
         order, _ = ops.argsort(idc, K)
         assert np.array_equal(order.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("dtype,K,d", [(torch.bfloat16, 300, 128), (torch.float16, 256, 64),
+                                       (torch.bfloat16, 4096, 128), (torch.bfloat16, 77, 200)])
+def test_normalize_bias_operand_is_assign_bias(ops, dtype, K, d):
+    """normalize(bias_out=) writes, bit for bit, the bias operand fk_assign would
+    compute from the rounded centroids, and assign gives the same ids with it."""
+    g = torch.Generator(device="cuda").manual_seed(K + d)
+    B = 2
+    sums = torch.randn((B, K, d), device="cuda", generator=g, dtype=torch.float64) * 50
+    counts = torch.randint(0, 9, (B, K), device="cuda", generator=g, dtype=torch.int64)
+    prev = torch.randn((B, K, d), device="cuda", generator=g)
+    kpad = ops.N.lib().fk_assign_bias_rows(K)
+    bias = torch.zeros((B, kpad, 16), dtype=torch.bfloat16, device="cuda")
+    ops.assign_bias(prev.to(dtype), out=bias)  # padding rows
+    out, operand, _ = ops.normalize(sums, counts, prev, operand_dtype=dtype, bias_out=bias)
+    ref = ops.assign_bias(operand)
+    assert torch.equal(bias.view(torch.int16), ref.view(torch.int16))
+    x = (torch.randn((B, 5000, d), device="cuda", generator=g) * 3).to(dtype)
+    a0, m0 = ops.assign(x, operand)
+    a1, m1 = ops.assign(x, operand, bias=bias)
+    assert torch.equal(a0, a1) and torch.equal(m0, m1)
