@@ -197,6 +197,20 @@ FK_API fk_status fk_merges_from_counts(const int64_t* counts, int64_t B, int64_t
                                        int64_t update_chunk, int64_t* merges, int32_t accumulate,
                                        void* stream);
 
+/* ---------------------------------------------------------- reseed_farthest
+ * The E points farthest from their assigned centroids, in the reference's
+ * order: distance descending, ties to the lowest point index
+ * (_farthest_order / _FarthestTracker, pipeline.py:76-89, 283-309).
+ *   mind   : (B,N) f32 or f64 assigned distances (fk_assign's min_dists)
+ *   idx_out: (B,E) int64 point indices
+ * A radix select over the unique 96-bit keys (f64 distance bits, inverted
+ * index) finds the E-th largest key on the device, then the E winners are
+ * sorted in shared memory -- no sort of all N, no host round trip.
+ * E <= 8192 (FK_EUNSUPPORTED beyond), N < 2^32.                             */
+FK_API size_t fk_farthest_workspace(int64_t B, int64_t E);
+FK_API fk_status fk_farthest(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N, int64_t E,
+                             int64_t* idx_out, void* workspace, size_t workspace_bytes, void* stream);
+
 /* ------------------------------------------------------------- k-means++
  * D^2 seeding of init_centroids(method="kmeanspp") on the device:
  *   fk_kmeanspp        <- _kmeanspp_indices      core.py:342-357

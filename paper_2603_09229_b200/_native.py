@@ -66,6 +66,10 @@ def _declare(L):
     L.fk_stats_pack.argtypes = [I32, P, P, P, P, I64, I64, P]
     L.fk_merges_from_counts.restype = ctypes.c_int
     L.fk_merges_from_counts.argtypes = [P, I64, I64, I64, P, I32, P]
+    L.fk_farthest_workspace.restype = SZ
+    L.fk_farthest_workspace.argtypes = [I64, I64]
+    L.fk_farthest.restype = ctypes.c_int
+    L.fk_farthest.argtypes = [ctypes.c_int, P, I64, I64, I64, P, P, SZ, P]
     L.fk_kmeanspp_workspace.restype = SZ
     L.fk_kmeanspp_workspace.argtypes = [I64, I64, I64, I64]
     L.fk_kmeanspp.restype = ctypes.c_int
@@ -84,7 +88,8 @@ EXPORTED = (
     "fk_assign_workspace", "fk_assign_bias_rows", "fk_assign_bias", "fk_assign", "fk_update_workspace",
     "fk_update", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
     "fk_objective_partials", "fk_loop_tail", "fk_scatter",
-    "fk_stats_pack", "fk_merges_from_counts", "fk_kmeanspp_workspace", "fk_kmeanspp",
+    "fk_stats_pack", "fk_merges_from_counts", "fk_farthest_workspace", "fk_farthest",
+    "fk_kmeanspp_workspace", "fk_kmeanspp",
     "fk_kmeanspp_init", "fk_kmeanspp_sweep", "fk_kmeanspp_select",
 )
 

@@ -262,6 +262,24 @@ fk_status fk_merges_from_counts(const int64_t* counts, int64_t B, int64_t K, int
                                               reinterpret_cast<cudaStream_t>(stream)));
 }
 
+// ------------------------------------------------------------- reseed
+size_t fk_farthest_workspace(int64_t B, int64_t E) {
+  if (B < 1 || E < 1) return 0;
+  return fk::farthest_workspace_bytes(B, E);
+}
+
+fk_status fk_farthest(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N, int64_t E,
+                      int64_t* idx_out, void* ws, size_t ws_bytes, void* stream) {
+  if ((mind_dt != FK_F32 && mind_dt != FK_F64) || !mind || !idx_out || B < 1 || N < 1 || E < 1 ||
+      E > N || N >= ((int64_t)1 << 32))
+    return FK_EINVAL;
+  if (E > 8192) return FK_EUNSUPPORTED;
+  if (!ws || ws_bytes < fk_farthest_workspace(B, E)) return FK_EWORKSPACE;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_farthest(mind_dt == FK_F64 ? 1 : 0, mind, B, N, E, idx_out, ws,
+                                         dev_info().sms, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 // ------------------------------------------------------------- k-means++
 size_t fk_kmeanspp_workspace(int64_t B, int64_t N, int64_t K, int64_t d) {
   if (B < 1 || N < 1 || B * N > kMaxPoints || K < 0 || d < 0) return 0;

@@ -65,6 +65,11 @@ cudaError_t launch_stats_pack(int unpack, int64_t* counts, double* obj, int32_t*
 cudaError_t launch_merges_counts(const int64_t* counts, int64_t B, int64_t K, int64_t chunk,
                                  int64_t* merges, int accumulate, cudaStream_t s);
 
+// fk_select.cu
+size_t farthest_workspace_bytes(int64_t B, int64_t E);
+cudaError_t launch_farthest(int mind_is_f64, const void* mind, int64_t B, int64_t N, int64_t E,
+                            int64_t* idx_out, void* ws, int num_sms, cudaStream_t s);
+
 // fk_kmeanspp.cu
 size_t kmeanspp_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d);
 cudaError_t launch_kmeanspp_init(int32_t* halted, void* ws, int64_t B, int64_t N, int64_t K,

@@ -519,7 +519,8 @@ __global__ void __launch_bounds__(SD_T, 1)
 // ranges < 2^16 points (update_bpb).
 constexpr int SW_KMAX = 16384;            // W * (K + 2) * 2 bytes <= 64 KB, + K * 8 bytes of bases
 constexpr int SW_TABLE_BYTES = 65536;
-constexpr int SW_U = 8;                   // steps in flight per warp
+constexpr int SW_U = 8;                   // 16-byte id vectors in flight per lane (counting)
+constexpr int SW_U3 = 16;                 // id loads in flight per lane (ranking)
 constexpr int SW_COLS_BPB = 16;           // up to this many blocks per batch element: no k_colscan
 
 // Exclusive scan, in place, of n int32 values in shared memory by the whole
@@ -581,7 +582,10 @@ __global__ void __launch_bounds__(W * 32)
   const int KS = (int)K + 2;
   uint16_t* tab = reinterpret_cast<uint16_t*>(sw_sm);                           // W * KS
   int32_t* kbase = reinterpret_cast<int32_t*>(sw_sm + ((W * KS * 2 + 15) & ~15));  // K
-  int32_t* kpre = kbase + K;                                                      // K
+  // the key prefix lives in the table's space when it fits (the table is
+  // cleared only after the prefix is folded into kbase)
+  const bool alias = (int64_t)W * KS * 2 >= K * 4;
+  int32_t* kpre = alias ? reinterpret_cast<int32_t*>(sw_sm) : kbase + K;         // K
   uint32_t* tab32 = reinterpret_cast<uint32_t*>(sw_sm);
   __shared__ int32_t wsum[32];
   __shared__ unsigned long long s_bad, s_mg;
@@ -595,8 +599,8 @@ __global__ void __launch_bounds__(W * 32)
     s_bad = 0;
     s_mg = 0;
   }
-  for (int i = t; i < W * KS / 2; i += W * 32) tab32[i] = 0u;
   // block base inside each key's run (kbase) and the key totals (kpre)
+#pragma unroll 4
   for (int k = t; k < K; k += W * 32) {
     if (COLS) {
       const int32_t* col = table + (int64_t)b * bpb * K + k;
@@ -638,26 +642,46 @@ __global__ void __launch_bounds__(W * 32)
     if (lane == 0 && mg) atomicAdd(&s_mg, mg);
   }
   for (int k = t; k < K; k += W * 32) kbase[k] += (int32_t)(base_b + kpre[k]);  // flat < 2^31
+  __syncthreads();  // kpre consumed: the table space is free
+  for (int i = t; i < W * KS / 2; i += W * 32) tab32[i] = 0u;
   // this warp's part [a, e) of the block range
   const int n = (int)(hi - lo);
   const int a = (int)((int64_t)n * w / W), e = (int)((int64_t)n * (w + 1) / W);
   const int32_t* idw = ids + lo;
   __syncthreads();
   if (j == 0 && merges && t == 0 && s_mg) atomicAdd((unsigned long long*)merges, s_mg);
-  // 1. per-warp counts (fire-and-forget shared atomics on packed u16 pairs)
-  for (int p0 = a; p0 < e; p0 += 32 * SW_U) {
-    uint32_t id[SW_U];
-#pragma unroll
-    for (int u = 0; u < SW_U; ++u) {
-      const int p = p0 + u * 32 + lane;
-      id[u] = p < e ? (uint32_t)__ldg(idw + p) : 0xffffffffu;
-    }
-#pragma unroll
-    for (int u = 0; u < SW_U; ++u)
-      if (id[u] < Ku) {
-        const uint32_t f = (uint32_t)(w * KS) + id[u];
+  // 1. per-warp counts (fire-and-forget shared atomics on packed u16 pairs);
+  //    order-free, so the ids come in as 16-byte vectors (SW_U of them in flight)
+  {
+    auto count = [&](uint32_t id) {
+      if (id < Ku) {
+        const uint32_t f = (uint32_t)(w * KS) + id;
         atomicAdd(tab32 + (f >> 1), 1u << (16 * (f & 1)));
       }
+    };
+    const int64_t ga = lo + a;
+    int h = (int)((4 - (ga & 3)) & 3);  // scalar head up to a 16-byte boundary
+    if (h > e - a) h = e - a;
+    if (lane < h) count((uint32_t)__ldg(idw + a + lane));
+    const int nv = (e - a - h) >> 2;
+    const int4* v4 = reinterpret_cast<const int4*>(idw + a + h);
+    for (int q0 = 0; q0 < nv; q0 += 32 * SW_U) {
+      int4 v[SW_U];
+#pragma unroll
+      for (int u = 0; u < SW_U; ++u) {
+        const int q = q0 + u * 32 + lane;
+        v[u] = q < nv ? __ldg(v4 + q) : make_int4(-1, -1, -1, -1);
+      }
+#pragma unroll
+      for (int u = 0; u < SW_U; ++u) {
+        count((uint32_t)v[u].x);
+        count((uint32_t)v[u].y);
+        count((uint32_t)v[u].z);
+        count((uint32_t)v[u].w);
+      }
+    }
+    const int t0 = a + h + 4 * nv;
+    if (lane < e - t0) count((uint32_t)__ldg(idw + t0 + lane));
   }
   __syncthreads();
   // 2. exclusive prefix over the W warp rows of each key: segmented warp scans
@@ -683,15 +707,15 @@ __global__ void __launch_bounds__(W * 32)
   //    the same counter are serialized in lane order, so the returned counts
   //    are the stable ranks (checked against numpy's stable argsort in
   //    tests/test_gpu_kernels.py).  The ids are re-read (L2-resident).
-  for (int p0 = a; p0 < e; p0 += 32 * SW_U) {
-    uint32_t id[SW_U];
+  for (int p0 = a; p0 < e; p0 += 32 * SW_U3) {
+    uint32_t id[SW_U3];
 #pragma unroll
-    for (int u = 0; u < SW_U; ++u) {
+    for (int u = 0; u < SW_U3; ++u) {
       const int p = p0 + u * 32 + lane;
       id[u] = p < e ? (uint32_t)__ldg(idw + p) : 0xffffffffu;
     }
 #pragma unroll
-    for (int u = 0; u < SW_U; ++u)
+    for (int u = 0; u < SW_U3; ++u)
       if (id[u] < Ku) {
         const uint32_t f = (uint32_t)(w * KS) + id[u];
         const uint32_t sh = 16 * (f & 1);
@@ -966,6 +990,8 @@ __global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restr
 // the shared bins the block rows live in global memory: keep them at most
 // ~2 bytes per point.
 static int64_t update_bpb(int64_t B, int64_t N, int64_t K, int num_sms) {
+  // ~2 blocks per SM (4 per SM measured no faster at config 3: the larger
+  // tables cost k_hist and k_colscan what the scatter gained)
   int64_t bpb = ((int64_t)num_sms * 2 + B - 1) / B;
   const int64_t max_bpb = (N + SD_S - 1) / SD_S;
   if (bpb > max_bpb) bpb = max_bpb;
@@ -1180,7 +1206,8 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
   if (scatter_is_warp(K)) {
     int W = 32;
     while (W > 1 && (int64_t)W * (K + 2) * 2 > SW_TABLE_BYTES) W >>= 1;
-    const size_t smem = (size_t)((W * (K + 2) * 2 + 15) & ~15) + (size_t)K * 8;
+    const bool alias = (int64_t)W * (K + 2) * 2 >= K * 4;
+    const size_t smem = (size_t)((W * (K + 2) * 2 + 15) & ~15) + (size_t)K * (alias ? 4 : 8);
     const bool cols = bpb <= SW_COLS_BPB;
 #define FK_SW2(WV, CV)                                                                             \
   do {                                                                                             \

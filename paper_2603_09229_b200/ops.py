@@ -233,6 +233,28 @@ def loop_tail(partials: torch.Tensor, B: int, n: int, obj: torch.Tensor, changed
                                  flags.data_ptr(), _stream(dev)), "fk_loop_tail")
 
 
+FARTHEST_EMAX = 8192
+
+
+def farthest(mind: torch.Tensor, take: int) -> torch.Tensor:
+    """The ``take`` points with the largest (B,N) min_dists, distance descending
+    then index ascending (the reference's _farthest_order): (B, take) int64."""
+    dev = _require_cuda(mind)
+    mind = mind.contiguous()
+    B, n = mind.shape
+    take = int(take)
+    if not 1 <= take <= n:
+        raise ValueError("take must be in [1, N]")
+    if mind.dtype not in (torch.float32, torch.float64):
+        mind = mind.float()
+    out = torch.empty((B, take), dtype=torch.int64, device=dev)
+    L = N.lib()
+    ws = _ws.get(dev, L.fk_farthest_workspace(B, take), "farthest")
+    N.check(L.fk_farthest(fk_dtype(mind.dtype), mind.data_ptr(), B, n, take, out.data_ptr(), ws.data_ptr(),
+                          ws.numel(), _stream(dev)), "fk_farthest")
+    return out
+
+
 def row_norms(m: torch.Tensor) -> torch.Tensor:
     """Exact row norms of a (rows, d) float32/float64 CUDA matrix (core.row_norms)."""
     dev = _require_cuda(m)

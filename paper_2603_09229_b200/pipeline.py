@@ -799,7 +799,10 @@ def _farthest(mind: torch.Tensor, take: int, offset: int, group=None):
     md = mind.double()
     n = md.numel()
     k = min(take, n)
-    order = torch.sort(-md, stable=True).indices[:k]
+    if mind.is_cuda and k <= ops.FARTHEST_EMAX:
+        order = ops.farthest(mind.reshape(1, n), k)[0]  # device radix select (fk_farthest)
+    else:  # host tensors (the CPU test backend) or more than 8192 empties: a stable sort
+        order = torch.sort(-md, stable=True).indices[:k]
     cand_d = torch.full((take,), float("-inf"), dtype=torch.float64, device=dev)
     cand_i = torch.full((take,), -1, dtype=torch.int64, device=dev)
     cand_d[:k] = md[order]

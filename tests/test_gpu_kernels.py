@@ -307,3 +307,20 @@ def test_normalize_bias_operand_is_assign_bias(ops, dtype, K, d):
     a0, m0 = ops.assign(x, operand)
     a1, m1 = ops.assign(x, operand, bias=bias)
     assert torch.equal(a0, a1) and torch.equal(m0, m1)
+
+
+@pytest.mark.parametrize("n,E,dtype,ties", [(1000, 1, torch.float32, False), (5_000_000, 37, torch.float32, True),
+                                             (300_001, 4096, torch.float64, True), (9, 9, torch.float32, True),
+                                             (2_000_000, 8192, torch.float32, False)])
+def test_device_farthest_is_reference_order(ops, n, E, dtype, ties):
+    """fk_farthest == np.lexsort((arange, -mind))[:E] (pipeline.py:76-81), ties included."""
+    g = torch.Generator().manual_seed(n + E)
+    m = torch.rand((2, n), generator=g, dtype=torch.float64) * 100
+    if ties:  # many exact duplicates, including among the winners
+        m = torch.round(m * 4) / 4
+    m = m.to(dtype)
+    got = ops.farthest(m.cuda(), E).cpu().numpy()
+    for b in range(2):
+        v = m[b].double().numpy()
+        ref = np.lexsort((np.arange(n), -v))[:E]
+        assert np.array_equal(got[b], ref)
