@@ -78,6 +78,12 @@ FK_API const char* fk_status_string(fk_status s);
 FK_API const char* fk_last_cuda_error(void);
 /* 1 if `device` is an sm_100 part this library has SASS for, else 0. */
 FK_API int fk_device_supported(int device);
+/* Load every kernel of the library on the current device now instead of at
+ * its first launch (lazy module loading), so a first call on a new shape
+ * pays no loading time (time-to-first-run, reference PAPER.md:392-395 and
+ * the `ttfr` bench, cli.py:261-336).  Idempotent per device.  The Python
+ * package calls it when it binds a device. */
+FK_API fk_status fk_preload(void);
 
 /* ---------------------------------------------------------------- assign
  * Nearest-centroid assignment without materializing the N x K distances.

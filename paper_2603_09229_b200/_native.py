@@ -34,6 +34,8 @@ def _declare(L):
     L.fk_last_cuda_error.restype = ctypes.c_char_p
     L.fk_device_supported.restype = ctypes.c_int
     L.fk_device_supported.argtypes = [ctypes.c_int]
+    L.fk_preload.restype = ctypes.c_int
+    L.fk_preload.argtypes = []
     L.fk_assign_workspace.restype = SZ
     L.fk_assign_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
     L.fk_assign_bias_rows.restype = I64
@@ -84,7 +86,7 @@ def _declare(L):
 
 
 EXPORTED = (
-    "fk_version", "fk_status_string", "fk_last_cuda_error", "fk_device_supported",
+    "fk_version", "fk_status_string", "fk_last_cuda_error", "fk_device_supported", "fk_preload",
     "fk_assign_workspace", "fk_assign_bias_rows", "fk_assign_bias", "fk_assign", "fk_update_workspace",
     "fk_update", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
     "fk_objective_partials", "fk_loop_tail", "fk_scatter",

@@ -4,6 +4,7 @@
 // baseline.py:134-137); kernels never see malformed shapes.
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/flashkmeans.h"
 #include "fk_common.cuh"
@@ -86,6 +87,54 @@ int fk_device_supported(int device) {
   if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device) != cudaSuccess)
     return 0;
   return major == 10 ? 1 : 0;
+}
+
+// Load every kernel of every translation unit on the current device now
+// (cuModuleEnumerateFunctions + cuFuncLoad, CUDA >= 12.4), so the first call
+// on a new shape -- a new head shape in the batched config
+// -- pays no lazy module-loading time.  Idempotent per device.
+fk_status fk_preload(void) {
+  typedef CUresult (*GetModFn)(CUmodule*, CUfunction);
+  typedef CUresult (*CountFn)(unsigned int*, CUmodule);
+  typedef CUresult (*EnumFn)(CUfunction*, unsigned int, CUmodule);
+  typedef CUresult (*LoadFn)(CUfunction);
+  static std::mutex mu;
+  static unsigned long long done_mask = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return FK_EUNSUPPORTED;
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev < 64 && (done_mask >> dev) & 1ull) return FK_OK;
+  auto sym = [](const char* name) -> void* {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(name, &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    return f;
+  };
+  auto get_mod = (GetModFn)sym("cuFuncGetModule");
+  auto count = (CountFn)sym("cuModuleGetFunctionCount");
+  auto enumerate = (EnumFn)sym("cuModuleEnumerateFunctions");
+  auto load = (LoadFn)sym("cuFuncLoad");
+  if (!get_mod || !count || !enumerate || !load) return FK_EUNSUPPORTED;
+  const void* anchors[] = {fk::module_anchor_assign_exact(), fk::module_anchor_assign_tc(),
+                           fk::module_anchor_kmeanspp(), fk::module_anchor_select(),
+                           fk::module_anchor_update()};
+  for (const void* a : anchors) {
+    cudaFunction_t f = nullptr;
+    cudaError_t e = cudaGetFuncBySymbol(&f, a);
+    if (e != cudaSuccess) return cuda_status(e);
+    CUmodule mod = nullptr;
+    unsigned int n = 0;
+    if (get_mod(&mod, (CUfunction)f) != CUDA_SUCCESS || count(&n, mod) != CUDA_SUCCESS)
+      return FK_ECUDA;
+    std::vector<CUfunction> fs(n);
+    if (n && enumerate(fs.data(), n, mod) != CUDA_SUCCESS) return FK_ECUDA;
+    for (CUfunction fn : fs)
+      if (load(fn) != CUDA_SUCCESS) return FK_ECUDA;
+  }
+  if (dev < 64) done_mask |= 1ull << dev;
+  return FK_OK;
 }
 
 // ------------------------------------------------------------------ assign

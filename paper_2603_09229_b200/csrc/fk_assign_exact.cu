@@ -283,4 +283,6 @@ cudaError_t launch_assign_cuda_core_lowp(int dt, const void* X, const void* C, c
   return cudaGetLastError();
 }
 
+FK_MODULE_ANCHOR(assign_exact)
+
 }  // namespace fk

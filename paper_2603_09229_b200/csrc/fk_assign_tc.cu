@@ -1100,4 +1100,6 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
 
 int assign_tc_kpad(int64_t K) { return (int)(((K + tc::BN - 1) / tc::BN) * tc::BN); }
 
+FK_MODULE_ANCHOR(assign_tc)
+
 }  // namespace fk

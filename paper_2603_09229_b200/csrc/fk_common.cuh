@@ -284,3 +284,11 @@ FK_DEV bool elect_one() {
 }
 
 }  // namespace fk
+
+// One empty kernel per translation unit: its address identifies the unit's
+// CUDA module, so fk_preload() can load every function of the module up front
+// (lazy module loading would otherwise load each kernel at its first launch).
+#define FK_MODULE_ANCHOR(name)                     \
+  __global__ void k_module_anchor_##name() {}      \
+  const void* module_anchor_##name() { return (const void*)k_module_anchor_##name; }
+

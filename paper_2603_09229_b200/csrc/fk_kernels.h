@@ -86,4 +86,11 @@ cudaError_t launch_kmeanspp(int dt, const void* X, int64_t B, int64_t N, int64_t
                             const double* u, int64_t* idx, int32_t* halted, double* m, void* ws,
                             cudaStream_t s);
 
+// FK_MODULE_ANCHOR of each translation unit (fk_preload)
+const void* module_anchor_assign_exact();
+const void* module_anchor_assign_tc();
+const void* module_anchor_kmeanspp();
+const void* module_anchor_select();
+const void* module_anchor_update();
+
 }  // namespace fk

@@ -1595,4 +1595,6 @@ cudaError_t launch_kmeanspp(int dt, const void* X, int64_t B, int64_t N, int64_t
   return cudaSuccess;
 }
 
+FK_MODULE_ANCHOR(kmeanspp)
+
 }  // namespace fk

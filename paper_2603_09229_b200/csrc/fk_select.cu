@@ -212,4 +212,6 @@ cudaError_t launch_farthest(int mind_is_f64, const void* mind, int64_t B, int64_
   return cudaGetLastError();
 }
 
+FK_MODULE_ANCHOR(select)
+
 }  // namespace fk

@@ -659,8 +659,10 @@ __global__ void __launch_bounds__(W * 32)
         atomicAdd(tab32 + (f >> 1), 1u << (16 * (f & 1)));
       }
     };
-    const int64_t ga = lo + a;
-    int h = (int)((4 - (ga & 3)) & 3);  // scalar head up to a 16-byte boundary
+    // scalar head up to a 16-byte boundary of the ADDRESS (ids may be a slice
+    // at any int32 offset, e.g. one streamed chunk)
+    const uintptr_t ga = reinterpret_cast<uintptr_t>(idw + a);
+    int h = (int)(((16 - (ga & 15)) & 15) >> 2);
     if (h > e - a) h = e - a;
     if (lane < h) count((uint32_t)__ldg(idw + a + lane));
     const int nv = (e - a - h) >> 2;
@@ -1654,5 +1656,7 @@ cudaError_t launch_scatter(int dt, const void* X, const int32_t* ids, int64_t B,
   }
   return cudaGetLastError();
 }
+
+FK_MODULE_ANCHOR(update)
 
 }  // namespace fk

@@ -55,9 +55,17 @@ def _require_cuda(*ts):
         if t is not None and not t.is_cuda:
             raise ValueError("device operators take CUDA tensors")
     dev = ts[0].device
-    if N.lib().fk_device_supported(dev.index if dev.index is not None else 0) != 1:
-        raise NotImplementedError("flash-kmeans kernels are compiled for sm_100a (B200) only")
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    if idx not in _bound:
+        if N.lib().fk_device_supported(idx) != 1:
+            raise NotImplementedError("flash-kmeans kernels are compiled for sm_100a (B200) only")
+        with torch.cuda.device(idx):  # load every kernel now: no lazy loading on a first shape
+            N.check(N.lib().fk_preload(), "fk_preload")
+        _bound.add(idx)
     return dev
+
+
+_bound: set = set()
 
 
 def assign_bias(c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
