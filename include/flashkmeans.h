@@ -95,9 +95,12 @@ FK_API fk_status fk_preload(void);
  *   idx_prev  : optional (B,N) int32; when given, *changed_flag (int32, device)
  *               is OR-ed with 1 if any id differs from idx_prev
  *               (the lloyd_run repeat test, pipeline.py:137)
- * FK_F32/FK_F64 always run the exact mirror (bitwise equal to the
- * reference); FK_BF16/FK_F16 run the tcgen05 kernel for d <= 256 (rows of
- * 16-byte multiples) and a CUDA-core kernel otherwise.
+ * FK_F32/FK_F64 are bitwise equal to the reference's dot_mode="exact": for
+ * d <= 128 and problems above ~6.7e7 multiply-adds through the certified
+ * tensor-core path (fk_assign_split below, X's split operand built in the
+ * workspace), otherwise through the exact CUDA-core mirror.  FK_BF16/FK_F16
+ * run the tcgen05 kernel for d <= 256 (rows of 16-byte multiples) and a
+ * CUDA-core kernel otherwise.
  * bias      : optional (FK_BF16/FK_F16 only) the tensor-core bias operand of C,
  *             (B, fk_assign_bias_rows(K), 16) bf16 = [hi, mid, lo, 0...] split of
  *             ||c||^2/2, as written by fk_normalize(bias_out) or fk_assign_bias;
@@ -110,6 +113,43 @@ FK_API fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void
                            int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
                            const int32_t* idx_prev, int32_t* changed_flag, void* workspace,
                            size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------- assign, f32 / f64 data
+ * The certified tensor-core path for the reference's own precisions
+ * (flash_assign dot_mode "exact" / "fast", flash_assign.py:203-208;
+ * dist_block and assign_tile_fast, _kernels.py:32-45, 85-104), d <= 128:
+ *   xsplit : (B, N, 32*ceil(d/16)) bf16 rows [hi | lo] of X, v = hi + lo +
+ *            O(2^-16 v), written once by fk_assign_xsplit and reusable while
+ *            X is unchanged (a Lloyd run builds it once).
+ *   dot_mode FK_DOT_EXACT: tcgen05 estimate of every distance (3 bf16 MMAs
+ *            per K=16 step, fp32 accumulation) + per-row certificate that the
+ *            estimated argmin is the reference's; uncertified rows (near and
+ *            exact ties, non-finite data) rerun the exact CUDA-core mirror.
+ *            Output bitwise equal to the reference's exact mode.
+ *   FK_DOT_FAST: the reference's relaxed mode (held to rtol 1e-6,
+ *            test_flash_assign.py:172-178) is served by the same certified
+ *            path, i.e. exactly: an uncertified tensor-core argmin can differ
+ *            from exact when two centroids are closer than the estimate's
+ *            error (~2^-16 |x||c|), which f64 reassociation never causes.
+ *   FK_DOT_MIRROR: the exact CUDA-core mirror for every row (xsplit unused).
+ * Workspace: fk_assign_split_workspace (does not include xsplit).           */
+enum { FK_DOT_EXACT = 0, FK_DOT_FAST = 1, FK_DOT_MIRROR = 2 };
+/* Diagnostic: how many rows of each batch element the last fk_assign_split
+ * call on `workspace` sent to the exact fallback (B int32 to host memory;
+ * synchronizes `stream`).  For fk_assign's own f32/f64 calls pass its
+ * workspace offset by fk_assign_xsplit_bytes.                              */
+FK_API fk_status fk_assign_split_fallback_rows(fk_dtype dt, int64_t B, int64_t N, int64_t K,
+                                               int64_t d, const void* workspace,
+                                               int32_t* counts_host, void* stream);
+FK_API size_t fk_assign_xsplit_bytes(fk_dtype dt, int64_t B, int64_t N, int64_t d);
+FK_API fk_status fk_assign_xsplit(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t d,
+                                  void* xsplit_out, void* stream);
+FK_API size_t fk_assign_split_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d);
+FK_API fk_status fk_assign_split(fk_dtype dt, const void* X, const void* xsplit, const void* C,
+                                 int64_t B, int64_t N, int64_t K, int64_t d, int32_t dot_mode,
+                                 int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+                                 int32_t* changed_flag, void* workspace, size_t workspace_bytes,
+                                 void* stream);
 
 /* ---------------------------------------------------------------- update
  * Per-cluster sums (f64) and counts (int64) from (X, ids) by a device stable

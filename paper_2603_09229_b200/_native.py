@@ -44,6 +44,16 @@ def _declare(L):
     L.fk_assign_bias.argtypes = [ctypes.c_int, P, I64, I64, I64, P, P]
     L.fk_assign.restype = ctypes.c_int
     L.fk_assign.argtypes = [ctypes.c_int, P, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P]
+    L.fk_assign_xsplit_bytes.restype = SZ
+    L.fk_assign_xsplit_bytes.argtypes = [ctypes.c_int, I64, I64, I64]
+    L.fk_assign_xsplit.restype = ctypes.c_int
+    L.fk_assign_xsplit.argtypes = [ctypes.c_int, P, I64, I64, I64, P, P]
+    L.fk_assign_split_workspace.restype = SZ
+    L.fk_assign_split_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
+    L.fk_assign_split_fallback_rows.restype = ctypes.c_int
+    L.fk_assign_split_fallback_rows.argtypes = [ctypes.c_int, I64, I64, I64, I64, P, P, P]
+    L.fk_assign_split.restype = ctypes.c_int
+    L.fk_assign_split.argtypes = [ctypes.c_int, P, P, P, I64, I64, I64, I64, I32, P, P, P, P, P, SZ, P]
     L.fk_update_workspace.restype = SZ
     L.fk_update_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
     L.fk_update.restype = ctypes.c_int
@@ -87,7 +97,9 @@ def _declare(L):
 
 EXPORTED = (
     "fk_version", "fk_status_string", "fk_last_cuda_error", "fk_device_supported", "fk_preload",
-    "fk_assign_workspace", "fk_assign_bias_rows", "fk_assign_bias", "fk_assign", "fk_update_workspace",
+    "fk_assign_workspace", "fk_assign_bias_rows", "fk_assign_bias", "fk_assign", "fk_assign_xsplit_bytes",
+    "fk_assign_xsplit", "fk_assign_split_workspace", "fk_assign_split", "fk_assign_split_fallback_rows",
+    "fk_update_workspace",
     "fk_update", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
     "fk_objective_partials", "fk_loop_tail", "fk_scatter",
     "fk_stats_pack", "fk_merges_from_counts", "fk_farthest_workspace", "fk_farthest",

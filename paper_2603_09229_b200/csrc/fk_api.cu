@@ -2,6 +2,7 @@
 // Validation happens here, before any launch (the reference validates before
 // any kernel call: flash_assign.py:152-157, sort_inverse.py:120-122,
 // baseline.py:134-137); kernels never see malformed shapes.
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -117,7 +118,8 @@ fk_status fk_preload(void) {
   auto enumerate = (EnumFn)sym("cuModuleEnumerateFunctions");
   auto load = (LoadFn)sym("cuFuncLoad");
   if (!get_mod || !count || !enumerate || !load) return FK_EUNSUPPORTED;
-  const void* anchors[] = {fk::module_anchor_assign_exact(), fk::module_anchor_assign_tc(),
+  const void* anchors[] = {fk::module_anchor_assign_exact(), fk::module_anchor_assign_split(),
+                           fk::module_anchor_assign_tc(),
                            fk::module_anchor_kmeanspp(), fk::module_anchor_select(),
                            fk::module_anchor_update()};
   for (const void* a : anchors) {
@@ -138,13 +140,157 @@ fk_status fk_preload(void) {
 }
 
 // ------------------------------------------------------------------ assign
+namespace {
+// f32/f64: the certified tensor-core path (fk_assign_split.cu) unless the
+// problem is too small to pay for its ~7 launches (the exact CUDA-core mirror
+// is then faster) or FK_ASSIGN_F32=mirror|split forces one.
+int f32_path_env() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("FK_ASSIGN_F32");
+    v = !e ? -1 : (e[0] == 'm' ? 0 : e[0] == 's' ? 1 : -1);
+  }
+  return v;
+}
+bool split_auto(int64_t B, int64_t N, int64_t K, int64_t d) {
+  if (!fk::assign_split_supported(d) || dev_info().major != 10) return false;
+  const int e = f32_path_env();
+  if (e >= 0) return e == 1;
+  return (double)B * N * K * d >= 6.7e7;  // ~20 us of the exact mirror
+}
+size_t xsplit_bytes(int64_t B, int64_t N, int64_t d) {
+  return al256((size_t)B * N * 32 * fk::split_steps(d) * 2);
+}
+struct SplitWs {
+  void *c2, *ext, *cn_ref, *xn_ref, *ct;
+  unsigned int* cmax;
+  int32_t *cnt, *list;
+  float *est, *second;
+  size_t bytes;
+};
+SplitWs split_ws_layout(uint8_t* base, int dt, int64_t B, int64_t N, int64_t K, int64_t d) {
+  const size_t es = elem_size(dt);
+  const int kpad = fk::assign_tc_kpad(K);
+  SplitWs w;
+  size_t o = 0;
+  auto take = [&](size_t n) { void* p = base ? base + o : nullptr; o += al256(n); return p; };
+  w.c2 = take((size_t)B * K * 32 * fk::split_steps(d) * 2);
+  w.ext = take((size_t)B * kpad * 32);
+  w.cn_ref = take((size_t)B * K * es);
+  w.ct = take((size_t)B * K * d * 4);  // fp32 (B, d, K): the fallback's estimate operand
+  w.cmax = (unsigned int*)take((size_t)B * 8);  // cmax (B) then cnt (B): one memset
+  w.cnt = base ? (int32_t*)(w.cmax + B) : nullptr;
+  w.est = (float*)take((size_t)B * N * 4);
+  w.second = (float*)take((size_t)B * N * 4);
+  w.list = (int32_t*)take((size_t)B * N * 4);
+  w.xn_ref = take((size_t)B * N * es);
+  w.bytes = o;
+  return w;
+}
+size_t exact_ws_bytes(int dt, int64_t B, int64_t N, int64_t K) {
+  const size_t es = elem_size(dt);
+  return al256((size_t)B * N * es) + al256((size_t)B * K * es);
+}
+
+fk_status run_split(int dt, const void* X, const void* xsplit, const void* C, int64_t B, int64_t N,
+                    int64_t K, int64_t d, int fast, int32_t* idx_out, void* mind_out,
+                    const int32_t* idx_prev, int32_t* changed, uint8_t* ws, cudaStream_t s) {
+  const SplitWs w = split_ws_layout(ws, dt, B, N, K, d);
+  const int kpad = fk::assign_tc_kpad(K);
+  const DevInfo di = dev_info();
+  fk_status st = cuda_status(cudaMemsetAsync(w.cmax, 0, (size_t)B * 8, s));
+  if (st != FK_OK) return st;
+  st = cuda_status(fk::launch_split_centroids(dt, C, B, K, d, kpad, w.c2, w.ext, w.cmax, w.ct, s));
+  if (st != FK_OK) return st;
+  st = cuda_status(fk::launch_row_norms_exact(dt, C, B * K, d, w.cn_ref, s));
+  if (st != FK_OK) return st;
+  st = cuda_status(fk::launch_assign_tc_split(xsplit, w.c2, w.ext, B, N, K, fk::split_steps(d),
+                                              idx_out, w.est, w.second, di.sms, s));
+  if (st != FK_OK) return st;
+  st = cuda_status(fk::launch_certify(dt, X, C, w.cn_ref, w.cmax, B, N, K, d, idx_out, w.est,
+                                      w.second, w.xn_ref, mind_out, idx_prev, changed, w.list,
+                                      w.cnt, fast, s));
+  if (st != FK_OK) return st;
+  return cuda_status(fk::launch_fallback_rows(dt, X, C, w.ct, w.cn_ref, w.xn_ref, w.cmax, B, N, K,
+                                              d, w.list, w.cnt, idx_out, mind_out, idx_prev, changed,
+                                              di.sms, s));
+}
+}  // namespace
+
 size_t fk_assign_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d) {
-  (void)d;
   if (!valid_dt(dt) || B < 1 || N < 1 || K < 1) return 0;
   if (is_lowp(dt))  // ||c||^2 (fp32) + the bias-in-GEMM operand (16 x 16-bit per centroid)
     return al256((size_t)B * fk::assign_tc_kpad(K) * 4) + al256((size_t)B * fk::assign_tc_kpad(K) * 32);
-  const size_t es = elem_size(dt);
-  return al256((size_t)B * N * es) + al256((size_t)B * K * es);
+  const size_t ex = exact_ws_bytes(dt, B, N, K);
+  if (!split_auto(B, N, K, d)) return ex;
+  const size_t sp = xsplit_bytes(B, N, d) + split_ws_layout(nullptr, dt, B, N, K, d).bytes;
+  return sp > ex ? sp : ex;
+}
+
+size_t fk_assign_xsplit_bytes(fk_dtype dt, int64_t B, int64_t N, int64_t d) {
+  if ((dt != FK_F32 && dt != FK_F64) || B < 1 || N < 1 || !fk::assign_split_supported(d)) return 0;
+  return xsplit_bytes(B, N, d);
+}
+
+fk_status fk_assign_xsplit(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t d,
+                           void* xsplit, void* stream) {
+  if ((dt != FK_F32 && dt != FK_F64) || !X || !xsplit || !shape_ok(B, N, 1, d)) return FK_EINVAL;
+  if (!fk::assign_split_supported(d)) return FK_EUNSUPPORTED;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_split_rows(dt, X, B * N, d, xsplit, dev_info().sms,
+                                           reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_assign_split_fallback_rows(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d,
+                                         const void* ws, int32_t* counts_host, void* stream) {
+  if ((dt != FK_F32 && dt != FK_F64) || !ws || !counts_host || !shape_ok(B, N, K, d)) return FK_EINVAL;
+  const SplitWs w = split_ws_layout(reinterpret_cast<uint8_t*>(const_cast<void*>(ws)), dt, B, N, K, d);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  fk_status st = cuda_status(cudaMemcpyAsync(counts_host, w.cnt, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+  if (st != FK_OK) return st;
+  return cuda_status(cudaStreamSynchronize(s));
+}
+
+size_t fk_assign_split_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d) {
+  if ((dt != FK_F32 && dt != FK_F64) || B < 1 || N < 1 || K < 1 || d < 1) return 0;
+  const size_t ex = exact_ws_bytes(dt, B, N, K);
+  const size_t sp = split_ws_layout(nullptr, dt, B, N, K, d).bytes;
+  return sp > ex ? sp : ex;
+}
+
+fk_status fk_assign_split(fk_dtype dt, const void* X, const void* xsplit, const void* C, int64_t B,
+                          int64_t N, int64_t K, int64_t d, int32_t dot_mode, int32_t* idx_out,
+                          void* mind_out, const int32_t* idx_prev, int32_t* changed_flag, void* ws,
+                          size_t ws_bytes, void* stream) {
+  if ((dt != FK_F32 && dt != FK_F64) || !shape_ok(B, N, K, d)) return FK_EINVAL;
+  if (!X || !C || !idx_out || !mind_out || dot_mode < 0 || dot_mode > 2) return FK_EINVAL;
+  if (idx_prev && !changed_flag) return FK_EINVAL;
+  if (!ws || ws_bytes < fk_assign_split_workspace(dt, B, N, K, d)) return FK_EWORKSPACE;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* w = reinterpret_cast<uint8_t*>(ws);
+  if (dot_mode == FK_DOT_MIRROR || !fk::assign_split_supported(d)) {
+    void* xn = w;
+    void* cn = w + al256((size_t)B * N * elem_size(dt));
+    fk_status st = cuda_status(fk::launch_row_norms_exact(dt, X, B * N, d, xn, s));
+    if (st != FK_OK) return st;
+    st = cuda_status(fk::launch_row_norms_exact(dt, C, B * K, d, cn, s));
+    if (st != FK_OK) return st;
+    return cuda_status(fk::launch_assign_exact(dt, X, C, xn, cn, B, N, K, d, idx_out, mind_out,
+                                               idx_prev, changed_flag, s));
+  }
+  if (!xsplit) return FK_EINVAL;
+  // FK_DOT_FAST: the certified path is already tensor-core speed, and a
+  // tensor-core argmin left uncertified can differ from the reference where
+  // two centroids sit closer than the estimate's error (same blob), which the
+  // reference's fast mode (f64 reassociation only) never does: serve it exactly.
+  static int nofb = -1;  // FK_SPLIT_NOFALLBACK=1: keep every estimate (measures the fallback's cost)
+  if (nofb < 0) {
+    const char* e = getenv("FK_SPLIT_NOFALLBACK");
+    nofb = (e && e[0] == '1') ? 1 : 0;
+  }
+  return run_split(dt, X, xsplit, C, B, N, K, d, nofb, idx_out, mind_out, idx_prev, changed_flag,
+                   w, s);
 }
 
 int64_t fk_assign_bias_rows(int64_t K) { return K < 1 ? 0 : fk::assign_tc_kpad(K); }
@@ -197,6 +343,12 @@ fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void* bias,
   }
   const size_t es = elem_size(dt);
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
+  if (split_auto(B, N, K, d)) {  // X's split operand in the workspace, then the certified path
+    fk_status st = cuda_status(fk::launch_split_rows(dt, X, B * N, d, w, di.sms, s));
+    if (st != FK_OK) return st;
+    return run_split(dt, X, w, C, B, N, K, d, 0, idx_out, mind_out, idx_prev, changed_flag,
+                     w + xsplit_bytes(B, N, d), s);
+  }
   void* xn = w;
   void* cn = w + al256((size_t)B * N * es);
   fk_status st = cuda_status(fk::launch_row_norms_exact(dt, X, B * N, d, xn, s));

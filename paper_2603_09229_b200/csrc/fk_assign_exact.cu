@@ -118,22 +118,34 @@ constexpr int EX_ROWS = 128;  // points per block (one per thread)
 constexpr int EX_KT = 16;     // centroids per register tile
 constexpr int EX_DC = 32;     // feature chunk staged in smem
 
-template <typename T, bool EXACT>
+// LIST: the block's rows are entries [128 x, 128 x + 128) of the per-batch
+// row list (list + b*N, list_cnt[b] entries) -- the rows the certified
+// tensor-core path could not decide (fk_assign_split.cu).
+template <typename T, bool EXACT, bool LIST = false>
 __global__ void __launch_bounds__(EX_ROWS)
     k_assign_cuda_core(const T* __restrict__ X, const T* __restrict__ C,
                        const void* __restrict__ xn_in, const void* __restrict__ cn_in,
                        int64_t N, int64_t K, int64_t d, int32_t* __restrict__ idx_out,
                        void* __restrict__ mind_out, const int32_t* __restrict__ idx_prev,
-                       int32_t* changed) {
+                       int32_t* changed, const int32_t* __restrict__ list = nullptr,
+                       const int32_t* __restrict__ list_cnt = nullptr) {
   using Acc = typename std::conditional<EXACT, double, float>::type;
   // Exact mode compares rounded T distances; low-precision mode compares fp32 scores.
   using Score = typename std::conditional<EXACT, T, float>::type;
   __shared__ T xs[EX_DC][EX_ROWS + 1];
   __shared__ T cs[EX_KT][EX_DC];
+  __shared__ int32_t srow[LIST ? EX_ROWS : 1];
   const int64_t b = blockIdx.y;
   const int64_t row0 = (int64_t)blockIdx.x * EX_ROWS;
   const int tid = threadIdx.x;
-  const int64_t row = row0 + tid;
+  int64_t row = row0 + tid;
+  if constexpr (LIST) {
+    const int64_t cnt = list_cnt[b];
+    if (row0 >= cnt) return;  // whole block: nothing listed here
+    srow[tid] = row0 + tid < cnt ? list[b * N + row0 + tid] : -1;
+    row = srow[tid] >= 0 ? srow[tid] : N;  // N = no row
+    __syncthreads();
+  }
   const T* Xb = X + b * N * d;
   const T* Cb = C + b * K * d;
 
@@ -155,7 +167,7 @@ __global__ void __launch_bounds__(EX_ROWS)
       __syncthreads();
       for (int e = tid; e < EX_ROWS * EX_DC; e += EX_ROWS) {
         int r = e / EX_DC, jj = e % EX_DC;
-        int64_t gr = row0 + r, gj = j0 + jj;
+        int64_t gr = LIST ? (srow[r] >= 0 ? (int64_t)srow[r] : N) : row0 + r, gj = j0 + jj;
         xs[jj][r] = (gr < N && gj < d) ? Xb[gr * d + gj] : (T)0.f;
       }
       for (int e = tid; e < EX_KT * EX_DC; e += EX_ROWS) {
@@ -261,6 +273,23 @@ cudaError_t launch_assign_exact(int dt, const void* X, const void* C, const void
   else
     k_assign_cuda_core<float, true><<<grid, EX_ROWS, 0, stream>>>(
         (const float*)X, (const float*)C, xn, cn, N, K, d, idx_out, mind_out, idx_prev, changed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assign_exact_rows(int dt, const void* X, const void* C, const void* xn,
+                                     const void* cn, int64_t B, int64_t N, int64_t K, int64_t d,
+                                     const int32_t* list, const int32_t* list_cnt,
+                                     int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+                                     int32_t* changed, cudaStream_t stream) {
+  dim3 grid((unsigned)((N + EX_ROWS - 1) / EX_ROWS), (unsigned)B);
+  if (dt == DT_F64)
+    k_assign_cuda_core<double, true, true><<<grid, EX_ROWS, 0, stream>>>(
+        (const double*)X, (const double*)C, xn, cn, N, K, d, idx_out, mind_out, idx_prev, changed,
+        list, list_cnt);
+  else
+    k_assign_cuda_core<float, true, true><<<grid, EX_ROWS, 0, stream>>>(
+        (const float*)X, (const float*)C, xn, cn, N, K, d, idx_out, mind_out, idx_prev, changed,
+        list, list_cnt);
   return cudaGetLastError();
 }
 

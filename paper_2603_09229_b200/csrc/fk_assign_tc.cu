@@ -69,6 +69,11 @@ struct TcArgs {
   int debug_mode;  // 0 normal; 1 epilogue skips math (MMA/TMA bound); 2 MMA skipped (epilogue bound)
   int epi2;        // 1: bias-in-GEMM epilogue processes 32-column chunks in pairs
   unsigned long long* trace;  // debug timeline (FK_ASSIGN_TRACE), nullptr normally
+  // split (f32/f64 data, fk_assign_split.cu): X and C are bf16 [hi | lo] rows
+  // of 2*ns K=16 steps; the MMA runs hi.hi + hi.lo + lo.hi per step and the
+  // epilogue also reports a lower bound on each row's second-best score.
+  int ns;
+  float* second_out;  // (B, N) second-best score bound (split only)
 };
 
 // Debug timeline: events of pair 0 / tile window [TR_G0, TR_G0 + TR_N) only.
@@ -407,7 +412,7 @@ constexpr int OFF_AEXT = 0;                                // constant ones oper
 constexpr int OFF_EXT = OFF_AEXT + BM * EXT_ROW;
 constexpr int OFF_CN = OFF_EXT + EXT_SLOTS * EXT_SLOT;
 constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;
-constexpr int OFF_BAR = OFF_XCH + BM * 12;  // [min | idx | ||x||^2 part] exchange
+constexpr int OFF_BAR = OFF_XCH + BM * 16;  // [min | idx | ||x||^2 part | second] exchange
 constexpr int A_SLOTS_MAX = 8;
 constexpr int NBARS = 2 * A_SLOTS_MAX + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
 constexpr int OFF_OPS = ((OFF_BAR + NBARS * 8 + 16) + 1023) & ~1023;  // 1 KB aligned (SW128)
@@ -434,7 +439,9 @@ __host__ __device__ inline void operand_plan(int katoms, int& a_slots, int& b_st
 }  // namespace tc2
 
 // Epilogue chunk when the bias is already in the accumulator (s = ||c||^2/2 - x.c).
-FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, float (&bestv)[32]) {
+template <bool S = false>
+FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, float (&bestv)[32],
+                          float& m2) {
   const float* s = reinterpret_cast<const float*>(v);
   float a[11];
 #pragma unroll
@@ -446,6 +453,9 @@ FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, f
   const float b3 = fminf(a[9], a[10]);
   const float mc = fmin3(b0, b1, fminf(b2, b3));
   const bool p = mc < M;
+  // split: every chunk other than the winner's bounds the second best from
+  // below by its minimum (the winner's own chunk is scanned at the end)
+  if constexpr (S) m2 = fminf(m2, fmaxf(M, mc));
   if (__any_sync(0xffffffffu, p)) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) bestv[j] = p ? s[j] : bestv[j];
@@ -469,8 +479,9 @@ FK_DEV float min_tree32(const float* s) {
 // Two adjacent chunks at once: independent min trees (ILP), one warp vote and
 // one conditional copy per pair.  Chunk a holds the lower columns, so strict
 // '<' in order a then b keeps the lowest index on ties, as epi_chunk_aug does.
+template <bool S = false>
 FK_DEV void epi_chunk2_aug(const uint32_t (&va)[32], const uint32_t (&vb)[32], int cola, int colb,
-                           float& M, int& best, float (&bestv)[32]) {
+                           float& M, int& best, float (&bestv)[32], float& m2) {
   const float* sa = reinterpret_cast<const float*>(va);
   const float* sb = reinterpret_cast<const float*>(vb);
   const float mca = min_tree32(sa);
@@ -478,6 +489,7 @@ FK_DEV void epi_chunk2_aug(const uint32_t (&va)[32], const uint32_t (&vb)[32], i
   const bool pa = mca < M;
   const float Ma = pa ? mca : M;
   const bool pb = mcb < Ma;
+  if constexpr (S) m2 = fminf(fminf(m2, fmaxf(M, mca)), fmaxf(Ma, mcb));
   if (__any_sync(0xffffffffu, pa || pb)) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) bestv[j] = pb ? sb[j] : (pa ? sa[j] : bestv[j]);
@@ -496,7 +508,7 @@ FK_DEV void epi_chunk2_aug(const uint32_t (&va)[32], const uint32_t (&vb)[32], i
 //              accumulate onto the seed.  No extra MMA step, no fp16 range
 //              issue, still a pure min-reduction epilogue.
 // BIAS = 0 (epilogue bias): bias added in the epilogue from a smem ring.
-template <int FMT, int BIAS, bool ALT>
+template <int FMT, int BIAS, bool ALT, bool SPLIT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     fk_assign_tc2_kernel(const __grid_constant__ CUtensorMap tmx,
                          const __grid_constant__ CUtensorMap tmc,
@@ -517,6 +529,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   float* xch_m = reinterpret_cast<float*>(smem + OFF_XCH);
   int* xch_i = reinterpret_cast<int*>(smem + OFF_XCH + BM * 4);
   float* xch_xn = reinterpret_cast<float*>(smem + OFF_XCH + BM * 8);
+  float* xch_m2 = reinterpret_cast<float*>(smem + OFF_XCH + BM * 12);
+  static_assert(!SPLIT || BIAS == 1, "split runs with the bias in the GEMM");
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* a_full = bars + 0;
   uint64_t* a_empty = bars + A_SLOTS_MAX;
@@ -682,7 +696,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             const uint64_t adesc = make_sdesc_sw128(a_base + ka * A_ATOM);
             const uint64_t bdesc = make_sdesc_sw128(smem_u32(sB + stage * B_STAGE));
             if (elect_one()) {
-              if (p.debug_mode != 2) {
+              if constexpr (SPLIT) {
+                // C step sc = 4 ka + k of the [c_hi | c_lo] row: c_hi steps meet
+                // x_hi and x_lo, c_lo steps meet x_hi (x_lo . c_lo is dropped)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                  const int sc = 4 * ka + k;
+                  if (sc < 2 * p.ns && p.debug_mode != 2) {
+                    const int sa = sc < p.ns ? sc : sc - p.ns;
+                    const uint64_t ad = make_sdesc_sw128(a_base + (sa >> 2) * A_ATOM) + 2 * (sa & 3);
+                    tc_mma_f16_cg2(d_tmem, ad, bdesc + 2 * k, idesc_main, sc != 0);
+                    if (sc < p.ns) {
+                      const int sl = sc + p.ns;
+                      const uint64_t al = make_sdesc_sw128(a_base + (sl >> 2) * A_ATOM) + 2 * (sl & 3);
+                      tc_mma_f16_cg2(d_tmem, al, bdesc + 2 * k, idesc_main, 1u);
+                    }
+                  }
+                }
+              } else if (p.debug_mode != 2) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)  // +32 B along K = +2 in the descriptor's address field
                   tc_mma_f16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc_main,
@@ -783,6 +814,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       if (p.idx_prev && (alt || wg == 0) && row0 + row < p.N)
         prev_id = __ldg(p.idx_prev + (size_t)b * p.N + row0 + row);
       float M = __int_as_float(0x7f800000);
+      float m2 = M;  // split: lower bound on the row's second-best score
       int best = -1;
       float bestv[32];
 #pragma unroll
@@ -800,9 +832,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         uint32_t va[32], vb[32];
         FK_TMEM_LD_32x32b_X32(taddr, va);
         if (c == 0) {  // ALT: the owning warpgroup; else each warpgroup half the chunk positions
-          xn = alt ? row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane)
-                   : row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane, 4 * wg,
-                                        4 * wg + 4);
+          if (!SPLIT)  // (split: the exact norms come from the certify pass)
+            xn = alt ? row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane)
+                     : row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane, 4 * wg,
+                                          4 * wg + 4);
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_empty[slot]);
         }
@@ -824,7 +857,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         };
         auto chunk = [&](uint32_t (&v)[32], int ch) {
           if (NEG)
-            epi_chunk_aug(v, col0 + 32 * ch, M, best, bestv);
+            epi_chunk_aug<SPLIT>(v, col0 + 32 * ch, M, best, bestv, m2);
           else
             epi_chunk(v, cnp + 128 * ch, col0 + 32 * ch, M, best, bestv);
         };
@@ -846,7 +879,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               release_tmem();  // every TMEM read of this buffer has landed
               if (tr) trace_ev(p, g, 3);
             }
-            epi_chunk2_aug(va, vb, col0 + 32 * ch, col0 + 32 * (ch + 1), M, best, bestv);
+            epi_chunk2_aug<SPLIT>(va, vb, col0 + 32 * ch, col0 + 32 * (ch + 1), M, best, bestv, m2);
             if (ch + 2 < nch) {
               FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 2), va);
               FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 3), vb);
@@ -885,18 +918,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
 #pragma unroll
         for (int j = 31; j >= 0; --j) found = (bestv[j] == M) ? j : found;
         idx = best + found;
+        if constexpr (SPLIT) {  // the rest of the winning chunk
+#pragma unroll
+          for (int j = 0; j < 32; ++j) m2 = j != found ? fminf(m2, bestv[j]) : m2;
+        }
       }
       if (!alt) {
         if (wg == 1) {
           xch_m[row] = M;
           xch_i[row] = idx;
           xch_xn[row] = xn;
+          if (SPLIT) xch_m2[row] = m2;
         }
         named_bar_sync(1, 256);
         if (wg == 0) {
           xn += xch_xn[row];
           const float M1 = xch_m[row];
           const int i1 = xch_i[row];
+          if (SPLIT) m2 = fminf(fminf(m2, xch_m2[row]), fmaxf(M, M1));
           if (M1 < M || (M1 == M && i1 >= 0 && (idx < 0 || i1 < idx))) {
             M = M1;
             idx = i1;
@@ -909,8 +948,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         if (grow < p.N) {
           const size_t o = (size_t)b * p.N + grow;
           p.idx_out[o] = idx;
-          p.mind_out[o] = fmaxf(0.f, NEG ? fmaf(2.f, M, xn) : xn + M);
-          if (p.idx_prev) ch = prev_id != idx;
+          if (SPLIT) {  // raw scores: the certify pass decides and computes the distance
+            p.mind_out[o] = M;
+            p.second_out[o] = m2;
+          } else {
+            p.mind_out[o] = fmaxf(0.f, NEG ? fmaf(2.f, M, xn) : xn + M);
+            if (p.idx_prev) ch = prev_id != idx;
+          }
         }
         if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
       }
@@ -925,7 +969,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   }
 }
 
-template <int FMT, int BIAS, bool ALT>
+template <int FMT, int BIAS, bool ALT, bool SPLIT = false>
 static cudaError_t launch_pair_t(const CUtensorMap& tmx, const CUtensorMap& tmc,
                                  const CUtensorMap& tmext, TcArgs a, int pairs,
                                  cudaStream_t stream) {
@@ -933,11 +977,11 @@ static cudaError_t launch_pair_t(const CUtensorMap& tmx, const CUtensorMap& tmc,
   int dev = 0;
   cudaGetDevice(&dev);
   if (!(attr_dev_mask & (1 << (dev & 31)))) {
-    cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, BIAS, ALT>,
+    cudaFuncSetAttribute(fk_assign_tc2_kernel<FMT, BIAS, ALT, SPLIT>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES);
     attr_dev_mask |= 1 << (dev & 31);
   }
-  fk_assign_tc2_kernel<FMT, BIAS, ALT><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(
+  fk_assign_tc2_kernel<FMT, BIAS, ALT, SPLIT><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(
       tmx, tmc, tmext, a);
   return cudaGetLastError();
 }
@@ -1037,6 +1081,8 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     a.epi2 = e2 ? (e2[0] == '1') : (a.ncol <= 4);
   }
   a.trace = nullptr;
+  a.ns = 0;
+  a.second_out = nullptr;
   static unsigned long long* trace_buf = nullptr;
   const char* trace_path = getenv("FK_ASSIGN_TRACE");
   if (trace_path) {
@@ -1096,6 +1142,51 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     fk_assign_tc_kernel<0><<<grid, tc::THREADS, tc::SMEM_BYTES, stream>>>(tmx, tmc, a);
   }
   return cudaGetLastError();
+}
+
+// Split operands (fk_assign_split.cu): X2 (B, N, 32 ns) and C2 (B, K, 32 ns)
+// bf16 rows [hi (16 ns) | lo (16 ns)], bias operand ext (B, kpad, 16).
+// Writes the estimated argmin ids, its score (||c||^2/2 - x.c) and a lower
+// bound on the row's second-best score.
+cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* ext, int64_t B,
+                                   int64_t N, int64_t K, int ns, int32_t* idx_out, float* est_out,
+                                   float* second_out, int num_sms, cudaStream_t stream) {
+  if (ns < 1 || 2 * ns > 4 * tc2::KATOMS_MAX) return cudaErrorInvalidValue;
+  const int64_t W = 32 * (int64_t)ns;
+  TcArgs a;
+  a.B = (int)B;
+  a.N = (int)N;
+  a.K = (int)K;
+  a.d = (int)W;
+  a.katoms = (int)((W + 63) / 64);
+  a.ncol = (int)((K + tc::BN - 1) / tc::BN);
+  a.kpad = a.ncol * tc::BN;
+  a.cn = nullptr;
+  a.idx_out = idx_out;
+  a.mind_out = est_out;
+  a.idx_prev = nullptr;
+  a.changed = nullptr;
+  {
+    const char* dm = getenv("FK_ASSIGN_DEBUG_MODE");
+    a.debug_mode = dm ? atoi(dm) : 0;
+    const char* e2 = getenv("FK_ASSIGN_EPI2");
+    a.epi2 = e2 ? (e2[0] == '1') : (a.ncol <= 4);
+  }
+  a.trace = nullptr;
+  a.ns = ns;
+  a.second_out = second_out;
+  CUtensorMap tmx2, tmc2, tmext;
+  if (!make_map(&tmx2, X2, 1, W, N, B, tc2::BM)) return cudaErrorInvalidValue;
+  if (!make_map(&tmc2, C2, 1, W, K, B, tc2::BNH)) return cudaErrorInvalidValue;
+  if (!make_map(&tmext, ext, 1, 16, a.kpad, B, tc2::BNH, 16, CU_TENSOR_MAP_SWIZZLE_32B))
+    return cudaErrorInvalidValue;
+  a.tiles_per_batch = (a.N + 2 * tc2::BM - 1) / (2 * tc2::BM);
+  a.total_tiles = a.B * a.tiles_per_batch;
+  int pairs = num_sms / 2;
+  if (a.total_tiles < pairs) pairs = a.total_tiles;
+  if (pairs <= 0) return cudaSuccess;
+  return a.ncol == 1 ? launch_pair_t<1, 1, true, true>(tmx2, tmc2, tmext, a, pairs, stream)
+                     : launch_pair_t<1, 1, false, true>(tmx2, tmc2, tmext, a, pairs, stream);
 }
 
 int assign_tc_kpad(int64_t K) { return (int)(((K + tc::BN - 1) / tc::BN) * tc::BN); }

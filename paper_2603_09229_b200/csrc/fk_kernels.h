@@ -18,6 +18,10 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
                              int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
                              int32_t* changed, int num_sms, cudaStream_t stream);
 
+cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* ext, int64_t B,
+                                   int64_t N, int64_t K, int ns, int32_t* idx_out, float* est_out,
+                                   float* second_out, int num_sms, cudaStream_t stream);
+
 // fk_assign_exact.cu
 cudaError_t launch_cn_pad(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
                           float* cn_pad, cudaStream_t stream, float scale = 1.0f);
@@ -30,6 +34,31 @@ cudaError_t launch_assign_exact(int dt, const void* X, const void* C, const void
                                 const void* cn, int64_t B, int64_t N, int64_t K, int64_t d,
                                 int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
                                 int32_t* changed, cudaStream_t stream);
+cudaError_t launch_assign_exact_rows(int dt, const void* X, const void* C, const void* xn,
+                                     const void* cn, int64_t B, int64_t N, int64_t K, int64_t d,
+                                     const int32_t* list, const int32_t* list_cnt,
+                                     int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+                                     int32_t* changed, cudaStream_t stream);
+
+// fk_assign_split.cu
+bool assign_split_supported(int64_t d);
+int split_steps(int64_t d);
+cudaError_t launch_split_rows(int dt, const void* M, int64_t rows, int64_t d, void* out,
+                              int num_sms, cudaStream_t s);
+cudaError_t launch_split_centroids(int dt, const void* C, int64_t B, int64_t K, int64_t d,
+                                   int kpad, void* c2, void* ext, unsigned int* cmax, void* ct,
+                                   cudaStream_t s);
+cudaError_t launch_fallback_rows(int dt, const void* X, const void* C, const void* ct,
+                                 const void* cn, const void* xn_ref, const unsigned int* cmax,
+                                 int64_t B, int64_t N, int64_t K, int64_t d, const int32_t* list,
+                                 const int32_t* list_cnt, int32_t* idx_out, void* mind_out,
+                                 const int32_t* idx_prev, int32_t* changed, int num_sms,
+                                 cudaStream_t s);
+cudaError_t launch_certify(int dt, const void* X, const void* C, const void* cn_ref,
+                           const unsigned int* cmax, int64_t B, int64_t N, int64_t K, int64_t d,
+                           const int32_t* ids, const float* est, const float* second, void* xn_out,
+                           void* mind_out, const int32_t* idx_prev, int32_t* changed,
+                           int32_t* list, int32_t* list_cnt, int fast, cudaStream_t s);
 cudaError_t launch_assign_cuda_core_lowp(int dt, const void* X, const void* C, const float* cn,
                                          int64_t B, int64_t N, int64_t K, int64_t d,
                                          int32_t* idx_out, float* mind_out,
@@ -88,6 +117,7 @@ cudaError_t launch_kmeanspp(int dt, const void* X, int64_t B, int64_t N, int64_t
 
 // FK_MODULE_ANCHOR of each translation unit (fk_preload)
 const void* module_anchor_assign_exact();
+const void* module_anchor_assign_split();
 const void* module_anchor_assign_tc();
 const void* module_anchor_kmeanspp();
 const void* module_anchor_select();

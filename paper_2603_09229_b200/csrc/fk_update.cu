@@ -1146,6 +1146,71 @@ size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d) {
   return update_ws_layout(B, N, K, d, kMaxSms, nullptr, nullptr);
 }
 
+// ------------------------------------------------------- serial f64 segsum
+// f64 data (the reference's default precision): f64 addition of f64 addends
+// is not associative, so the sums must follow the reference's order exactly
+// (sort_inverse.py:106-149, _kernels.py:135-171): per batch element the stable
+// sorted order is cut into spans of `chunk` positions; each (span, key) run is
+// summed serially from 0.0 in sorted order (segment_stats), and the runs are
+// merged into the key's sum in ascending span order, again from 0.0
+// (merge_segments).  A streamed chunk's result is added to the running sums
+// (PartialStats.combine, pipeline.py:250-257) when `accumulate`.
+// One warp per (key, 32-feature group): lane f walks the key's run and keeps
+// exactly that order; U rows are gathered ahead (independent loads) before
+// the dependent adds.  Bandwidth-bound when the clusters are balanced; the
+// longest cluster's run is the serial critical path.
+template <int U>
+__global__ void __launch_bounds__(256)
+    k_segsum_serial(const double* __restrict__ X, const int32_t* __restrict__ order,
+                    const int64_t* __restrict__ off, int64_t BK, int64_t K, int d, int fgs,
+                    int64_t chunk, double* __restrict__ sums, int accumulate) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= BK * fgs) return;
+  const int64_t key = warp / fgs;
+  const int f = (int)(warp - key * fgs) * 32 + lane;
+  const bool act = f < d;
+  const int64_t b = key / K;
+  const int64_t s = off[key], e = off[key + 1], base = off[b * K];
+  int64_t nb = base + ((s - base) / chunk + 1) * chunk;  // first span start after s
+  double tot = 0.0, acc = 0.0;
+  for (int64_t p0 = s; p0 < e; p0 += U) {
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + u;
+      const int64_t row = p < e ? (int64_t)__ldg(order + p) : 0;
+      v[u] = (act && p < e) ? __ldg(X + row * d + f) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = p0 + u;
+      if (p < e) {
+        if (p == nb) {  // span boundary: merge the finished segment
+          tot = __dadd_rn(tot, acc);
+          acc = 0.0;
+          nb += chunk;
+        }
+        acc = __dadd_rn(acc, v[u]);
+      }
+    }
+  }
+  tot = __dadd_rn(tot, acc);
+  if (act) {
+    double* o = sums + key * d + f;
+    *o = accumulate ? __dadd_rn(*o, tot) : tot;
+  }
+}
+
+static bool segsum_f64_serial() {
+  static int v = -1;  // FK_SEGSUM_F64=parallel: the slice-parallel k_segsum for f64 (A/B)
+  if (v < 0) {
+    const char* e = getenv("FK_SEGSUM_F64");
+    v = (e && e[0] == 'p') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <typename T, typename A>
 static cudaError_t dispatch_segsum(const void* X, const UpdateWs& w, int64_t BK, int64_t P, int64_t d,
                                    double* sums, int num_sms, cudaStream_t s, const int32_t* ids,
@@ -1336,7 +1401,15 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
     case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, w, BK, P, d, sums, sms, s, ids, N, K);
     case DT_F16: return dispatch_segsum<__half, float>(X, w, BK, P, d, sums, sms, s, ids, N, K);
     case DT_F32: return dispatch_segsum<float, double>(X, w, BK, P, d, sums, sms, s, ids, N, K);
-    default: return dispatch_segsum<double, double>(X, w, BK, P, d, sums, sms, s, ids, N, K);
+    default:
+      if (segsum_f64_serial()) {
+        const int fgs = (int)((d + 31) / 32);
+        const int64_t threads = BK * fgs * 32;
+        k_segsum_serial<8><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+            (const double*)X, w.order, w.off, BK, K, (int)d, fgs, ch, sums, accumulate);
+        return cudaGetLastError();
+      }
+      return dispatch_segsum<double, double>(X, w, BK, P, d, sums, sms, s, ids, N, K);
   }
 }
 

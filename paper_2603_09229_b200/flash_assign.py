@@ -139,5 +139,5 @@ def flash_assign(x: DataMatrix, c: Centroids, tiling: TilingConfig, counters: Co
     dev = device_of(x.data)
     xd = to_device(x.data, dev)
     cd = to_device(c.data, dev)
-    ids, mind = ops.assign(xd, cd)
+    ids, mind = ops.assign(xd, cd, dot_mode=dot_mode)
     return Assignments(ids, validate=False, id_bound=c.clusters), mind, counters

@@ -8,6 +8,7 @@ tensors.  Nothing here computes on the host; nothing synchronizes.
 
 from __future__ import annotations
 
+import os
 import threading
 
 import torch
@@ -82,21 +83,88 @@ def assign_bias(c: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tenso
     return out
 
 
+def split_supported(x: torch.Tensor) -> bool:
+    """f32/f64 data whose rows the certified tensor-core assign takes (d <= 128)."""
+    B, n, d = x.shape
+    return x.dtype in (torch.float32, torch.float64) and N.lib().fk_assign_xsplit_bytes(
+        fk_dtype(x.dtype), B, n, d) > 0
+
+
+def assign_xsplit(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """The bf16 [hi | lo] split operand of f32/f64 data (B,N,d), d <= 128:
+    (B, N, 32*ceil(d/16)) bf16.  Build once per data set and pass it to
+    ``assign(xsplit=)`` while X is unchanged."""
+    dev = _require_cuda(x)
+    x = x.contiguous()
+    B, n, d = x.shape
+    if not split_supported(x):
+        raise ValueError("the split operand needs float32/float64 data with d <= 128")
+    w = 32 * (-(-d // 16))
+    if out is None:
+        out = torch.empty((B, n, w), dtype=torch.bfloat16, device=dev)
+    N.check(N.lib().fk_assign_xsplit(fk_dtype(x.dtype), x.data_ptr(), B, n, d, out.data_ptr(),
+                                     _stream(dev)), "fk_assign_xsplit")
+    return out
+
+
+def split_fallback_rows(x: torch.Tensor, clusters: int) -> list:
+    """Diagnostic: rows per batch element that the last certified assign of
+    this shape (on this thread and stream) sent to the exact fallback."""
+    import ctypes
+
+    dev = _require_cuda(x)
+    B, n, d = x.shape
+    ws = _ws.get(dev, 1, "assign")
+    out = (ctypes.c_int32 * B)()
+    N.check(N.lib().fk_assign_split_fallback_rows(fk_dtype(x.dtype), B, n, int(clusters), d, ws.data_ptr(),
+                                                  ctypes.addressof(out), _stream(dev)),
+            "fk_assign_split_fallback_rows")
+    return list(out)
+
+
+_DOT = {"exact": 0, "fast": 1, "mirror": 2}
+SPLIT_MIN_MACS = 6.7e7  # fk_api.cu split_auto: below this the exact mirror is faster
+
+
+def split_auto(x: torch.Tensor, clusters: int) -> bool:
+    """Whether ``assign`` on this data picks the certified tensor-core path by
+    itself (same rule as the library: FK_ASSIGN_F32=mirror|split overrides)."""
+    if not split_supported(x):
+        return False
+    env = os.environ.get("FK_ASSIGN_F32", "")
+    if env[:1] in ("m", "s"):
+        return env[0] == "s"
+    B, n, d = x.shape
+    return float(B) * n * clusters * d >= SPLIT_MIN_MACS
+
+
 def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = None,
            changed: torch.Tensor | None = None, idx_out: torch.Tensor | None = None,
-           mind_out: torch.Tensor | None = None, bias: torch.Tensor | None = None):
+           mind_out: torch.Tensor | None = None, bias: torch.Tensor | None = None,
+           xsplit: torch.Tensor | None = None, dot_mode: str = "exact", path: str = "auto"):
     """Nearest centroid per point: (ids int32 (B,N), min_dists (B,N)).
 
     min_dists is in the data dtype for float32/float64 data and float32 for
     bfloat16/float16 data.  If ``idx_prev`` is given, ``changed`` (int32
     device scalar) is OR-ed with 1 when any id differs.  ``bias`` (bf16/fp16
     only): the precomputed ``assign_bias(c)``.
+
+    float32/float64 data (the reference's dot modes, flash_assign.py:203-208):
+    ``dot_mode="exact"`` is bitwise equal to the reference; for d <= 128 it
+    runs the certified tensor-core path (``xsplit``: the cached
+    ``assign_xsplit(x)``).  ``"fast"`` (the reference's relaxed mode) is
+    served by the same certified path, so it returns the exact answer.  ``path``: "auto" | "split" | "mirror" (the exact
+    CUDA-core kernel for every row) -- A/B and tests.
     """
     dev = _require_cuda(x, c)
     if x.dim() != 3 or c.dim() != 3 or x.shape[0] != c.shape[0] or x.shape[2] != c.shape[2]:
         raise ValueError("x must be (B,N,d) and c (B,K,d) with matching B and d")
     if x.dtype != c.dtype:
         raise ValueError("data and centroids must share one precision")
+    if dot_mode not in ("exact", "fast"):
+        raise ValueError("dot_mode must be 'exact' or 'fast'")
+    if path not in ("auto", "split", "mirror"):
+        raise ValueError("path must be 'auto', 'split' or 'mirror'")
     x = x.contiguous()
     c = c.contiguous()
     B, n, d = x.shape
@@ -108,6 +176,22 @@ def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = Non
         mdt = torch.float32 if x.dtype in LOWP else x.dtype
         mind_out = torch.empty((B, n), dtype=mdt, device=dev)
     L = N.lib()
+    if x.dtype not in LOWP and (xsplit is not None or dot_mode == "fast" or path != "auto"):
+        mode = "mirror" if path == "mirror" or not split_supported(x) else dot_mode
+        if mode != "mirror" and xsplit is None:
+            xsplit = assign_xsplit(x)
+        if xsplit is not None and (xsplit.dtype != torch.bfloat16 or xsplit.shape[:2] != (B, n)
+                                   or not xsplit.is_contiguous()):
+            raise ValueError("xsplit must be the (B, N, w) bf16 assign_xsplit(x) of this data")
+        need = L.fk_assign_split_workspace(dt, B, n, K, d)
+        ws = _ws.get(dev, need, "assign")
+        st = L.fk_assign_split(dt, x.data_ptr(), None if mode == "mirror" else xsplit.data_ptr(),
+                               c.data_ptr(), B, n, K, d, _DOT[mode], idx_out.data_ptr(),
+                               mind_out.data_ptr(), None if idx_prev is None else idx_prev.data_ptr(),
+                               None if changed is None else changed.data_ptr(), ws.data_ptr(),
+                               ws.numel(), _stream(dev))
+        N.check(st, "fk_assign_split")
+        return idx_out, mind_out
     need = L.fk_assign_workspace(dt, B, n, K, d)
     ws = _ws.get(dev, need, "assign")
     st = L.fk_assign(dt, x.data_ptr(), c.data_ptr(), None if bias is None else bias.data_ptr(),

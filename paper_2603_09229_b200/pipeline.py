@@ -118,6 +118,10 @@ class LloydEngine:
         # tensor-core bias operand of the next centroids comes out of normalize
         self.fused = backend is None and allreduce is None
         self.bias = None
+        # f32/f64 data: the split operand of X for the certified tensor-core
+        # assign, built once (X never changes during a run)
+        self.xsplit = ops.assign_xsplit(self.x) if backend is None and ops.split_auto(
+            self.x, K) else None
         if self.fused:
             from .ops import OBJ_BLOCK
 
@@ -146,6 +150,8 @@ class LloydEngine:
             ops.assign_bias(self.operand[slot], out=self.bias[slot])
 
     def _assign_kw(self, csrc: int) -> dict:
+        if self.xsplit is not None:
+            return {"xsplit": self.xsplit}
         return {} if self.bias is None else {"bias": self.bias[csrc]}
 
     def _normalize(self, nxt: int) -> None:

@@ -1,0 +1,75 @@
+"""f64 data (the reference's default precision): the device update is bitwise
+equal to the reference's sort_inverse_update, whose f64 sums depend on the
+addition order (sort_inverse.py:106-149: spans of `chunk` sorted positions,
+serial segment sums, in-order merges; _kernels.py:135-171), and a streamed
+pass equals the reference's in-order PartialStats fold (pipeline.py:250-257,
+360-365).  The oracle's restatement is pinned to the live reference in
+tests/test_oracle_*.py."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    from paper_2603_09229_b200 import ops
+
+    return ops
+
+
+def rough_data(rng, B, N, d):
+    # magnitudes spread over many binades: f64 sums round, so order matters
+    return (rng.standard_normal((B, N, d)) * np.exp(rng.uniform(-20, 20, (B, N, 1)))).astype(np.float64)
+
+
+@pytest.mark.parametrize("B,N,K,d,chunk", [
+    (1, 1, 1, 1, 1), (1, 1000, 8, 16, 256), (2, 5000, 37, 33, 777), (1, 20000, 300, 64, 20000),
+    (3, 4096, 64, 128, 1000), (1, 9000, 1, 5, 64), (1, 3000, 4000, 24, 512),
+])
+def test_update_f64_bitwise(ops, B, N, K, d, chunk):
+    rng = np.random.default_rng(N + K + d)
+    x = rough_data(rng, B, N, d)
+    ids = rng.integers(0, K, (B, N)).astype(np.int32)
+    if K > 3:
+        ids[:, : N // 3] = 2  # one heavy cluster spanning many spans
+    s_ref, c_ref, m_ref = O.sort_inverse_update(x, ids, K, chunk)
+    merges = torch.zeros((), dtype=torch.int64, device="cuda")
+    s, c = ops.update(torch.from_numpy(x).cuda(), torch.from_numpy(ids).cuda(), K, chunk, merges=merges)
+    assert np.array_equal(c.cpu().numpy(), c_ref)
+    assert np.array_equal(s.cpu().numpy().view(np.uint64), s_ref.view(np.uint64))
+    assert int(merges) == m_ref
+
+
+def test_update_f64_streamed_fold(ops):
+    """Chunks accumulated in ascending order equal the reference's fold of
+    per-chunk partials: running = running + part (pipeline.py:360-365)."""
+    rng = np.random.default_rng(1)
+    B, N, K, d, pts, chunk = 2, 10000, 50, 40, 3000, 700
+    x = rough_data(rng, B, N, d)
+    ids = rng.integers(0, K, (B, N)).astype(np.int32)
+    ref = None
+    xd, idd = torch.from_numpy(x).cuda(), torch.from_numpy(ids).cuda()
+    sums = torch.empty((B, K, d), dtype=torch.float64, device="cuda")
+    counts = torch.empty((B, K), dtype=torch.int64, device="cuda")
+    for lo in range(0, N, pts):
+        hi = min(lo + pts, N)
+        part, _, _ = O.sort_inverse_update(x[:, lo:hi], ids[:, lo:hi], K, chunk)
+        ref = part if ref is None else ref + part
+        ops.update(xd[:, lo:hi].contiguous(), idd[:, lo:hi].contiguous(), K, chunk,
+                   accumulate=lo > 0, sums=sums, counts=counts)
+    assert np.array_equal(sums.cpu().numpy().view(np.uint64), ref.view(np.uint64))
+
+
+def test_update_f64_repeatable(ops):
+    rng = np.random.default_rng(2)
+    x = torch.from_numpy(rough_data(rng, 1, 50000, 64)).cuda()
+    ids = torch.from_numpy(rng.integers(0, 128, (1, 50000)).astype(np.int32)).cuda()
+    s1, _ = ops.update(x, ids, 128, 4096)
+    s1 = s1.clone()
+    s2, _ = ops.update(x, ids, 128, 4096)
+    assert torch.equal(s1.view(torch.int64), s2.view(torch.int64))
