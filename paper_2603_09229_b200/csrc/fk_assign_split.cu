@@ -117,8 +117,9 @@ FK_DEV double prod_term(double x, double c) { return __dmul_rn(x, c); }
 // One thread per row: the reference's ||x||^2 (kept for the fallback), the
 // margin test, and for certified rows the reference distance to the chosen
 // centroid.  Rows that do not certify go to the per-batch fallback list.
-// The block's 128 rows and their chosen centroid rows are staged through
-// shared memory DC columns at a time (coalesced row reads), then each thread
+// The block's 128 rows and their chosen centroid rows stream through shared
+// memory DC columns at a time (coalesced row reads, double-buffered: the next
+// chunk's loads are in flight while the current one is summed); each thread
 // runs its two serial f64 chains in ascending j, the reference's order.
 template <typename T>
 __global__ void __launch_bounds__(128)
@@ -128,9 +129,9 @@ __global__ void __launch_bounds__(128)
               const float* __restrict__ second, T* __restrict__ xn_out, T* __restrict__ mind_out,
               const int32_t* __restrict__ idx_prev, int32_t* changed, int32_t* __restrict__ list,
               int32_t* __restrict__ list_cnt, int fast) {
-  constexpr int DC = 16;
-  __shared__ T xs[DC][129];
-  __shared__ T cs[DC][129];
+  constexpr int DC = sizeof(T) == 4 ? 16 : 8;
+  __shared__ T xs[2][DC][129];
+  __shared__ T cs[2][DC][129];
   __shared__ int32_t sid[128];
   const int64_t b = blockIdx.y;
   const int64_t row0 = blockIdx.x * (int64_t)128;
@@ -141,23 +142,38 @@ __global__ void __launch_bounds__(128)
   if (row < N) id = ids[o];
   const bool valid = id >= 0 && id < K;
   sid[tid] = valid ? id : -1;
-  double xa = 0.0, da = 0.0;
-  for (int j0 = 0; j0 < d; j0 += DC) {
-    __syncthreads();
-#pragma unroll 8
-    for (int e = tid; e < 128 * DC; e += 128) {  // 16 loads in flight per thread
+  __syncthreads();
+  T px[DC], pc[DC];
+  auto fetch = [&](int j0) {
+#pragma unroll
+    for (int i = 0; i < DC; ++i) {
+      const int e = tid + 128 * i;
       const int r = e / DC, jj = e - r * DC;
       const int64_t gr = row0 + r;
       const int j = j0 + jj;
       const bool in = gr < N && j < d;
-      xs[jj][r] = in ? X[(b * N + gr) * d + j] : (T)0;
       const int32_t cid = sid[r];
-      cs[jj][r] = (in && cid >= 0) ? C[(b * K + cid) * d + j] : (T)0;
+      px[i] = in ? __ldg(X + (b * N + gr) * d + j) : (T)0;
+      pc[i] = (in && cid >= 0) ? __ldg(C + (b * K + cid) * d + j) : (T)0;
+    }
+  };
+  double xa = 0.0, da = 0.0;
+  const int nch = (d + DC - 1) / DC;
+  fetch(0);
+  for (int c = 0; c < nch; ++c) {
+    const int buf = c & 1;
+#pragma unroll
+    for (int i = 0; i < DC; ++i) {
+      const int e = tid + 128 * i;
+      const int r = e / DC, jj = e - r * DC;
+      xs[buf][jj][r] = px[i];
+      cs[buf][jj][r] = pc[i];
     }
     __syncthreads();
-    const int jn = d - j0 < DC ? d - j0 : DC;
+    if (c + 1 < nch) fetch((c + 1) * DC);
+    const int jn = d - c * DC < DC ? d - c * DC : DC;
     for (int jj = 0; jj < jn; ++jj) {
-      const T xv = xs[jj][tid], cv = cs[jj][tid];
+      const T xv = xs[buf][jj][tid], cv = cs[buf][jj][tid];
       xa = __dadd_rn(xa, prod_term(xv, xv));
       da = __dadd_rn(da, prod_term(xv, cv));
     }
@@ -203,7 +219,8 @@ __global__ void __launch_bounds__(128)
 // The rows k_certify could not settle.  Two stages per row, both sweeping
 // the centroids in tiles of 128 with the fp32 transposed C staged in shared
 // memory (coalesced, shared by the block's FB_W * FB_R rows; lane = centroid
-// in a 32-wide group, 4 groups x FB_R rows of independent chains):
+// owns 4 consecutive centroids of the tile, FB_R rows: 16 independent fp32
+// chains fed by 16-byte shared-memory reads):
 //  A. an fp32 FMA estimate D~_k = xn + cn_k - 2 sum_j x_j c_kj of every
 //     distance and its row minimum dmin;
 //  B. the same estimate again (bitwise the same values), and for every
@@ -226,10 +243,11 @@ __global__ void __launch_bounds__(FB_W * 32)
                     int32_t* __restrict__ idx_out, T* __restrict__ mind_out,
                     const int32_t* __restrict__ idx_prev, int32_t* changed) {
   constexpr int RB = FB_W * FB_R;  // rows per block
-  __shared__ float cts[FB_DC][FB_KT];
-  extern __shared__ uint8_t fb_sm[];
+  __shared__ __align__(16) float cts[FB_DC][FB_KT];
+  extern __shared__ __align__(16) uint8_t fb_sm[];
   float* xf = reinterpret_cast<float*>(fb_sm);  // (RB, d) fp32 copies of the rows
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int dp = (d + 3) & ~3;  // shared row stride: float4 reads
   bool ch = false;
   for (int64_t b = 0; b < B; ++b) {
     const int64_t cnt = list_cnt[b];
@@ -246,8 +264,8 @@ __global__ void __launch_bounds__(FB_W * 32)
         const int64_t i = i0 + wib * FB_R + q;
         const bool live = i < cnt;
         o[q] = live ? b * N + list[b * N + i] : -1;
-        for (int j = lane; j < d; j += 32)
-          xf[(wib * FB_R + q) * d + j] = live ? (float)X[o[q] * d + j] : 0.f;
+        for (int j = lane; j < dp; j += 32)
+          xf[(wib * FB_R + q) * dp + j] = (live && j < d) ? (float)X[o[q] * d + j] : 0.f;
         xn[q] = live ? xn_ref[o[q]] : (T)0;
         xnf[q] = (float)xn[q];
         const float nx = sqrtf(xnf[q]) * (1.f + 0x1p-20f);
@@ -259,7 +277,7 @@ __global__ void __launch_bounds__(FB_W * 32)
         best[q] = (T)__int_as_float(0x7f800000);
         bi[q] = -1;
       }
-      const float* xw = xf + (int64_t)wib * FB_R * d;
+      const float* xw = xf + (int64_t)wib * FB_R * dp;
       for (int stage = 0; stage < 2; ++stage) {
         for (int64_t kb = 0; kb < K; kb += FB_KT) {
           float acc[FB_R][4];
@@ -278,21 +296,28 @@ __global__ void __launch_bounds__(FB_W * 32)
             }
             __syncthreads();
             const int jn = d - j0 < FB_DC ? d - j0 : FB_DC;
-            for (int jj = 0; jj < jn; ++jj) {
-              float cv[4];
+            for (int jj = 0; jj < jn; jj += 4) {  // rows are zero padded to a multiple of 4
+              float4 xv[FB_R];
 #pragma unroll
-              for (int u = 0; u < 4; ++u) cv[u] = cts[jj][32 * u + lane];
+              for (int q = 0; q < FB_R; ++q)
+                xv[q] = *reinterpret_cast<const float4*>(xw + q * dp + j0 + jj);
 #pragma unroll
-              for (int q = 0; q < FB_R; ++q) {
-                const float xv = xw[q * d + j0 + jj];
+              for (int t = 0; t < 4; ++t) {
+                const float4 c4 = *reinterpret_cast<const float4*>(&cts[jj + t][4 * lane]);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) acc[q][u] = fmaf(xv, cv[u], acc[q][u]);
+                for (int q = 0; q < FB_R; ++q) {
+                  const float x1 = t == 0 ? xv[q].x : t == 1 ? xv[q].y : t == 2 ? xv[q].z : xv[q].w;
+                  acc[q][0] = fmaf(x1, c4.x, acc[q][0]);
+                  acc[q][1] = fmaf(x1, c4.y, acc[q][1]);
+                  acc[q][2] = fmaf(x1, c4.z, acc[q][2]);
+                  acc[q][3] = fmaf(x1, c4.w, acc[q][3]);
+                }
               }
             }
           }
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int64_t k = kb + 32 * u + lane;
+            const int64_t k = kb + 4 * lane + u;  // the lane's 4 consecutive centroids, ascending
             if (k < K) {
               const T cnk = cn[b * K + k];
 #pragma unroll
@@ -414,7 +439,7 @@ cudaError_t launch_fallback_rows(int dt, const void* X, const void* C, const voi
                                  const int32_t* list_cnt, int32_t* idx_out, void* mind_out,
                                  const int32_t* idx_prev, int32_t* changed, int num_sms,
                                  cudaStream_t s) {
-  const size_t smem = FB_W * FB_R * (size_t)d * 4;
+  const size_t smem = FB_W * FB_R * (size_t)((d + 3) & ~3) * 4;
   const unsigned grid = (unsigned)num_sms * 4;
   if (dt == DT_F64)
     k_fallback_rows<double><<<grid, FB_W * 32, smem, s>>>(
