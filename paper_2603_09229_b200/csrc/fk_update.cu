@@ -1271,8 +1271,19 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
   }
   const unsigned blocks = (unsigned)(B * bpb);
   if (scatter_is_warp(K)) {
+    // warp-table budget per block: 64 KB, or 96 KB from K = 2048 on (K = 4096:
+    // 8 warps per block instead of 4; config 3 459.6 vs 469.9 us, configs 2
+    // and 4 are slower with wider tables, profiles/r02_ab_sw_table.txt);
+    // FK_SW_TABLE_KB overrides (A/B)
+    static int tab_env = -2;
+    if (tab_env == -2) {
+      const char* e = getenv("FK_SW_TABLE_KB");
+      tab_env = e ? atoi(e) * 1024 : -1;
+      if (e && tab_env < 4096) tab_env = -1;
+    }
+    const int tab_bytes = tab_env > 0 ? tab_env : (K >= 2048 ? 96 * 1024 : SW_TABLE_BYTES);
     int W = 32;
-    while (W > 1 && (int64_t)W * (K + 2) * 2 > SW_TABLE_BYTES) W >>= 1;
+    while (W > 1 && (int64_t)W * (K + 2) * 2 > tab_bytes) W >>= 1;
     const bool alias = (int64_t)W * (K + 2) * 2 >= K * 4;
     const size_t smem = (size_t)((W * (K + 2) * 2 + 15) & ~15) + (size_t)K * (alias ? 4 : 8);
     const bool cols = bpb <= SW_COLS_BPB;
@@ -1283,7 +1294,7 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
     cudaGetDevice(&dev);                                                                           \
     if (!attr_set[dev & 63]) { /* the largest table + bases */                                     \
       cudaFuncSetAttribute(k_scatter_warp<WV, CV>, cudaFuncAttributeMaxDynamicSharedMemorySize,     \
-                           SW_TABLE_BYTES + SW_KMAX * 8 + 16);                                     \
+                           220 * 1024);                                                            \
       attr_set[dev & 63] = true;                                                                   \
     }                                                                                              \
     k_scatter_warp<WV, CV><<<blocks, WV * 32, smem, s>>>(ids, N, K, (int)bpb, w.table, w.hist,     \
