@@ -994,7 +994,13 @@ __global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restr
 static int64_t update_bpb(int64_t B, int64_t N, int64_t K, int num_sms) {
   // ~2 blocks per SM (4 per SM measured no faster at config 3: the larger
   // tables cost k_hist and k_colscan what the scatter gained)
-  int64_t bpb = ((int64_t)num_sms * 2 + B - 1) / B;
+  static int bps = -1;  // FK_UPDATE_BPS: histogram/scatter blocks per SM (A/B)
+  if (bps < 0) {
+    const char* e = getenv("FK_UPDATE_BPS");
+    bps = e ? atoi(e) : 2;
+    if (bps < 1 || bps > 16) bps = 2;
+  }
+  int64_t bpb = ((int64_t)num_sms * bps + B - 1) / B;
   const int64_t max_bpb = (N + SD_S - 1) / SD_S;
   if (bpb > max_bpb) bpb = max_bpb;
   if (K > HIST_SMEM_KEYS) {
