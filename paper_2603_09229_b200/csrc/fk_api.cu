@@ -2,6 +2,7 @@
 // Validation happens here, before any launch (the reference validates before
 // any kernel call: flash_assign.py:152-157, sort_inverse.py:120-122,
 // baseline.py:134-137); kernels never see malformed shapes.
+#include <climits>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -164,8 +165,10 @@ size_t xsplit_bytes(int64_t B, int64_t N, int64_t d) {
 struct SplitWs {
   void *c2, *ext, *cn_ref, *xn_ref, *ct;
   unsigned int* cmax;
-  int32_t *cnt, *list;
+  int32_t *cnt, *list, *rec, *rec_cnt;
+  int8_t* stat;
   float *est, *second;
+  int rec_cap;
   size_t bytes;
 };
 SplitWs split_ws_layout(uint8_t* base, int dt, int64_t B, int64_t N, int64_t K, int64_t d) {
@@ -177,9 +180,14 @@ SplitWs split_ws_layout(uint8_t* base, int dt, int64_t B, int64_t N, int64_t K, 
   w.c2 = take((size_t)B * K * 32 * fk::split_steps(d) * 2);
   w.ext = take((size_t)B * kpad * 32);
   w.cn_ref = take((size_t)B * K * es);
-  w.ct = take((size_t)B * K * d * 4);  // fp32 (B, d, K): the fallback's estimate operand
-  w.cmax = (unsigned int*)take((size_t)B * 8);  // cmax (B) then cnt (B): one memset
+  w.ct = take((size_t)B * K * d * es);  // (B, d, K) transposed C: coalesced candidate columns
+  w.cmax = (unsigned int*)take((size_t)B * 8 + 16);  // cmax (B), cnt (B), rec_cnt: one memset
   w.cnt = base ? (int32_t*)(w.cmax + B) : nullptr;
+  w.rec_cnt = base ? (int32_t*)(w.cmax + 2 * B) : nullptr;
+  const int64_t cap = B * N / 8 + 1024;  // beyond: full fallback
+  w.rec_cap = (int)(cap < INT32_MAX ? cap : INT32_MAX);
+  w.rec = (int32_t*)take((size_t)w.rec_cap * fk::kSplitRecInts * 4);
+  w.stat = (int8_t*)take((size_t)B * N);
   w.est = (float*)take((size_t)B * N * 4);
   w.second = (float*)take((size_t)B * N * 4);
   w.list = (int32_t*)take((size_t)B * N * 4);
@@ -198,18 +206,22 @@ fk_status run_split(int dt, const void* X, const void* xsplit, const void* C, in
   const SplitWs w = split_ws_layout(ws, dt, B, N, K, d);
   const int kpad = fk::assign_tc_kpad(K);
   const DevInfo di = dev_info();
-  fk_status st = cuda_status(cudaMemsetAsync(w.cmax, 0, (size_t)B * 8, s));
+  fk_status st = cuda_status(cudaMemsetAsync(w.cmax, 0, (size_t)B * 8 + 16, s));
   if (st != FK_OK) return st;
   st = cuda_status(fk::launch_split_centroids(dt, C, B, K, d, kpad, w.c2, w.ext, w.cmax, w.ct, s));
   if (st != FK_OK) return st;
   st = cuda_status(fk::launch_row_norms_exact(dt, C, B * K, d, w.cn_ref, s));
   if (st != FK_OK) return st;
   st = cuda_status(fk::launch_assign_tc_split(xsplit, w.c2, w.ext, B, N, K, fk::split_steps(d),
-                                              idx_out, w.est, w.second, di.sms, s));
+                                              idx_out, w.est, w.second, w.cmax, w.stat, w.rec,
+                                              w.rec_cnt, w.rec_cap, di.sms, s));
   if (st != FK_OK) return st;
   st = cuda_status(fk::launch_certify(dt, X, C, w.cn_ref, w.cmax, B, N, K, d, idx_out, w.est,
-                                      w.second, w.xn_ref, mind_out, idx_prev, changed, w.list,
-                                      w.cnt, fast, s));
+                                      w.second, w.stat, w.xn_ref, mind_out, idx_prev, changed,
+                                      w.list, w.cnt, fast, s));
+  if (st != FK_OK) return st;
+  st = cuda_status(fk::launch_candidates(dt, X, w.ct, w.cn_ref, w.xn_ref, w.cmax, N, K, d, w.rec, w.rec_cnt,
+                                         w.rec_cap, idx_out, mind_out, idx_prev, changed, di.sms, s));
   if (st != FK_OK) return st;
   return cuda_status(fk::launch_fallback_rows(dt, X, C, w.ct, w.cn_ref, w.xn_ref, w.cmax, B, N, K,
                                               d, w.list, w.cnt, idx_out, mind_out, idx_prev, changed,

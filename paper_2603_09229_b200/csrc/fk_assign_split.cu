@@ -71,7 +71,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     k_split_centroids(const T* __restrict__ C, int64_t B, int64_t K, int d, int dp, int kpad,
                       __nv_bfloat16* __restrict__ c2, __nv_bfloat16* __restrict__ ext,
-                      unsigned int* __restrict__ cmax, float* __restrict__ ct) {
+                      unsigned int* __restrict__ cmax, T* __restrict__ ct) {
   const int64_t gi = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gi >= B * kpad) return;
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256)
   for (int j = lane; j < dp; j += 32) {
     const T v = j < d ? p[j] : (T)0;
     const __nv_bfloat16 h = to_bf16_rn(v);
-    if (j < d) ct[(b * d + j) * K + k] = (float)v;  // (B, d, K) fp32: the fallback's estimate operand
+    if (j < d) ct[(b * d + j) * K + k] = v;  // (B, d, K): coalesced centroid columns
     q[j] = h;
     q[dp + j] = to_bf16_rn(v - (T)__bfloat162float(h));
     acc = fma((double)v, (double)v, acc);
@@ -126,7 +126,8 @@ __global__ void __launch_bounds__(128)
     k_certify(const T* __restrict__ X, const T* __restrict__ C, const T* __restrict__ cn_ref,
               const unsigned int* __restrict__ cmax, int64_t N, int64_t K, int d,
               const int32_t* __restrict__ ids, const float* __restrict__ est,
-              const float* __restrict__ second, T* __restrict__ xn_out, T* __restrict__ mind_out,
+              const float* __restrict__ second, const int8_t* __restrict__ stat,
+              T* __restrict__ xn_out, T* __restrict__ mind_out,
               const int32_t* __restrict__ idx_prev, int32_t* changed, int32_t* __restrict__ list,
               int32_t* __restrict__ list_cnt, int fast) {
   constexpr int DC = sizeof(T) == 4 ? 16 : 8;
@@ -179,9 +180,10 @@ __global__ void __launch_bounds__(128)
     }
   }
   bool flag = false, ch = false;
-  if (row < N) {
+  if (row < N) xn_out[o] = (T)xa;
+  // stat 1: the epilogue listed this row's candidate chunks (k_candidates)
+  if (row < N && stat[o] != 1) {
     const T xn = (T)xa;
-    xn_out[o] = xn;
     const float cm = __uint_as_float(cmax[b]);
     const float nx = __fsqrt_ru(__double2float_ru(xa)) * (1.0f + 0x1p-20f);
     const float scale = __fmaf_ru(nx, cm, cm * cm);
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(128)
 constexpr int FB_W = 8, FB_R = 4, FB_KT = 128, FB_DC = 32;
 template <typename T>
 __global__ void __launch_bounds__(FB_W * 32)
-    k_fallback_rows(const T* __restrict__ X, const T* __restrict__ C, const float* __restrict__ ct,
+    k_fallback_rows(const T* __restrict__ X, const T* __restrict__ C, const T* __restrict__ ct,
                     const T* __restrict__ cn, const T* __restrict__ xn_ref,
                     const unsigned int* __restrict__ cmax, int64_t B, int64_t N, int64_t K, int d,
                     const int32_t* __restrict__ list, const int32_t* __restrict__ list_cnt,
@@ -251,7 +253,7 @@ __global__ void __launch_bounds__(FB_W * 32)
   bool ch = false;
   for (int64_t b = 0; b < B; ++b) {
     const int64_t cnt = list_cnt[b];
-    const float* ctb = ct + b * d * K;
+    const T* ctb = ct + b * d * K;
     const float cm = __uint_as_float(cmax[b]);
     for (int64_t i0 = (int64_t)blockIdx.x * RB; i0 < cnt; i0 += (int64_t)gridDim.x * RB) {
       int64_t o[FB_R];
@@ -292,7 +294,7 @@ __global__ void __launch_bounds__(FB_W * 32)
               const int jj = e / FB_KT, kk = e - jj * FB_KT;
               const int j = j0 + jj;
               const int64_t k = kb + kk;
-              cts[jj][kk] = (j < d && k < K) ? __ldg(ctb + (int64_t)j * K + k) : 0.f;
+              cts[jj][kk] = (j < d && k < K) ? (float)__ldg(ctb + (int64_t)j * K + k) : 0.f;
             }
             __syncthreads();
             const int jn = d - j0 < FB_DC ? d - j0 : FB_DC;
@@ -376,6 +378,120 @@ __global__ void __launch_bounds__(FB_W * 32)
   if (changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(changed, 1);
 }
 
+// -------------------------------------------------------------- candidates
+// Rows the epilogue could not certify but whose near chunks it listed: the
+// exact argmin is in one of those <= 8 chunks of 32 centroids (a chunk is
+// listed when its estimated minimum came within the certificate margin of the
+// running best).  One warp per record:
+//  1. an fp32 FMA estimate of every listed centroid's distance (lane =
+//     centroid of the chunk, coalesced reads of the transposed C), with the
+//     fallback's rigorous bound thr >= 2 (E + R);
+//  2. the centroids with NOT(D~ > min D~ + thr) -- the exact minimiser and
+//     everything tied with it -- compacted and evaluated with the reference
+//     arithmetic, lanes = candidates; lexicographic (value, id) selection.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    k_candidates(const T* __restrict__ X, const T* __restrict__ ct, const T* __restrict__ cn,
+                 const T* __restrict__ xn_ref, const unsigned int* __restrict__ cmax, int64_t N,
+                 int64_t K, int d, const int32_t* __restrict__ rec,
+                 const int32_t* __restrict__ rec_cnt, int rec_cap, int32_t* __restrict__ idx_out,
+                 T* __restrict__ mind_out, const int32_t* __restrict__ idx_prev, int32_t* changed) {
+  constexpr int NQ = kSplitRecInts - 2;  // chunks per record (max)
+  extern __shared__ __align__(16) uint8_t cd_sm[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  T* xs = reinterpret_cast<T*>(cd_sm) + (int64_t)wib * d;
+  __shared__ int32_t cand[8][NQ * 32];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t cnt = *rec_cnt < rec_cap ? *rec_cnt : rec_cap;
+  bool ch = false;
+  for (int64_t i = gw; i < cnt; i += nw) {
+    const int32_t* r = rec + i * kSplitRecInts;
+    const int64_t o = r[0];
+    const int64_t b = o / N;
+    const int n = r[1];
+    __syncwarp();
+    for (int j = lane; j < d; j += 32) xs[j] = X[o * d + j];
+    __syncwarp();
+    const T xn = xn_ref[o];
+    const T* ctb = ct + b * d * K;
+    const float cm = __uint_as_float(cmax[b]);
+    const float xnf = (float)xn;
+    const float nx = sqrtf(xnf) * (1.f + 0x1p-20f);
+    const float e = 0x1p-22f * (xnf + cm * cm) + (float)(d + 4) * 0x1p-23f * nx * cm;
+    const float rr = 0x1p-20f * (xnf + cm * cm + nx * cm);
+    const float thr = 8.f * (e + rr);  // 2 (E + R) with a factor 4 of slack (as k_fallback_rows)
+    // 1. fp32 estimates
+    float dt[NQ];
+    float dmin = __int_as_float(0x7f800000);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      dt[q] = __int_as_float(0x7f800000);
+      if (q < n) {
+        const int64_t k = (int64_t)r[2 + q] + lane;
+        if (k < K) {
+          const T* col = ctb + k;
+          float acc = 0.f;
+#pragma unroll 8
+          for (int j = 0; j < d; ++j) acc = fmaf((float)xs[j], (float)__ldg(col + (int64_t)j * K), acc);
+          dt[q] = (xnf + (float)cn[b * K + k]) - 2.f * acc;
+          dmin = fminf(dmin, dt[q]);
+        }
+      }
+    }
+#pragma unroll
+    for (int sh = 16; sh; sh >>= 1) dmin = fminf(dmin, __shfl_xor_sync(0xffffffffu, dmin, sh));
+    // 2. compact the candidates (NaN / inf estimates included), then exact
+    int nc = 0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      if (q < n) {
+        const int64_t k = (int64_t)r[2 + q] + lane;
+        const bool c = k < K && !(dt[q] > dmin + thr);
+        const unsigned m = __ballot_sync(0xffffffffu, c);
+        if (c) cand[wib][nc + __popc(m & ((1u << lane) - 1))] = (int32_t)k;
+        nc += __popc(m);
+      }
+    }
+    __syncwarp();
+    T best = (T)__int_as_float(0x7f800000);
+    int32_t bi = -1;
+    for (int c0 = 0; c0 < nc; c0 += 32) {
+      if (c0 + lane < nc) {
+        const int64_t k = cand[wib][c0 + lane];
+        const T* col = ctb + k;
+        double da = 0.0;
+        for (int j = 0; j < d; ++j) da = __dadd_rn(da, prod_term(xs[j], __ldg(col + (int64_t)j * K)));
+        T sv;
+        if constexpr (sizeof(T) == 4) sv = __fadd_rn(xn, cn[b * K + k]);
+        else sv = __dadd_rn(xn, cn[b * K + k]);
+        double dv = __dsub_rn((double)sv, __dmul_rn(2.0, da));
+        if (dv < 0.0) dv = 0.0;
+        const T v = (T)dv;
+        if (v < best || (v == best && (bi < 0 || k < bi))) {
+          best = v;
+          bi = (int32_t)k;
+        }
+      }
+    }
+#pragma unroll
+    for (int sh = 16; sh; sh >>= 1) {
+      const T ob = __shfl_xor_sync(0xffffffffu, best, sh);
+      const int32_t oi = __shfl_xor_sync(0xffffffffu, bi, sh);
+      if (ob < best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (lane == 0) {
+      idx_out[o] = bi;
+      mind_out[o] = best;
+      if (idx_prev && idx_prev[o] != bi) ch = true;
+    }
+  }
+  if (changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(changed, 1);
+}
+
 // ---------------------------------------------------------------- launchers
 bool assign_split_supported(int64_t d) { return d >= 1 && d <= 128; }
 
@@ -406,7 +522,7 @@ cudaError_t launch_split_centroids(int dt, const void* C, int64_t B, int64_t K, 
   if (dt == DT_F64)
     k_split_centroids<double><<<grid, 256, 0, s>>>((const double*)C, B, K, (int)d, dp, kpad,
                                                    (__nv_bfloat16*)c2, (__nv_bfloat16*)ext, cmax,
-                                                   (float*)ct);
+                                                   (double*)ct);
   else
     k_split_centroids<float><<<grid, 256, 0, s>>>((const float*)C, B, K, (int)d, dp, kpad,
                                                   (__nv_bfloat16*)c2, (__nv_bfloat16*)ext, cmax,
@@ -416,20 +532,42 @@ cudaError_t launch_split_centroids(int dt, const void* C, int64_t B, int64_t K, 
 
 cudaError_t launch_certify(int dt, const void* X, const void* C, const void* cn_ref,
                            const unsigned int* cmax, int64_t B, int64_t N, int64_t K, int64_t d,
-                           const int32_t* ids, const float* est, const float* second, void* xn_out,
-                           void* mind_out, const int32_t* idx_prev, int32_t* changed,
-                           int32_t* list, int32_t* list_cnt, int fast, cudaStream_t s) {
+                           const int32_t* ids, const float* est, const float* second,
+                           const int8_t* stat, void* xn_out, void* mind_out,
+                           const int32_t* idx_prev, int32_t* changed, int32_t* list,
+                           int32_t* list_cnt, int fast, cudaStream_t s) {
   dim3 grid((unsigned)((N + 127) / 128), (unsigned)B);
   if (dt == DT_F64)
     k_certify<double><<<grid, 128, 0, s>>>((const double*)X, (const double*)C,
                                            (const double*)cn_ref, cmax, N, K, (int)d, ids, est,
-                                           second, (double*)xn_out, (double*)mind_out, idx_prev,
-                                           changed, list, list_cnt, fast);
+                                           second, stat, (double*)xn_out, (double*)mind_out,
+                                           idx_prev, changed, list, list_cnt, fast);
   else
     k_certify<float><<<grid, 128, 0, s>>>((const float*)X, (const float*)C, (const float*)cn_ref,
-                                          cmax, N, K, (int)d, ids, est, second, (float*)xn_out,
-                                          (float*)mind_out, idx_prev, changed, list, list_cnt,
-                                          fast);
+                                          cmax, N, K, (int)d, ids, est, second, stat,
+                                          (float*)xn_out, (float*)mind_out, idx_prev, changed,
+                                          list, list_cnt, fast);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_candidates(int dt, const void* X, const void* ct, const void* cn_ref,
+                              const void* xn_ref, const unsigned int* cmax, int64_t N, int64_t K,
+                              int64_t d,
+                              const int32_t* rec, const int32_t* rec_cnt, int rec_cap,
+                              int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+                              int32_t* changed, int num_sms, cudaStream_t s) {
+  const size_t smem = 8 * (size_t)d * (dt == DT_F64 ? 8 : 4);
+  const unsigned grid = (unsigned)num_sms * 8;
+  if (dt == DT_F64)
+    k_candidates<double><<<grid, 256, smem, s>>>((const double*)X, (const double*)ct,
+                                                 (const double*)cn_ref, (const double*)xn_ref, cmax, N, K,
+                                                 (int)d, rec, rec_cnt, rec_cap, idx_out,
+                                                 (double*)mind_out, idx_prev, changed);
+  else
+    k_candidates<float><<<grid, 256, smem, s>>>((const float*)X, (const float*)ct,
+                                                (const float*)cn_ref, (const float*)xn_ref, cmax, N, K,
+                                                (int)d, rec, rec_cnt, rec_cap, idx_out,
+                                                (float*)mind_out, idx_prev, changed);
   return cudaGetLastError();
 }
 
@@ -443,7 +581,7 @@ cudaError_t launch_fallback_rows(int dt, const void* X, const void* C, const voi
   const unsigned grid = (unsigned)num_sms * 4;
   if (dt == DT_F64)
     k_fallback_rows<double><<<grid, FB_W * 32, smem, s>>>(
-        (const double*)X, (const double*)C, (const float*)ct, (const double*)cn,
+        (const double*)X, (const double*)C, (const double*)ct, (const double*)cn,
         (const double*)xn_ref, cmax, B, N, K, (int)d, list, list_cnt, idx_out, (double*)mind_out,
         idx_prev, changed);
   else

@@ -74,7 +74,20 @@ struct TcArgs {
   // epilogue also reports a lower bound on each row's second-best score.
   int ns;
   float* second_out;  // (B, N) second-best score bound (split only)
+  // split: the epilogue's own certificate (margin from an upper bound of |x|
+  // read off the [hi | lo] tile and cmax) and, for rows it cannot certify,
+  // the column bases of every 32-column chunk whose minimum came within the
+  // margin of the running best (the only places the exact argmin can be)
+  const unsigned int* cmax;  // (B) float bits, upper bound of max_k |c_k|
+  int8_t* stat_out;          // (B, N) 0 certified, 1 candidate chunks listed, 2 full fallback
+  int32_t* cand_rec;         // records [row, n, chunk bases...], FK_SPLIT_REC ints each
+  int32_t* cand_cnt;         // record count (device)
+  int cand_cap;
 };
+
+constexpr int SPLIT_NREC = 4;                  // near chunks kept per thread (per column half)
+constexpr int FK_SPLIT_REC = 2 + 2 * SPLIT_NREC;
+static_assert(FK_SPLIT_REC == kSplitRecInts, "candidate record layout (fk_kernels.h)");
 
 // Debug timeline: events of pair 0 / tile window [TR_G0, TR_G0 + TR_N) only.
 constexpr int TR_G0 = 16, TR_N = 32, TR_EV = 8;
@@ -412,7 +425,7 @@ constexpr int OFF_AEXT = 0;                                // constant ones oper
 constexpr int OFF_EXT = OFF_AEXT + BM * EXT_ROW;
 constexpr int OFF_CN = OFF_EXT + EXT_SLOTS * EXT_SLOT;
 constexpr int OFF_XCH = OFF_CN + CN_SLOTS * BN * 4;
-constexpr int OFF_BAR = OFF_XCH + BM * 16;  // [min | idx | ||x||^2 part | second] exchange
+constexpr int OFF_BAR = OFF_XCH + BM * 48;  // [min | idx | ||x||^2 part | second | 8 near-chunk words]
 constexpr int A_SLOTS_MAX = 8;
 constexpr int NBARS = 2 * A_SLOTS_MAX + 2 * NBUF + 2 * STAGES + 2 * CN_SLOTS + 2 * EXT_SLOTS;
 constexpr int OFF_OPS = ((OFF_BAR + NBARS * 8 + 16) + 1023) & ~1023;  // 1 KB aligned (SW128)
@@ -441,7 +454,7 @@ __host__ __device__ inline void operand_plan(int katoms, int& a_slots, int& b_st
 // Epilogue chunk when the bias is already in the accumulator (s = ||c||^2/2 - x.c).
 template <bool S = false>
 FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, float (&bestv)[32],
-                          float& m2) {
+                          float& m2, float& mc_out) {
   const float* s = reinterpret_cast<const float*>(v);
   float a[11];
 #pragma unroll
@@ -455,7 +468,10 @@ FK_DEV void epi_chunk_aug(uint32_t (&v)[32], int colbase, float& M, int& best, f
   const bool p = mc < M;
   // split: every chunk other than the winner's bounds the second best from
   // below by its minimum (the winner's own chunk is scanned at the end)
-  if constexpr (S) m2 = fminf(m2, fmaxf(M, mc));
+  if constexpr (S) {
+    m2 = fminf(m2, fmaxf(M, mc));
+    mc_out = mc;
+  }
   if (__any_sync(0xffffffffu, p)) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) bestv[j] = p ? s[j] : bestv[j];
@@ -481,7 +497,8 @@ FK_DEV float min_tree32(const float* s) {
 // '<' in order a then b keeps the lowest index on ties, as epi_chunk_aug does.
 template <bool S = false>
 FK_DEV void epi_chunk2_aug(const uint32_t (&va)[32], const uint32_t (&vb)[32], int cola, int colb,
-                           float& M, int& best, float (&bestv)[32], float& m2) {
+                           float& M, int& best, float (&bestv)[32], float& m2, float& mca_out,
+                           float& mcb_out) {
   const float* sa = reinterpret_cast<const float*>(va);
   const float* sb = reinterpret_cast<const float*>(vb);
   const float mca = min_tree32(sa);
@@ -489,13 +506,45 @@ FK_DEV void epi_chunk2_aug(const uint32_t (&va)[32], const uint32_t (&vb)[32], i
   const bool pa = mca < M;
   const float Ma = pa ? mca : M;
   const bool pb = mcb < Ma;
-  if constexpr (S) m2 = fminf(fminf(m2, fmaxf(M, mca)), fmaxf(Ma, mcb));
+  if constexpr (S) {
+    m2 = fminf(fminf(m2, fmaxf(M, mca)), fmaxf(Ma, mcb));
+    mca_out = mca;
+    mcb_out = mcb;
+  }
   if (__any_sync(0xffffffffu, pa || pb)) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) bestv[j] = pb ? sb[j] : (pa ? sa[j] : bestv[j]);
   }
   M = pb ? mcb : Ma;
   best = pb ? colb : (pa ? cola : best);
+}
+
+// Split tile row: upper bound of |x| from the [hi | lo] bf16 operand row,
+// |x| <= |hi| + |lo| + 2^-16 |x| (hi columns: the first 16 ns of the row).
+// Physical 16-byte chunk p of a 128-byte-swizzled row r holds logical chunk
+// p ^ (r & 7).
+FK_DEV float split_norm_ub(const uint8_t* a_slot, int row, int katoms, int ns, int lane) {
+  float sh = 0.f, sl = 0.f;
+  for (int ka = 0; ka < katoms; ++ka) {
+    const uint4* r = reinterpret_cast<const uint4*>(a_slot + ka * tc::A_ATOM + row * 128);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int pc = (j + lane) & 7;
+      const bool hi = ka * 64 + 8 * (pc ^ (row & 7)) < 16 * ns;
+      uint4 w = r[pc];
+      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+      float acc = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float lo = __uint_as_float(ws[e] << 16), hv = __uint_as_float(ws[e] & 0xffff0000u);
+        acc = fmaf(lo, lo, acc);
+        acc = fmaf(hv, hv, acc);
+      }
+      if (hi) sh += acc;
+      else sl += acc;
+    }
+  }
+  return (sqrtf(sh) + sqrtf(sl)) * (1.0f + 0x1p-10f) + 0x1p-60f;
 }
 
 // BIAS = 1 (bias-in-GEMM): the ||c||^2 bias rides in the GEMM as one extra
@@ -530,6 +579,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   int* xch_i = reinterpret_cast<int*>(smem + OFF_XCH + BM * 4);
   float* xch_xn = reinterpret_cast<float*>(smem + OFF_XCH + BM * 8);
   float* xch_m2 = reinterpret_cast<float*>(smem + OFF_XCH + BM * 12);
+  int32_t* xch_rec = reinterpret_cast<int32_t*>(smem + OFF_XCH + BM * 16);  // [row][8]: n, bases
   static_assert(!SPLIT || BIAS == 1, "split runs with the bias in the GEMM");
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_BAR);
   uint64_t* a_full = bars + 0;
@@ -815,6 +865,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         prev_id = __ldg(p.idx_prev + (size_t)b * p.N + row0 + row);
       float M = __int_as_float(0x7f800000);
       float m2 = M;  // split: lower bound on the row's second-best score
+      float smg = 0.f;  // split: certificate margin of this row
+      bool rovf = false;  // split: more near chunks than slots at some point
+      int rec[SPLIT_NREC];  // near chunks: column base (-1 = free) and chunk minimum
+      float rmn[SPLIT_NREC];
+#pragma unroll
+      for (int r = 0; r < SPLIT_NREC; ++r) {
+        rec[r] = -1;
+        rmn[r] = 0.f;
+      }
+      float cmx = 0.f;
+      if (SPLIT) cmx = __uint_as_float(p.cmax[b]);
       int best = -1;
       float bestv[32];
 #pragma unroll
@@ -832,10 +893,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         uint32_t va[32], vb[32];
         FK_TMEM_LD_32x32b_X32(taddr, va);
         if (c == 0) {  // ALT: the owning warpgroup; else each warpgroup half the chunk positions
-          if (!SPLIT)  // (split: the exact norms come from the certify pass)
+          if (SPLIT) {  // |x| upper bound -> this row's certificate margin (k_certify's formula)
+            xn = split_norm_ub(sA + slot * a_slot_bytes, row, p.katoms, p.ns, lane);
+            smg = 0x1p-11f * fmaf(xn, cmx, cmx * cmx) + 0x1p-18f * xn * xn + 0x1p-100f;
+            smg *= 1.0f + 0x1p-20f;
+          } else {
             xn = alt ? row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane)
                      : row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane, 4 * wg,
                                           4 * wg + 4);
+          }
           __syncwarp();
           if (lane == 0) mbar_arrive(&a_empty[slot]);
         }
@@ -855,10 +921,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[buf]), 0));
           }
         };
+        // split: keep the chunk if its minimum is within the margin of the
+        // running best (every centroid the exact argmin could be, or tie with)
+        // (slots whose chunk minimum fell out of the margin of the current
+        // best are freed first: the best only decreases)
+        auto near = [&](float mc, int colbase) {
+          if (SPLIT && mc <= M + smg) {
+            bool put = false;
+#pragma unroll
+            for (int r = 0; r < SPLIT_NREC; ++r) {
+              if (rec[r] >= 0 && rmn[r] > M + smg) rec[r] = -1;
+              if (!put && rec[r] < 0) {
+                rec[r] = colbase;
+                rmn[r] = mc;
+                put = true;
+              }
+            }
+            rovf |= !put;
+          }
+        };
         auto chunk = [&](uint32_t (&v)[32], int ch) {
-          if (NEG)
-            epi_chunk_aug<SPLIT>(v, col0 + 32 * ch, M, best, bestv, m2);
-          else
+          if (NEG) {
+            float mc = 0.f;
+            epi_chunk_aug<SPLIT>(v, col0 + 32 * ch, M, best, bestv, m2, mc);
+            near(mc, col0 + 32 * ch);
+          } else
             epi_chunk(v, cnp + 128 * ch, col0 + 32 * ch, M, best, bestv);
         };
         if (p.debug_mode == 1) {
@@ -879,7 +966,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               release_tmem();  // every TMEM read of this buffer has landed
               if (tr) trace_ev(p, g, 3);
             }
-            epi_chunk2_aug<SPLIT>(va, vb, col0 + 32 * ch, col0 + 32 * (ch + 1), M, best, bestv, m2);
+            float mca = 0.f, mcb = 0.f;
+            epi_chunk2_aug<SPLIT>(va, vb, col0 + 32 * ch, col0 + 32 * (ch + 1), M, best, bestv, m2, mca,
+                                  mcb);
+            near(mca, col0 + 32 * ch);
+            near(mcb, col0 + 32 * (ch + 1));
             if (ch + 2 < nch) {
               FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 2), va);
               FK_TMEM_LD_32x32b_X32(taddr + 32 * (ch + 3), vb);
@@ -923,16 +1014,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           for (int j = 0; j < 32; ++j) m2 = j != found ? fminf(m2, bestv[j]) : m2;
         }
       }
+      int nrec = 0;  // split: the near chunks still within the margin of this half's best
+      if constexpr (SPLIT) {
+#pragma unroll
+        for (int r = 0; r < SPLIT_NREC; ++r) {
+          if (rec[r] >= 0 && rmn[r] > M + smg) rec[r] = -1;
+          nrec += rec[r] >= 0 ? 1 : 0;
+        }
+        if (rovf) nrec = SPLIT_NREC + 1;
+      }
       if (!alt) {
         if (wg == 1) {
           xch_m[row] = M;
           xch_i[row] = idx;
           xch_xn[row] = xn;
-          if (SPLIT) xch_m2[row] = m2;
+          if (SPLIT) {
+            xch_m2[row] = m2;
+            xch_rec[row * 8] = nrec;
+            int w8 = 0;
+#pragma unroll
+            for (int r = 0; r < SPLIT_NREC; ++r)
+              if (rec[r] >= 0) xch_rec[row * 8 + 1 + w8++] = rec[r];
+          }
         }
         named_bar_sync(1, 256);
         if (wg == 0) {
-          xn += xch_xn[row];
+          if (!SPLIT) xn += xch_xn[row];
           const float M1 = xch_m[row];
           const int i1 = xch_i[row];
           if (SPLIT) m2 = fminf(fminf(m2, xch_m2[row]), fmaxf(M, M1));
@@ -957,6 +1064,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           }
         }
         if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
+        if constexpr (SPLIT) {
+          // the epilogue's certificate (margin >= k_certify's: |x| bounded from
+          // above), else the near chunks of both column halves, else a full
+          // fallback; records appended warp-aggregated
+          const int n1 = alt ? 0 : xch_rec[row * 8];
+          const float scale = fmaf(xn, cmx, cmx * cmx);
+          const bool cert = idx >= 0 && (m2 - M > smg) && scale > 0x1p-60f && smg < 3e38f;
+          const bool live = grow < p.N;
+          const bool lst = live && !cert && nrec <= SPLIT_NREC && n1 <= SPLIT_NREC && smg < 3e38f;
+          const unsigned m = __ballot_sync(0xffffffffu, lst);
+          int pos = -1;
+          if (m) {
+            int base = 0;
+            if (lane == __ffs(m) - 1) base = atomicAdd(p.cand_cnt, __popc(m));
+            base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+            if (lst) pos = base + __popc(m & ((1u << lane) - 1));
+          }
+          const bool listed = lst && pos < p.cand_cap;
+          if (listed) {
+            int32_t* r = p.cand_rec + (int64_t)pos * FK_SPLIT_REC;
+            r[0] = (int32_t)((int64_t)b * p.N + grow);
+            const int n0 = nrec;  // <= SPLIT_NREC here
+            r[1] = n0 + n1;
+            int w8 = 0;
+#pragma unroll
+            for (int q2 = 0; q2 < SPLIT_NREC; ++q2)
+              if (rec[q2] >= 0) r[2 + w8++] = rec[q2];
+            for (int q2 = 0; q2 < n1; ++q2) r[2 + n0 + q2] = xch_rec[row * 8 + 1 + q2];
+          }
+          if (live) p.stat_out[(size_t)b * p.N + grow] = cert ? 0 : (listed ? 1 : 2);
+        }
       }
       if (!alt) named_bar_sync(2, 256);
     }
@@ -1150,7 +1288,9 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
 // bound on the row's second-best score.
 cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* ext, int64_t B,
                                    int64_t N, int64_t K, int ns, int32_t* idx_out, float* est_out,
-                                   float* second_out, int num_sms, cudaStream_t stream) {
+                                   float* second_out, const unsigned int* cmax, int8_t* stat_out,
+                                   int32_t* cand_rec, int32_t* cand_cnt, int cand_cap, int num_sms,
+                                   cudaStream_t stream) {
   if (ns < 1 || 2 * ns > 4 * tc2::KATOMS_MAX) return cudaErrorInvalidValue;
   const int64_t W = 32 * (int64_t)ns;
   TcArgs a;
@@ -1175,6 +1315,11 @@ cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* e
   a.trace = nullptr;
   a.ns = ns;
   a.second_out = second_out;
+  a.cmax = cmax;
+  a.stat_out = stat_out;
+  a.cand_rec = cand_rec;
+  a.cand_cnt = cand_cnt;
+  a.cand_cap = cand_cap;
   CUtensorMap tmx2, tmc2, tmext;
   if (!make_map(&tmx2, X2, 1, W, N, B, tc2::BM)) return cudaErrorInvalidValue;
   if (!make_map(&tmc2, C2, 1, W, K, B, tc2::BNH)) return cudaErrorInvalidValue;

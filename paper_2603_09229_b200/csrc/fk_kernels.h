@@ -18,9 +18,12 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
                              int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
                              int32_t* changed, int num_sms, cudaStream_t stream);
 
+constexpr int kSplitRecInts = 10;  // fk_assign_tc.cu FK_SPLIT_REC: [row, n, up to 8 chunk bases]
 cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* ext, int64_t B,
                                    int64_t N, int64_t K, int ns, int32_t* idx_out, float* est_out,
-                                   float* second_out, int num_sms, cudaStream_t stream);
+                                   float* second_out, const unsigned int* cmax, int8_t* stat_out,
+                                   int32_t* cand_rec, int32_t* cand_cnt, int cand_cap, int num_sms,
+                                   cudaStream_t stream);
 
 // fk_assign_exact.cu
 cudaError_t launch_cn_pad(int dt, const void* C, int64_t B, int64_t K, int64_t d, int kpad,
@@ -56,9 +59,16 @@ cudaError_t launch_fallback_rows(int dt, const void* X, const void* C, const voi
                                  cudaStream_t s);
 cudaError_t launch_certify(int dt, const void* X, const void* C, const void* cn_ref,
                            const unsigned int* cmax, int64_t B, int64_t N, int64_t K, int64_t d,
-                           const int32_t* ids, const float* est, const float* second, void* xn_out,
-                           void* mind_out, const int32_t* idx_prev, int32_t* changed,
-                           int32_t* list, int32_t* list_cnt, int fast, cudaStream_t s);
+                           const int32_t* ids, const float* est, const float* second,
+                           const int8_t* stat, void* xn_out, void* mind_out,
+                           const int32_t* idx_prev, int32_t* changed, int32_t* list,
+                           int32_t* list_cnt, int fast, cudaStream_t s);
+cudaError_t launch_candidates(int dt, const void* X, const void* ct, const void* cn_ref,
+                              const void* xn_ref, const unsigned int* cmax, int64_t N, int64_t K,
+                              int64_t d,
+                              const int32_t* rec, const int32_t* rec_cnt, int rec_cap,
+                              int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
+                              int32_t* changed, int num_sms, cudaStream_t s);
 cudaError_t launch_assign_cuda_core_lowp(int dt, const void* X, const void* C, const float* cn,
                                          int64_t B, int64_t N, int64_t K, int64_t d,
                                          int32_t* idx_out, float* mind_out,
