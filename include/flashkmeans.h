@@ -118,9 +118,11 @@ FK_API fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void
  * The certified tensor-core path for the reference's own precisions
  * (flash_assign dot_mode "exact" / "fast", flash_assign.py:203-208;
  * dist_block and assign_tile_fast, _kernels.py:32-45, 85-104), d <= 128:
- *   xsplit : (B, N, 32*ceil(d/16)) bf16 rows [hi | lo] of X, v = hi + lo +
- *            O(2^-16 v), written once by fk_assign_xsplit and reusable while
- *            X is unchanged (a Lloyd run builds it once).
+ *   xsplit : fk_assign_xsplit_bytes of device memory: the (B, N, 32*ceil(d/16))
+ *            bf16 rows [hi | lo] of X, v = hi + lo + O(2^-16 v), then the
+ *            reference's exact ||x||^2 (row_norms, core.py:307-318); written
+ *            once by fk_assign_xsplit, reusable while X is unchanged (a Lloyd
+ *            run builds it once).
  *   dot_mode FK_DOT_EXACT: tcgen05 estimate of every distance (3 bf16 MMAs
  *            per K=16 step, fp32 accumulation) + per-row certificate that the
  *            estimated argmin is the reference's; uncertified rows (near and

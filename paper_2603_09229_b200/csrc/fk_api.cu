@@ -159,8 +159,19 @@ bool split_auto(int64_t B, int64_t N, int64_t K, int64_t d) {
   if (e >= 0) return e == 1;
   return (double)B * N * K * d >= 6.7e7;  // ~20 us of the exact mirror
 }
-size_t xsplit_bytes(int64_t B, int64_t N, int64_t d) {
+// X's split operand (B, N, 32 ns) bf16, then the reference's exact ||x||^2
+// (B, N) in the data type: both fixed while X is.
+size_t xsplit_x2_bytes(int64_t B, int64_t N, int64_t d) {
   return al256((size_t)B * N * 32 * fk::split_steps(d) * 2);
+}
+size_t xsplit_bytes(int dt, int64_t B, int64_t N, int64_t d) {
+  return xsplit_x2_bytes(B, N, d) + al256((size_t)B * N * elem_size(dt));
+}
+fk_status build_xsplit(int dt, const void* X, int64_t B, int64_t N, int64_t d, uint8_t* xs,
+                       int sms, cudaStream_t s) {
+  fk_status st = cuda_status(fk::launch_split_rows(dt, X, B * N, d, xs, sms, s));
+  if (st != FK_OK) return st;
+  return cuda_status(fk::launch_row_norms_exact(dt, X, B * N, d, xs + xsplit_x2_bytes(B, N, d), s));
 }
 struct SplitWs {
   void *c2, *ext, *cn_ref, *xn_ref, *ct;
@@ -191,7 +202,6 @@ SplitWs split_ws_layout(uint8_t* base, int dt, int64_t B, int64_t N, int64_t K, 
   w.est = (float*)take((size_t)B * N * 4);
   w.second = (float*)take((size_t)B * N * 4);
   w.list = (int32_t*)take((size_t)B * N * 4);
-  w.xn_ref = take((size_t)B * N * es);
   w.bytes = o;
   return w;
 }
@@ -203,7 +213,8 @@ size_t exact_ws_bytes(int dt, int64_t B, int64_t N, int64_t K) {
 fk_status run_split(int dt, const void* X, const void* xsplit, const void* C, int64_t B, int64_t N,
                     int64_t K, int64_t d, int fast, int32_t* idx_out, void* mind_out,
                     const int32_t* idx_prev, int32_t* changed, uint8_t* ws, cudaStream_t s) {
-  const SplitWs w = split_ws_layout(ws, dt, B, N, K, d);
+  SplitWs w = split_ws_layout(ws, dt, B, N, K, d);
+  w.xn_ref = const_cast<uint8_t*>(reinterpret_cast<const uint8_t*>(xsplit)) + xsplit_x2_bytes(B, N, d);
   const int kpad = fk::assign_tc_kpad(K);
   const DevInfo di = dev_info();
   fk_status st = cuda_status(cudaMemsetAsync(w.cmax, 0, (size_t)B * 8 + 16, s));
@@ -235,13 +246,13 @@ size_t fk_assign_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t
     return al256((size_t)B * fk::assign_tc_kpad(K) * 4) + al256((size_t)B * fk::assign_tc_kpad(K) * 32);
   const size_t ex = exact_ws_bytes(dt, B, N, K);
   if (!split_auto(B, N, K, d)) return ex;
-  const size_t sp = xsplit_bytes(B, N, d) + split_ws_layout(nullptr, dt, B, N, K, d).bytes;
+  const size_t sp = xsplit_bytes(dt, B, N, d) + split_ws_layout(nullptr, dt, B, N, K, d).bytes;
   return sp > ex ? sp : ex;
 }
 
 size_t fk_assign_xsplit_bytes(fk_dtype dt, int64_t B, int64_t N, int64_t d) {
   if ((dt != FK_F32 && dt != FK_F64) || B < 1 || N < 1 || !fk::assign_split_supported(d)) return 0;
-  return xsplit_bytes(B, N, d);
+  return xsplit_bytes(dt, B, N, d);
 }
 
 fk_status fk_assign_xsplit(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t d,
@@ -249,8 +260,8 @@ fk_status fk_assign_xsplit(fk_dtype dt, const void* X, int64_t B, int64_t N, int
   if ((dt != FK_F32 && dt != FK_F64) || !X || !xsplit || !shape_ok(B, N, 1, d)) return FK_EINVAL;
   if (!fk::assign_split_supported(d)) return FK_EUNSUPPORTED;
   if (dev_info().major != 10) return FK_EUNSUPPORTED;
-  return cuda_status(fk::launch_split_rows(dt, X, B * N, d, xsplit, dev_info().sms,
-                                           reinterpret_cast<cudaStream_t>(stream)));
+  return build_xsplit(dt, X, B, N, d, reinterpret_cast<uint8_t*>(xsplit), dev_info().sms,
+                      reinterpret_cast<cudaStream_t>(stream));
 }
 
 fk_status fk_assign_split_fallback_rows(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d,
@@ -356,10 +367,10 @@ fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void* bias,
   const size_t es = elem_size(dt);
   uint8_t* w = reinterpret_cast<uint8_t*>(ws);
   if (split_auto(B, N, K, d)) {  // X's split operand in the workspace, then the certified path
-    fk_status st = cuda_status(fk::launch_split_rows(dt, X, B * N, d, w, di.sms, s));
+    fk_status st = build_xsplit(dt, X, B, N, d, w, di.sms, s);
     if (st != FK_OK) return st;
     return run_split(dt, X, w, C, B, N, K, d, 0, idx_out, mind_out, idx_prev, changed_flag,
-                     w + xsplit_bytes(B, N, d), s);
+                     w + xsplit_bytes(dt, B, N, d), s);
   }
   void* xn = w;
   void* cn = w + al256((size_t)B * N * es);

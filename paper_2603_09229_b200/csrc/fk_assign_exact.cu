@@ -44,6 +44,38 @@ __global__ void k_row_norms_exact(const T* __restrict__ M, int64_t rows, int64_t
   out[r] = (T)acc;
 }
 
+// Same sums, rows staged through shared memory 128 at a time (coalesced row
+// reads; one thread per row keeps the serial ascending-j chain).
+template <typename T>
+__global__ void __launch_bounds__(128) k_row_norms_staged(const T* __restrict__ M, int64_t rows,
+                                                          int64_t d, T* out) {
+  constexpr int DC = sizeof(T) == 4 ? 32 : 16;
+  __shared__ T ms[DC][129];
+  const int tid = threadIdx.x;
+  const int64_t row0 = blockIdx.x * (int64_t)128;
+  double acc = 0.0;
+  for (int64_t j0 = 0; j0 < d; j0 += DC) {
+    __syncthreads();
+#pragma unroll 8
+    for (int e = tid; e < 128 * DC; e += 128) {
+      const int r = e / DC, jj = e - r * DC;
+      const int64_t gr = row0 + r, j = j0 + jj;
+      ms[jj][r] = (gr < rows && j < d) ? M[gr * d + j] : (T)0;
+    }
+    __syncthreads();
+    const int jn = (int)(d - j0 < DC ? d - j0 : DC);
+    for (int jj = 0; jj < jn; ++jj) {
+      const T v = ms[jj][tid];
+      if constexpr (sizeof(T) == 4) {
+        acc = __dadd_rn(acc, (double)__fmul_rn(v, v));
+      } else {
+        acc = __dadd_rn(acc, __dmul_rn(v, v));
+      }
+    }
+  }
+  if (row0 + tid < rows) out[row0 + tid] = (T)acc;
+}
+
 // ||c||^2 in fp32 for the low-precision paths, padded to kpad with +inf so
 // columns beyond K never win the argmin.
 template <typename T>
@@ -255,10 +287,16 @@ cudaError_t launch_row_norms_exact(int dt, const void* M, int64_t rows, int64_t 
   if (rows <= 0) return cudaSuccess;
   const int th = 128;
   const unsigned grid = (unsigned)((rows + th - 1) / th);
-  if (dt == DT_F64)
+  if (rows >= 4096) {  // enough rows to fill the GPU with 128-row tiles
+    if (dt == DT_F64)
+      k_row_norms_staged<double><<<grid, th, 0, stream>>>((const double*)M, rows, d, (double*)out);
+    else
+      k_row_norms_staged<float><<<grid, th, 0, stream>>>((const float*)M, rows, d, (float*)out);
+  } else if (dt == DT_F64) {
     k_row_norms_exact<double><<<grid, th, 0, stream>>>((const double*)M, rows, d, (double*)out);
-  else
+  } else {
     k_row_norms_exact<float><<<grid, th, 0, stream>>>((const float*)M, rows, d, (float*)out);
+  }
   return cudaGetLastError();
 }
 

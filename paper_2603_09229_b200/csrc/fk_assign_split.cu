@@ -114,9 +114,9 @@ FK_DEV double prod_term(float x, float c) { return (double)__fmul_rn(x, c); }
 FK_DEV double prod_term(double x, double c) { return __dmul_rn(x, c); }
 
 // ---------------------------------------------------------------- certify
-// One thread per row: the reference's ||x||^2 (kept for the fallback), the
-// margin test, and for certified rows the reference distance to the chosen
-// centroid.  Rows that do not certify go to the per-batch fallback list.
+// One thread per row: the margin test (with the reference's ||x||^2, cached
+// next to X's split operand), and for certified rows the reference distance to
+// the chosen centroid.  Rows that do not certify go to the per-batch fallback list.
 // The block's 128 rows and their chosen centroid rows stream through shared
 // memory DC columns at a time (coalesced row reads, double-buffered: the next
 // chunk's loads are in flight while the current one is summed); each thread
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(128)
               const unsigned int* __restrict__ cmax, int64_t N, int64_t K, int d,
               const int32_t* __restrict__ ids, const float* __restrict__ est,
               const float* __restrict__ second, const int8_t* __restrict__ stat,
-              T* __restrict__ xn_out, T* __restrict__ mind_out,
+              const T* __restrict__ xn_in, T* __restrict__ mind_out,
               const int32_t* __restrict__ idx_prev, int32_t* changed, int32_t* __restrict__ list,
               int32_t* __restrict__ list_cnt, int fast) {
   constexpr int DC = sizeof(T) == 4 ? 16 : 8;
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(128)
       pc[i] = (in && cid >= 0) ? __ldg(C + (b * K + cid) * d + j) : (T)0;
     }
   };
-  double xa = 0.0, da = 0.0;
+  double da = 0.0;
   const int nch = (d + DC - 1) / DC;
   fetch(0);
   for (int c = 0; c < nch; ++c) {
@@ -175,15 +175,14 @@ __global__ void __launch_bounds__(128)
     const int jn = d - c * DC < DC ? d - c * DC : DC;
     for (int jj = 0; jj < jn; ++jj) {
       const T xv = xs[buf][jj][tid], cv = cs[buf][jj][tid];
-      xa = __dadd_rn(xa, prod_term(xv, xv));
       da = __dadd_rn(da, prod_term(xv, cv));
     }
   }
   bool flag = false, ch = false;
-  if (row < N) xn_out[o] = (T)xa;
   // stat 1: the epilogue listed this row's candidate chunks (k_candidates)
   if (row < N && stat[o] != 1) {
-    const T xn = (T)xa;
+    const T xn = xn_in[o];
+    const double xa = (double)xn;
     const float cm = __uint_as_float(cmax[b]);
     const float nx = __fsqrt_ru(__double2float_ru(xa)) * (1.0f + 0x1p-20f);
     const float scale = __fmaf_ru(nx, cm, cm * cm);
@@ -533,19 +532,19 @@ cudaError_t launch_split_centroids(int dt, const void* C, int64_t B, int64_t K, 
 cudaError_t launch_certify(int dt, const void* X, const void* C, const void* cn_ref,
                            const unsigned int* cmax, int64_t B, int64_t N, int64_t K, int64_t d,
                            const int32_t* ids, const float* est, const float* second,
-                           const int8_t* stat, void* xn_out, void* mind_out,
+                           const int8_t* stat, const void* xn_in, void* mind_out,
                            const int32_t* idx_prev, int32_t* changed, int32_t* list,
                            int32_t* list_cnt, int fast, cudaStream_t s) {
   dim3 grid((unsigned)((N + 127) / 128), (unsigned)B);
   if (dt == DT_F64)
     k_certify<double><<<grid, 128, 0, s>>>((const double*)X, (const double*)C,
                                            (const double*)cn_ref, cmax, N, K, (int)d, ids, est,
-                                           second, stat, (double*)xn_out, (double*)mind_out,
+                                           second, stat, (const double*)xn_in, (double*)mind_out,
                                            idx_prev, changed, list, list_cnt, fast);
   else
     k_certify<float><<<grid, 128, 0, s>>>((const float*)X, (const float*)C, (const float*)cn_ref,
                                           cmax, N, K, (int)d, ids, est, second, stat,
-                                          (float*)xn_out, (float*)mind_out, idx_prev, changed,
+                                          (const float*)xn_in, (float*)mind_out, idx_prev, changed,
                                           list, list_cnt, fast);
   return cudaGetLastError();
 }

@@ -60,7 +60,7 @@ cudaError_t launch_fallback_rows(int dt, const void* X, const void* C, const voi
 cudaError_t launch_certify(int dt, const void* X, const void* C, const void* cn_ref,
                            const unsigned int* cmax, int64_t B, int64_t N, int64_t K, int64_t d,
                            const int32_t* ids, const float* est, const float* second,
-                           const int8_t* stat, void* xn_out, void* mind_out,
+                           const int8_t* stat, const void* xn_in, void* mind_out,
                            const int32_t* idx_prev, int32_t* changed, int32_t* list,
                            int32_t* list_cnt, int fast, cudaStream_t s);
 cudaError_t launch_candidates(int dt, const void* X, const void* ct, const void* cn_ref,

@@ -91,17 +91,20 @@ def split_supported(x: torch.Tensor) -> bool:
 
 
 def assign_xsplit(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-    """The bf16 [hi | lo] split operand of f32/f64 data (B,N,d), d <= 128:
-    (B, N, 32*ceil(d/16)) bf16.  Build once per data set and pass it to
-    ``assign(xsplit=)`` while X is unchanged."""
+    """X's operand for the certified tensor-core assign of f32/f64 data (B,N,d),
+    d <= 128: a uint8 device buffer holding the (B, N, 32*ceil(d/16)) bf16
+    [hi | lo] rows (``xsplit_rows``) and the exact row norms.  Build once per
+    data set and pass it to ``assign(xsplit=)`` while X is unchanged."""
     dev = _require_cuda(x)
     x = x.contiguous()
     B, n, d = x.shape
     if not split_supported(x):
         raise ValueError("the split operand needs float32/float64 data with d <= 128")
-    w = 32 * (-(-d // 16))
+    nb = N.lib().fk_assign_xsplit_bytes(fk_dtype(x.dtype), B, n, d)
     if out is None:
-        out = torch.empty((B, n, w), dtype=torch.bfloat16, device=dev)
+        out = torch.empty((nb,), dtype=torch.uint8, device=dev)
+    elif out.dtype != torch.uint8 or out.numel() < nb:
+        raise ValueError("out must be a uint8 buffer of fk_assign_xsplit_bytes")
     N.check(N.lib().fk_assign_xsplit(fk_dtype(x.dtype), x.data_ptr(), B, n, d, out.data_ptr(),
                                      _stream(dev)), "fk_assign_xsplit")
     return out
@@ -120,6 +123,13 @@ def split_fallback_rows(x: torch.Tensor, clusters: int) -> list:
                                                   ctypes.addressof(out), _stream(dev)),
             "fk_assign_split_fallback_rows")
     return list(out)
+
+
+def xsplit_rows(xsplit: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
+    """The (B, N, 32*ceil(d/16)) bf16 [hi | lo] rows inside ``assign_xsplit(x)``."""
+    B, n, d = x.shape
+    w = 32 * (-(-d // 16))
+    return xsplit[: B * n * w * 2].view(torch.bfloat16).view(B, n, w)
 
 
 _DOT = {"exact": 0, "fast": 1, "mirror": 2}
@@ -180,9 +190,9 @@ def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = Non
         mode = "mirror" if path == "mirror" or not split_supported(x) else dot_mode
         if mode != "mirror" and xsplit is None:
             xsplit = assign_xsplit(x)
-        if xsplit is not None and (xsplit.dtype != torch.bfloat16 or xsplit.shape[:2] != (B, n)
-                                   or not xsplit.is_contiguous()):
-            raise ValueError("xsplit must be the (B, N, w) bf16 assign_xsplit(x) of this data")
+        if xsplit is not None and (xsplit.dtype != torch.uint8 or not xsplit.is_contiguous()
+                                   or xsplit.numel() < L.fk_assign_xsplit_bytes(dt, B, n, d)):
+            raise ValueError("xsplit must be assign_xsplit(x) of this data")
         need = L.fk_assign_split_workspace(dt, B, n, K, d)
         ws = _ws.get(dev, need, "assign")
         st = L.fk_assign_split(dt, x.data_ptr(), None if mode == "mirror" else xsplit.data_ptr(),

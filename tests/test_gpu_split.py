@@ -121,7 +121,8 @@ def test_split_changed_flag_and_preallocated_xsplit(ops):
     c = rng.standard_normal((2, 700, 64)).astype(np.float32)
     xd, cd = torch.from_numpy(x).to(DEV), torch.from_numpy(c).to(DEV)
     xs = ops.assign_xsplit(xd)
-    assert xs.shape == (2, 5000, 128) and xs.dtype == torch.bfloat16
+    rows = ops.xsplit_rows(xs, xd)
+    assert rows.shape == (2, 5000, 128) and rows.dtype == torch.bfloat16
     ids0, _ = ops.assign(xd, cd, xsplit=xs)
     changed = torch.zeros((), dtype=torch.int32, device=DEV)
     ids1, _ = ops.assign(xd, cd, xsplit=xs, idx_prev=ids0, changed=changed)
@@ -131,7 +132,7 @@ def test_split_changed_flag_and_preallocated_xsplit(ops):
     ops.assign(xd, cd, xsplit=xs, idx_prev=prev, changed=changed)
     assert int(changed) == 1
     # the split operand is exact to 2^-16 of each value
-    hi, lo = xs[..., :64].double(), xs[..., 64:].double()
+    hi, lo = rows[..., :64].double(), rows[..., 64:].double()
     err = (hi + lo - xd.double()).abs()
     assert bool((err <= xd.double().abs() * 2.0 ** -16 + 1e-300).all())
 
