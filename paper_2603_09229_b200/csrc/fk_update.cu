@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(W * 32)
                    const int32_t* __restrict__ table, const int32_t* __restrict__ hist,
                    const int32_t* __restrict__ inval, int64_t B, int64_t chunk, int accumulate,
                    int64_t* __restrict__ off, int64_t* __restrict__ counts, int64_t* __restrict__ merges,
-                   int32_t* __restrict__ order) {
+                   int32_t* __restrict__ order, int rank_sort) {
   extern __shared__ __align__(16) uint8_t sw_sm[];
   // rows padded to K + 2 entries: the W rows of one key fall in different banks
   const int KS = (int)K + 2;
@@ -704,11 +704,52 @@ __global__ void __launch_bounds__(W * 32)
     }
   }
   __syncthreads();
-  // 3. ranks in index order: every lane bumps its warp's running count of its
-  //    id with a returning shared atomic; lanes of one instruction that hit
-  //    the same counter are serialized in lane order, so the returned counts
-  //    are the stable ranks (checked against numpy's stable argsort in
-  //    tests/test_gpu_kernels.py).  The ids are re-read (L2-resident).
+  // 3. ranks in index order.  FK_SCATTER_RANK=sort: 32 points a step, the
+  //    step's ids are sorted across the warp by (id, lane) with a shuffle
+  //    bitonic network;
+  //    the lane holding a sorted entry reads its id's running count from the
+  //    warp's row, adds its position inside the id's run (ballot of run
+  //    starts) and writes the point index; the last lane of each run stores
+  //    the new count (one writer per id).  (id, lane) keys are unique, so the
+  //    ranks are the stable ones (numpy's stable argsort,
+  //    tests/test_gpu_kernels.py), with no returning atomics on the critical
+  //    path -- but more instructions: slower (A/B record).  Default: every
+  //    lane bumps its counter with a returning shared atomic (lanes of one
+  //    instruction on one counter are served in lane order).  The ids are
+  //    re-read (L2-resident).
+  if (rank_sort) {
+    for (int p0 = a; p0 < e; p0 += 32) {
+      const int p = p0 + lane;
+      const uint32_t id = p < e ? (uint32_t)__ldg(idw + p) : 0xffffffffu;
+      uint32_t key = id < Ku ? ((id << 5) | (uint32_t)lane) : 0xffffffffu;
+#pragma unroll
+      for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, key, j);
+          const bool up = (lane & k) == 0;       // ascending block
+          const bool lower = (lane & j) == 0;    // this lane keeps the smaller key
+          key = (lower == up) ? min(key, o) : max(key, o);
+        }
+      }
+      const bool valid = key != 0xffffffffu;
+      const uint32_t sid = key >> 5;
+      const uint32_t prev = __shfl_up_sync(0xffffffffu, sid, 1);
+      const uint32_t next = __shfl_down_sync(0xffffffffu, sid, 1);
+      const bool first = lane == 0 || prev != sid;
+      const bool last = lane == 31 || next != sid;
+      const unsigned starts = __ballot_sync(0xffffffffu, first);
+      const int run0 = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+      if (valid) {
+        uint16_t* cnt = tab + w * KS + sid;
+        const uint32_t r = (uint32_t)*cnt + (uint32_t)(lane - run0);
+        order[kbase[sid] + (int32_t)r] = (int32_t)(lo + p0 + (int)(key & 31u));
+        if (last) *cnt = (uint16_t)(r + 1);
+      }
+      __syncwarp();
+    }
+    return;
+  }
   for (int p0 = a; p0 < e; p0 += 32 * SW_U3) {
     uint32_t id[SW_U3];
 #pragma unroll
@@ -1288,6 +1329,13 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
       if (e && tab_env < 4096) tab_env = -1;
     }
     const int tab_bytes = tab_env > 0 ? tab_env : (K >= 2048 ? 96 * 1024 : SW_TABLE_BYTES);
+    // FK_SCATTER_RANK=sort: bitonic (id, lane) ranks instead of returning
+    // atomics (A/B: config 3 update 521 vs 465 us, profiles/r02_ab_rank.txt)
+    static int rank_sort = -1;
+    if (rank_sort < 0) {
+      const char* e = getenv("FK_SCATTER_RANK");
+      rank_sort = (e && e[0] == 's') ? 1 : 0;
+    }
     int W = 32;
     while (W > 1 && (int64_t)W * (K + 2) * 2 > tab_bytes) W >>= 1;
     const bool alias = (int64_t)W * (K + 2) * 2 >= K * 4;
@@ -1305,7 +1353,7 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
     }                                                                                              \
     k_scatter_warp<WV, CV><<<blocks, WV * 32, smem, s>>>(ids, N, K, (int)bpb, w.table, w.hist,     \
                                                          w.inval, B, chunk, accumulate, w.off,     \
-                                                         counts, merges, w.order);                 \
+                                                         counts, merges, w.order, rank_sort);      \
   } while (0)
 #define FK_SW(WV)        \
   do {                   \

@@ -19,7 +19,8 @@ for rep in sys.argv[2:]:
         return v * scale
     for r in rows[2:]:
         name = r[h.index("Kernel Name")]
-        key = next((k for k in ("fk_assign_tc2", "fk_assign_tc", "k_segsum", "k_scatter_staged", "k_scatter_block", "k_hist", "k_scan")
+        key = next((k for k in ("fk_assign_tc2", "fk_assign_tc", "k_segsum", "k_scatter_warp", "k_scatter_staged",
+                                "k_scatter_block", "k_hist", "k_colscan", "k_scan")
                     if k in name), name[:40])
         if key == "fk_assign_tc2":
             key = "fk_assign_tc"
@@ -38,7 +39,7 @@ for rep in sys.argv[2:]:
         lines.append(f"{key:16s} {t*1e3:8.3f} ms  DRAM {rd/1e9:7.3f} GB read {wr/1e6:8.2f} MB written  "
                      + "  ".join(f"{k.split('.')[0].split('__')[1]}={rec[k]:.1f}" for k in rec if k.endswith("active") or k.endswith("elapsed")))
 os.makedirs("profiles", exist_ok=True)
-json.dump({"round": tag, "source": "ncu --set full --clock-control none (scripts/ncu_round.sh)", **out},
+json.dump({"round": tag, "source": "ncu --set full --clock-control none (scripts/r02_ncu.sh)", **out},
           open("profiles/ncu_summary.json", "w"), indent=1)
 open(f"profiles/{tag}_ncu_full.txt", "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
