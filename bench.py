@@ -349,6 +349,9 @@ def run_ours(args):
 
     run_steps(args.warmup)
     torch.cuda.synchronize()
+    # this library's kernels per step, counted (not assumed) over one extra
+    # untimed step with the CUDA activity profiler
+    per_step = count_launches(lambda: run_steps(1))
     if world > 1:
         dist.barrier()
     timers = [[ev() for _ in range(4)] for _ in range(args.steps)]
@@ -404,7 +407,7 @@ def run_ours(args):
         cpu = {"value": v, "unit": "points/s", "cores": threads, "kind": "port",
                "sample": f"{args.cpu_sample} of the workload's points, K={CLUSTERS}, d={DIMS}: one exact "
                          f"Lloyd iteration of the oracle restatement ({dt:.1f} s), rank 0"}
-    launches = 9 + (3 if world > 1 else 0)  # cn_ext, assign, obj x2, hist, scan, scatter, segsum, normalize
+    launches = per_step
     line = {
         "metric": METRIC,
         "value": N_TOTAL / (ms * 1e-3),
@@ -522,6 +525,18 @@ def relaunch(args) -> int:
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port", str(port),
            os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd, env=os.environ.copy())
+
+
+def count_launches(fn) -> int:
+    """Kernels of libflashkmeans.so (namespace fk::) launched by fn, counted with
+    torch's CUDA activity profiler; torch's own kernels are excluded."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return sum(1 for e in prof.events() if e.device_type.name == "CUDA" and "fk::" in e.name)
 
 
 def main():
