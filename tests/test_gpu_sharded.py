@@ -184,3 +184,29 @@ def test_repeated_out_of_core_iterations_reuse_buffers():
     r = fk.lloyd_run(fk.DataMatrix(x.data.cuda()), cfg)
     # lloyd_run stops early only at a fixed point, which further passes reproduce bitwise
     assert np.array_equal(c.numpy(), r.centroids.numpy())
+
+
+@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1)])
+def test_sharded_lloyd_f32_split_path_bitwise(backend, world):
+    """Every rank on the certified tensor-core f32 assign (FK_ASSIGN_F32=split):
+    still bit for bit the single-process run (which may take the exact mirror)."""
+    res = spawn_world(world, _in_core_worker, "single", 30, backend=backend, env={"FK_ASSIGN_F32": "split"})
+    ref = _single("single", 30)
+    a = np.concatenate([r[1] for r in res], axis=1)
+    assert np.array_equal(a, ref.assignments.numpy())
+    for c, _, hist, iters, merges in res:
+        assert iters == ref.iterations_run
+        assert np.array_equal(c, ref.centroids.numpy())
+        np.testing.assert_array_equal(hist, ref.objective_history)
+
+
+def test_sharded_stream_run_f32_split_path_bitwise():
+    res = spawn_world(2, _stream_worker, "single", 3001, True, "keep", "random_distinct",
+                      env={"FK_ASSIGN_F32": "split"})
+    ref, rc = _stream_single("single", 3001, "keep", "random_distinct")
+    a = np.concatenate([r[3] for r in res], axis=1)
+    assert np.array_equal(a, ref.assignments.numpy())
+    for lo, hi, c, _, hist, iters, merges, streamed in res:
+        assert iters == ref.iterations_run
+        assert np.array_equal(c, ref.centroids.numpy())
+        np.testing.assert_array_equal(hist, ref.objective_history)

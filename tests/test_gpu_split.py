@@ -194,3 +194,21 @@ def test_split_engine_lloyd_matches_oracle(ops, dtype):
         assert np.array_equal(eng.counts.cpu().numpy(), n_ref)
         assert np.array_equal(eng.master[eng.cur ^ 1].cpu().numpy(), c)
         eng.commit()
+
+
+def test_split_streamed_iteration_matches_oracle():
+    """out_of_core_iteration over a HostStream with chunks large enough for the
+    split path (per chunk 40000 x 64 x 32 multiply-adds): one streamed pass ==
+    the oracle's iteration, bitwise (f32)."""
+    import paper_2603_09229_b200 as fk
+
+    x = O.generate_dataset(1, 120000, 50, 32, 1.0, seed=31, dtype=np.float32)
+    K = 64
+    c0 = O.init_centroids(x, K, seed=32)
+    cfg = fk.KMeansConfig(K, max_iters=1, precision="single", tiling=fk.TilingConfig(64, 16, 120000))
+    new_c, store, _ = fk.out_of_core_iteration(fk.HostStream(torch.from_numpy(x), 40000),
+                                               fk.Centroids(torch.from_numpy(c0).cuda()), cfg, fk.Counters())
+    a_ref, _ = O.assign(x, c0)
+    s_ref, n_ref, _ = O.sort_inverse_update(x, a_ref, K, 120000)
+    c_ref, _ = O.normalize(s_ref, n_ref, c0)
+    assert np.array_equal(np.asarray(new_c.data.cpu()), c_ref)
