@@ -219,6 +219,19 @@ FK_API fk_status fk_objective_partials(fk_dtype mind_dt, const void* mind, int64
 FK_API fk_status fk_loop_tail(const double* partials, int64_t B, int64_t N, double* objective,
                               double* history, int64_t* history_row, int32_t* changed,
                               double* max_shift2, int64_t* merges, double* flags_out, void* stream);
+/* fk_normalize + fk_objective_partials + fk_loop_tail in ONE launch (the end
+ * of a single-device iteration): the normalize blocks also compute the
+ * objective partials of `mind` (same blocks and trees, so the same doubles)
+ * and the last block to finish runs fk_loop_tail's work.  `counter` is a
+ * device uint32 that is 0 before the call and left at 0.                   */
+FK_API fk_status fk_normalize_loop_tail(fk_dtype master_dt, const double* sums, const int64_t* counts,
+                                        const void* prev, void* out, fk_dtype operand_dt,
+                                        void* operand_out, uint8_t* empty_mask, double* max_shift2,
+                                        int64_t B, int64_t K, int64_t d, void* bias_out,
+                                        fk_dtype mind_dt, const void* mind, int64_t N, double* partials,
+                                        double* objective, double* history, int64_t* history_row,
+                                        int32_t* changed_flag, int64_t* merges, double* flags_out,
+                                        uint32_t* counter, void* stream);
 FK_API fk_status fk_objective(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N, double* out,
                        void* workspace, size_t workspace_bytes, void* stream);
 

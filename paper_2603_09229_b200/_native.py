@@ -64,6 +64,9 @@ def _declare(L):
     L.fk_normalize.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, P, P, P, I64, I64, I64, P, P]
     L.fk_objective_partials.restype = ctypes.c_int
     L.fk_objective_partials.argtypes = [ctypes.c_int, P, I64, I64, P, P]
+    L.fk_normalize_loop_tail.restype = ctypes.c_int
+    L.fk_normalize_loop_tail.argtypes = [ctypes.c_int, P, P, P, P, ctypes.c_int, P, P, P, I64, I64, I64, P,
+                                         ctypes.c_int, P, I64, P, P, P, P, P, P, P, P, P]
     L.fk_loop_tail.restype = ctypes.c_int
     L.fk_loop_tail.argtypes = [P, I64, I64, P, P, P, P, P, P, P, P]
     L.fk_row_norms.restype = ctypes.c_int
@@ -101,7 +104,7 @@ EXPORTED = (
     "fk_assign_xsplit", "fk_assign_split_workspace", "fk_assign_split", "fk_assign_split_fallback_rows",
     "fk_update_workspace",
     "fk_update", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
-    "fk_objective_partials", "fk_loop_tail", "fk_scatter",
+    "fk_objective_partials", "fk_loop_tail", "fk_normalize_loop_tail", "fk_scatter",
     "fk_stats_pack", "fk_merges_from_counts", "fk_farthest_workspace", "fk_farthest",
     "fk_kmeanspp_workspace", "fk_kmeanspp",
     "fk_kmeanspp_init", "fk_kmeanspp_sweep", "fk_kmeanspp_select",

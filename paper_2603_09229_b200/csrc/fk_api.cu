@@ -426,6 +426,28 @@ fk_status fk_normalize(fk_dtype master_dt, const double* sums, const int64_t* co
                                           reinterpret_cast<cudaStream_t>(stream)));
 }
 
+fk_status fk_normalize_loop_tail(fk_dtype master_dt, const double* sums, const int64_t* counts,
+                                 const void* prev, void* out, fk_dtype operand_dt, void* operand_out,
+                                 uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,
+                                 int64_t d, void* bias_out, fk_dtype mind_dt, const void* mind,
+                                 int64_t N, double* partials, double* objective, double* history,
+                                 int64_t* history_row, int32_t* changed_flag, int64_t* merges,
+                                 double* flags, uint32_t* counter, void* stream) {
+  if (master_dt != FK_F32 && master_dt != FK_F64) return FK_EINVAL;
+  if (operand_out && !valid_dt(operand_dt)) return FK_EINVAL;
+  if (!sums || !counts || !prev || !out || !empty_mask || !max_shift2 || B < 1 || K < 1 || d < 1)
+    return FK_EINVAL;
+  if (bias_out && !(operand_out && is_lowp(operand_dt))) return FK_EINVAL;
+  if (!valid_dt(mind_dt) || !mind || N < 1 || !partials || !objective || !changed_flag || !merges ||
+      !flags || !counter || (history && !history_row))
+    return FK_EINVAL;
+  return cuda_status(fk::launch_normalize_tail(
+      master_dt, sums, counts, prev, out, operand_dt, operand_out, empty_mask, max_shift2, B, K, d,
+      bias_out, fk::assign_tc_kpad(K), mind_dt == FK_F64 ? 1 : 0, mind, N, partials, objective,
+      history, history_row, changed_flag, merges, flags, counter,
+      reinterpret_cast<cudaStream_t>(stream)));
+}
+
 fk_status fk_objective_partials(fk_dtype mind_dt, const void* mind, int64_t B, int64_t N,
                                 double* partials, void* stream) {
   if (!valid_dt(mind_dt) || !mind || !partials || B < 1 || N < 1) return FK_EINVAL;

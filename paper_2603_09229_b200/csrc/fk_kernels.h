@@ -87,6 +87,14 @@ cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* c
                              const void* prev, void* out, int operand_dt, void* operand_out,
                              uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,
                              int64_t d, void* bias_out, int64_t bias_kpad, cudaStream_t stream);
+cudaError_t launch_normalize_tail(int master_dt, const double* sums, const int64_t* counts,
+                                  const void* prev, void* out, int operand_dt, void* operand_out,
+                                  uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,
+                                  int64_t d, void* bias_out, int64_t bias_kpad, int mind_f64,
+                                  const void* mind, int64_t N, double* part, double* obj,
+                                  double* hist, int64_t* hist_it, int32_t* changed,
+                                  int64_t* merges, double* flags, unsigned int* counter,
+                                  cudaStream_t s);
 cudaError_t launch_objective_partials(int mind_is_f64, const void* mind, int64_t B, int64_t N,
                                       double* part, cudaStream_t s);
 cudaError_t launch_loop_tail(const double* part, int64_t B, int64_t N, double* obj, double* hist,

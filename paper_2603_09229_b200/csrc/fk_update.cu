@@ -1493,12 +1493,32 @@ FK_DEV float op_to_f32(__half v) { return __half2float(v); }
 // k_cn_ext (lane-strided fmaf over the columns in increasing order, then an
 // xor-shuffle tree), so precomputing it here leaves the assignment bitwise
 // unchanged and saves the assign its own pass over C.
-template <typename TM, typename TO>
+// The end of a single-device iteration in the same launch (TAIL): the blocks
+// also compute the objective partials (k_obj_partial's blocks and tree, so the
+// same doubles) and the last block to finish runs k_loop_tail's work
+// (objective, history row, flags, cleared accumulators).
+struct TailArgs {
+  const void* mind;
+  int mind_f64;
+  int64_t B, N, nblk;
+  double* part;
+  double* obj;
+  double* hist;
+  int64_t* hist_it;
+  int32_t* changed;
+  int64_t* merges;
+  double* flags;
+  unsigned int* counter;
+};
+
+constexpr int OBJ_BLOCK_N = 8192;  // = OBJ_BLOCK (k_obj_partial's block), defined below
+
+template <typename TM, typename TO, bool TAIL = false>
 __global__ void __launch_bounds__(256)
     k_normalize(const double* __restrict__ sums, const int64_t* __restrict__ counts,
                 const TM* __restrict__ prev, TM* __restrict__ out, TO* __restrict__ operand,
                 uint8_t* __restrict__ empty, double* max_shift2, int64_t BK, int64_t d,
-                __nv_bfloat16* __restrict__ bias, int64_t K, int64_t kpad) {
+                __nv_bfloat16* __restrict__ bias, int64_t K, int64_t kpad, TailArgs ta = TailArgs{}) {
   __shared__ double wmax[8];
   // NORM_RW rows per warp, every load of a pass (64 columns of each row) issued
   // before the first division so the latencies overlap, and 4x fewer blocks
@@ -1589,6 +1609,73 @@ __global__ void __launch_bounds__(256)
       atomicMax((unsigned long long*)max_shift2, (unsigned long long)__double_as_longlong(mb));
     }
   }
+  if constexpr (TAIL) {
+    __shared__ double red[256];
+    const int t = threadIdx.x;
+    for (int64_t ob = blockIdx.x; ob < ta.B * ta.nblk; ob += gridDim.x) {  // k_obj_partial
+      const int64_t b = ob / ta.nblk, blk = ob - b * ta.nblk;
+      const int64_t lo = blk * OBJ_BLOCK_N;
+      const int64_t hi = (lo + OBJ_BLOCK_N < ta.N) ? lo + OBJ_BLOCK_N : ta.N;
+      double acc = 0.0;
+      if (ta.mind_f64) {
+        const double* m = reinterpret_cast<const double*>(ta.mind);
+        for (int64_t i = lo + t; i < hi; i += 256) acc += m[b * ta.N + i];
+      } else {
+        const float* m = reinterpret_cast<const float*>(ta.mind);
+        for (int64_t i = lo + t; i < hi; i += 256) acc += (double)m[b * ta.N + i];
+      }
+      __syncthreads();
+      red[t] = acc;
+      __syncthreads();
+      for (int s2 = 128; s2 > 0; s2 >>= 1) {
+        if (t < s2) red[t] += red[t + s2];
+        __syncthreads();
+      }
+      if (t == 0) ta.part[ob] = red[0];
+    }
+    // the last block to arrive finishes the iteration
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (t == 0) s_last = atomicAdd(ta.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const int lane2 = t & 31, w = t >> 5;
+      const int64_t row = ta.hist ? __ldcg(ta.hist_it) : 0;
+      for (int64_t b = w; b < ta.B; b += 8) {  // k_loop_tail's tree, 8 warps
+        double v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          double acc = 0.0;
+          for (int64_t i = lane2 + 32 * j; i < ta.nblk; i += 256) acc += __ldcg(ta.part + b * ta.nblk + i);
+          v[j] = acc;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] += v[j + 4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) v[j] += v[j + 2];
+        v[0] += v[1];
+        double x = v[0];
+        for (int s2 = 16; s2; s2 >>= 1) x += __shfl_down_sync(0xffffffffu, x, s2);
+        if (lane2 == 0) {
+          ta.obj[b] = x;
+          if (ta.hist) ta.hist[row * ta.B + b] = x;
+        }
+      }
+      __syncthreads();
+      if (t == 0) {
+        if (ta.hist) *ta.hist_it = row + 1;
+        ta.flags[0] = (double)__ldcg(ta.changed);
+        ta.flags[1] = __ldcg(max_shift2);
+        ta.flags[2] = (double)__ldcg(ta.merges);
+        *ta.changed = 0;
+        *max_shift2 = 0.0;
+        *ta.merges = 0;
+        *ta.counter = 0u;
+      }
+    }
+  }
 }
 
 template <typename TM>
@@ -1620,6 +1707,65 @@ static cudaError_t norm_dispatch(int operand_dt, const double* sums, const int64
   return cudaGetLastError();
 }
 
+template <typename TM>
+static cudaError_t norm_tail_dispatch(int operand_dt, const double* sums, const int64_t* counts,
+                                      const void* prev, void* out, void* operand_out, uint8_t* empty,
+                                      double* ms2, int64_t BK, int64_t d, void* bias, int64_t K,
+                                      int64_t kpad, const TailArgs& ta, cudaStream_t s) {
+  const int th = 256;
+  const int64_t rows_per_block = (th / 32) * NORM_RW;
+  const unsigned grid = (unsigned)((BK + rows_per_block - 1) / rows_per_block);
+  const TM* pv = (const TM*)prev;
+  TM* ov = (TM*)out;
+  __nv_bfloat16* bz = (__nv_bfloat16*)bias;
+  if (!operand_out)
+    k_normalize<TM, float, true><<<grid, th, 0, s>>>(sums, counts, pv, ov, nullptr, empty, ms2, BK, d,
+                                                     nullptr, K, kpad, ta);
+  else if (operand_dt == DT_BF16)
+    k_normalize<TM, __nv_bfloat16, true><<<grid, th, 0, s>>>(sums, counts, pv, ov,
+                                                             (__nv_bfloat16*)operand_out, empty, ms2,
+                                                             BK, d, bz, K, kpad, ta);
+  else if (operand_dt == DT_F16)
+    k_normalize<TM, __half, true><<<grid, th, 0, s>>>(sums, counts, pv, ov, (__half*)operand_out,
+                                                      empty, ms2, BK, d, bz, K, kpad, ta);
+  else if (operand_dt == DT_F32)
+    k_normalize<TM, float, true><<<grid, th, 0, s>>>(sums, counts, pv, ov, (float*)operand_out, empty,
+                                                     ms2, BK, d, nullptr, K, kpad, ta);
+  else
+    k_normalize<TM, double, true><<<grid, th, 0, s>>>(sums, counts, pv, ov, (double*)operand_out,
+                                                      empty, ms2, BK, d, nullptr, K, kpad, ta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_normalize_tail(int master_dt, const double* sums, const int64_t* counts,
+                                  const void* prev, void* out, int operand_dt, void* operand_out,
+                                  uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,
+                                  int64_t d, void* bias_out, int64_t bias_kpad, int mind_f64,
+                                  const void* mind, int64_t N, double* part, double* obj,
+                                  double* hist, int64_t* hist_it, int32_t* changed,
+                                  int64_t* merges, double* flags, unsigned int* counter,
+                                  cudaStream_t s) {
+  TailArgs ta;
+  ta.mind = mind;
+  ta.mind_f64 = mind_f64;
+  ta.B = B;
+  ta.N = N;
+  ta.nblk = (N + OBJ_BLOCK_N - 1) / OBJ_BLOCK_N;
+  ta.part = part;
+  ta.obj = obj;
+  ta.hist = hist;
+  ta.hist_it = hist_it;
+  ta.changed = changed;
+  ta.merges = merges;
+  ta.flags = flags;
+  ta.counter = counter;
+  if (master_dt == DT_F64)
+    return norm_tail_dispatch<double>(operand_dt, sums, counts, prev, out, operand_out, empty_mask,
+                                      max_shift2, B * K, d, bias_out, K, bias_kpad, ta, s);
+  return norm_tail_dispatch<float>(operand_dt, sums, counts, prev, out, operand_out, empty_mask,
+                                   max_shift2, B * K, d, bias_out, K, bias_kpad, ta, s);
+}
+
 cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* counts,
                              const void* prev, void* out, int operand_dt, void* operand_out,
                              uint8_t* empty_mask, double* max_shift2, int64_t B, int64_t K,
@@ -1636,7 +1782,7 @@ cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* c
 // For float32 min_dists every float64 partial sum is exact in practice, so
 // the result equals numpy's np.sum(m, dtype=float64) bit for bit; for
 // float64 data the summation order differs from numpy's pairwise tree.
-constexpr int OBJ_BLOCK = 8192;
+constexpr int OBJ_BLOCK = OBJ_BLOCK_N;
 
 template <typename T>
 __global__ void k_obj_partial(const T* __restrict__ m, int64_t B, int64_t N, int64_t nblk,

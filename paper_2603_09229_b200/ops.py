@@ -335,6 +335,22 @@ def loop_tail(partials: torch.Tensor, B: int, n: int, obj: torch.Tensor, changed
                                  flags.data_ptr(), _stream(dev)), "fk_loop_tail")
 
 
+def normalize_loop_tail(sums, counts, prev, out, operand_out, empty, shift2, bias_out, mind, partials,
+                        obj, changed, merges, flags, counter, history=None, history_row=None) -> None:
+    """normalize + objective partials + loop tail in one launch (fk_normalize_loop_tail)."""
+    dev = _require_cuda(sums, counts, prev, mind)
+    B, K, d = prev.shape
+    n = mind.shape[1]
+    odt = fk_dtype(operand_out.dtype) if operand_out is not None else 0
+    N.check(N.lib().fk_normalize_loop_tail(
+        fk_dtype(prev.dtype), sums.data_ptr(), counts.data_ptr(), prev.data_ptr(), out.data_ptr(), odt,
+        None if operand_out is None else operand_out.data_ptr(), empty.data_ptr(), shift2.data_ptr(),
+        B, K, d, None if bias_out is None else bias_out.data_ptr(), fk_dtype(mind.dtype), mind.data_ptr(),
+        n, partials.data_ptr(), obj.data_ptr(), None if history is None else history.data_ptr(),
+        None if history_row is None else history_row.data_ptr(), changed.data_ptr(), merges.data_ptr(),
+        flags.data_ptr(), counter.data_ptr(), _stream(dev)), "fk_normalize_loop_tail")
+
+
 FARTHEST_EMAX = 8192
 
 

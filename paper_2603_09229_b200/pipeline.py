@@ -129,6 +129,7 @@ class LloydEngine:
             self._flags_d = torch.zeros(3, dtype=torch.float64, device=dev)
             self._hist = None
             self._hist_row = torch.zeros((), dtype=torch.int64, device=dev)
+            self._tail_ctr = torch.zeros((1,), dtype=torch.int32, device=dev)  # last-block counter
             if self.dtype in LOW_PRECISION:
                 kpad = ops.N.lib().fk_assign_bias_rows(K)
                 self.bias = [torch.zeros((B, kpad, 16), dtype=torch.bfloat16, device=dev) for _ in range(2)]
@@ -285,16 +286,20 @@ class LloydEngine:
         nxt = self.cur ^ 1
 
         def fn_fused():
-            ops.objective_partials(self.mind, self._part)
+            # objective partials, normalize and the loop tail are one launch
+            # (fk_normalize_loop_tail) after the update
             if timers is not None:  # bench: live per-kernel timing (eager only)
                 timers[0].record()
             self.be.update(self.x, self.ids[slot], self.K, self.chunk, sums=self.sums,
                            counts=self.counts, merges=self.merges_it)
             if timers is not None:
                 timers[1].record()
-            self._normalize(nxt)
-            ops.loop_tail(self._part, self.B, self.N, self.obj, self.changed, self.shift2, self.merges_it,
-                          self._flags_d, self._hist, None if self._hist is None else self._hist_row)
+            ops.normalize_loop_tail(
+                self.sums, self.counts, self.master[self.cur], self.master[nxt],
+                None if self.operand is self.master else self.operand[nxt], self.empty, self.shift2,
+                None if self.bias is None else self.bias[nxt], self.mind, self._part, self.obj, self.changed,
+                self.merges_it, self._flags_d, self._tail_ctr, self._hist,
+                None if self._hist is None else self._hist_row)
 
         def fn():
             self.shift2.zero_()
