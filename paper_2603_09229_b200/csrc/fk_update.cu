@@ -1060,7 +1060,13 @@ constexpr int kSegWarpsPerSm = 32;
 // and config 4 from 52 to 49.5 us, config 3 unchanged; 16 starves config 3
 // of bytes in flight), at least 64 points each.
 static int64_t segsum_slice(int64_t P, int num_sms) {
-  const int64_t want = (int64_t)num_sms * kSegWarpsPerSm;
+  static int wps = -1;  // FK_SEGSUM_WPS: warp slices per SM (A/B)
+  if (wps < 0) {
+    const char* e = getenv("FK_SEGSUM_WPS");
+    wps = e ? atoi(e) : kSegWarpsPerSm;
+    if (wps < 1 || wps > 64) wps = kSegWarpsPerSm;
+  }
+  const int64_t want = (int64_t)num_sms * wps;
   int64_t L = (P + want - 1) / want;
   return L < 64 ? 64 : L;
 }
