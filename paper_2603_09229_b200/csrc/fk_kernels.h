@@ -118,6 +118,9 @@ cudaError_t launch_farthest(int mind_is_f64, const void* mind, int64_t B, int64_
                             int64_t* idx_out, void* ws, int num_sms, cudaStream_t s);
 
 // fk_kmeanspp.cu
+size_t pairwise_total_workspace(int64_t B, int64_t N);
+cudaError_t launch_pairwise_total(const double* m, int64_t B, int64_t N, double* out, void* ws,
+                                  cudaStream_t s);
 size_t kmeanspp_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d);
 cudaError_t launch_kmeanspp_init(int32_t* halted, void* ws, int64_t B, int64_t N, int64_t K,
                                  cudaStream_t s);

@@ -622,7 +622,7 @@ __global__ void __launch_bounds__(256) k_pp_node(const double* __restrict__ m, i
   __shared__ int nleaf;
   __shared__ DD wb[32];
   const int b = blockIdx.y;
-  if (halted[b] < j) return;
+  if (halted && halted[b] < j) return;
   const int64_t node = blockIdx.x;
   int64_t lo0, n0;
   pw_walk(N, t1, node, lo0, n0);
@@ -724,7 +724,7 @@ __global__ void __launch_bounds__(256) k_pp_tier(const double* __restrict__ in, 
   __shared__ double A[1 << kTierLevels];
   __shared__ double Bf[1 << (kTierLevels - 1)];
   const int b = blockIdx.y;
-  if (halted[b] < j) return;
+  if (halted && halted[b] < j) return;
   const int L = t_in - t_out;
   const int cnt = 1 << L;
   const double* src = in + b * ((int64_t)1 << t_in) + (int64_t)blockIdx.x * cnt;
@@ -1510,6 +1510,41 @@ cudaError_t launch_kmeanspp_sweep(int dt, const void* X, int64_t B, int64_t rows
                                   cudaStream_t s) {
   return sweep_dispatch(dt, X, B, rows, (int)d, x_sb, cen, cen_sb, idx, K, col, m, m_sb, first,
                         halted, j, s);
+}
+
+// numpy's pairwise sum (np.sum of a contiguous float64 array) of every row of
+// the (B, N) table m -- the objective of f64 data (pipeline._objective_row):
+// the bottom nodes and tiers of the k-means++ total, no selection.  Returns
+// cudaErrorInvalidValue for the (tiny) sizes the node plan does not cover.
+size_t pairwise_total_workspace(int64_t B, int64_t N) {
+  const Plan p = make_plan(N);
+  const size_t nb = (size_t)1 << p.t1;
+  return al256(B * nb * 8) + al256(B * std::max<size_t>(1, nb >> kTierLevels) * 8 + 8 * B) +
+         al256(B * nb * 16);
+}
+
+cudaError_t launch_pairwise_total(const double* m, int64_t B, int64_t N, double* out, void* ws,
+                                  cudaStream_t s) {
+  const Plan p = make_plan(N);
+  if (!p.valid || p.rdepth > kNodeLevels) return cudaErrorInvalidValue;
+  const size_t nb = (size_t)1 << p.t1;
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  double* vals = reinterpret_cast<double*>(base);
+  double* vals2 = reinterpret_cast<double*>(base + al256(B * nb * 8));
+  double2* dd = reinterpret_cast<double2*>(base + al256(B * nb * 8) +
+                                           al256(B * std::max<size_t>(1, nb >> kTierLevels) * 8 + 8 * B));
+  dim3 g1((unsigned)nb, (unsigned)B);
+  k_pp_node<<<g1, 256, 0, s>>>(m, N, N, p.t1, p.rdepth, nullptr, 0, p.t1 == 0 ? out : vals, dd);
+  const double* in = vals;
+  for (size_t k = 0; k < p.tiers.size(); ++k) {
+    const int t_in = p.tiers[k];
+    const int t_out = std::max(0, t_in - kTierLevels);
+    double* o = t_out == 0 ? out : ((k & 1) ? vals : vals2);
+    dim3 g((unsigned)((int64_t)1 << t_out), (unsigned)B);
+    k_pp_tier<<<g, 256, 0, s>>>(in, t_in, o, t_out, nullptr, 0);
+    in = o;
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_kmeanspp_select(const double* m, int64_t B, int64_t N, const double* u,

@@ -1515,6 +1515,7 @@ struct TailArgs {
   int64_t* merges;
   double* flags;
   unsigned int* counter;
+  int obj_ready;  // obj[] already holds the objective (f64 min_dists: numpy's pairwise tree)
 };
 
 constexpr int OBJ_BLOCK_N = 8192;  // = OBJ_BLOCK (k_obj_partial's block), defined below
@@ -1618,7 +1619,7 @@ __global__ void __launch_bounds__(256)
   if constexpr (TAIL) {
     __shared__ double red[256];
     const int t = threadIdx.x;
-    for (int64_t ob = blockIdx.x; ob < ta.B * ta.nblk; ob += gridDim.x) {  // k_obj_partial
+    for (int64_t ob = blockIdx.x; !ta.obj_ready && ob < ta.B * ta.nblk; ob += gridDim.x) {  // k_obj_partial
       const int64_t b = ob / ta.nblk, blk = ob - b * ta.nblk;
       const int64_t lo = blk * OBJ_BLOCK_N;
       const int64_t hi = (lo + OBJ_BLOCK_N < ta.N) ? lo + OBJ_BLOCK_N : ta.N;
@@ -1650,6 +1651,10 @@ __global__ void __launch_bounds__(256)
       const int lane2 = t & 31, w = t >> 5;
       const int64_t row = ta.hist ? __ldcg(ta.hist_it) : 0;
       for (int64_t b = w; b < ta.B; b += 8) {  // k_loop_tail's tree, 8 warps
+        if (ta.obj_ready) {
+          if (lane2 == 0 && ta.hist) ta.hist[row * ta.B + b] = __ldcg(ta.obj + b);
+          continue;
+        }
         double v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -1765,6 +1770,10 @@ cudaError_t launch_normalize_tail(int master_dt, const double* sums, const int64
   ta.merges = merges;
   ta.flags = flags;
   ta.counter = counter;
+  ta.obj_ready = 0;
+  if (mind_f64 && launch_pairwise_total((const double*)mind, B, N, obj, part, s) == cudaSuccess)
+    ta.obj_ready = 1;  // part is the objective workspace (objective_workspace_bytes)
+  (void)cudaGetLastError();
   if (master_dt == DT_F64)
     return norm_tail_dispatch<double>(operand_dt, sums, counts, prev, out, operand_out, empty_mask,
                                       max_shift2, B * K, d, bias_out, K, bias_kpad, ta, s);
@@ -1890,11 +1899,19 @@ cudaError_t launch_loop_tail(const double* part, int64_t B, int64_t N, double* o
 }
 
 size_t objective_workspace_bytes(int64_t B, int64_t N) {
-  return (size_t)(B * ((N + OBJ_BLOCK - 1) / OBJ_BLOCK)) * 8 + 256;
+  const size_t tree = (size_t)(B * ((N + OBJ_BLOCK - 1) / OBJ_BLOCK)) * 8 + 256;
+  const size_t pw = pairwise_total_workspace(B, N);  // f64 min_dists: numpy's pairwise order
+  return tree > pw ? tree : pw;
 }
 
 cudaError_t launch_objective(int mind_is_f64, const void* mind, int64_t B, int64_t N, double* out,
                              void* ws, cudaStream_t s) {
+  // f64 min_dists (f64 data): np.sum's pairwise tree exactly (bitwise); f32
+  // min_dists: the fixed two-level tree (every f64 partial of f32 values is
+  // exact in practice, so any order gives numpy's double)
+  if (mind_is_f64 && launch_pairwise_total((const double*)mind, B, N, out, ws, s) == cudaSuccess)
+    return cudaSuccess;
+  (void)cudaGetLastError();
   const int64_t nblk = (N + OBJ_BLOCK - 1) / OBJ_BLOCK;
   double* part = (double*)ws;
   dim3 grid((unsigned)nblk, (unsigned)B);

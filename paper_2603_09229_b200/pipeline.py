@@ -125,7 +125,9 @@ class LloydEngine:
         if self.fused:
             from .ops import OBJ_BLOCK
 
-            self._part = torch.empty((B * -(-N // OBJ_BLOCK),), dtype=torch.float64, device=dev)
+            # objective partials (f32 min_dists) or numpy's pairwise-tree workspace (f64)
+            nb = max(int(ops.N.lib().fk_objective_workspace(B, N)), B * -(-N // OBJ_BLOCK) * 8)
+            self._part = torch.empty((-(-nb // 8),), dtype=torch.float64, device=dev)
             self._flags_d = torch.zeros(3, dtype=torch.float64, device=dev)
             self._hist = None
             self._hist_row = torch.zeros((), dtype=torch.int64, device=dev)

@@ -73,3 +73,34 @@ def test_update_f64_repeatable(ops):
     s1 = s1.clone()
     s2, _ = ops.update(x, ids, 128, 4096)
     assert torch.equal(s1.view(torch.int64), s2.view(torch.int64))
+
+
+@pytest.mark.parametrize("N", [1, 7, 8, 129, 1000, 4097, 100000, 1 << 20])
+def test_objective_f64_is_numpys_pairwise_sum(ops, N):
+    """pipeline._objective_row for f64 data: np.sum(m, dtype=float64) of a float64
+    row is numpy's pairwise summation -- reproduced addition for addition."""
+    rng = np.random.default_rng(N)
+    m = rng.random((3, N)) * np.exp(rng.uniform(-30, 30, (3, N)))
+    out = ops.objective(torch.from_numpy(m).cuda()).cpu().numpy()
+    ref = np.array([np.sum(m[b], dtype=np.float64) for b in range(3)])
+    assert np.array_equal(out.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("B,N,K,d", [(2, 30000, 24, 16), (1, 70000, 200, 32)])
+def test_f64_lloyd_run_every_field_bitwise(B, N, K, d):
+    """f64 data end to end (the reference's default precision): centroids,
+    assignments, objective history, iteration count and merge counter equal the
+    oracle's lloyd_run bit for bit (assign certified or exact mirror, update in
+    the reference's serial order, objective in numpy's pairwise order)."""
+    import paper_2603_09229_b200 as fk
+
+    x = O.generate_dataset(B, N, K, d, 1.0, seed=5, dtype=np.float64)
+    c0 = O.init_centroids(x, K, seed=6)
+    c_ref, a_ref, h_ref, it_ref, m_ref = O.lloyd_run(x, K, max_iters=8, c0=c0, chunk=4096)
+    cfg = fk.KMeansConfig(K, max_iters=8, seed=6, precision="double", tiling=fk.TilingConfig(64, 16, 4096))
+    r = fk.lloyd_run(fk.DataMatrix(torch.from_numpy(x).cuda()), cfg)
+    assert r.iterations_run == it_ref
+    assert np.array_equal(np.asarray(r.assignments.values.cpu()), a_ref)
+    assert np.array_equal(np.asarray(r.centroids.data.cpu()).view(np.uint64), c_ref.view(np.uint64))
+    assert np.array_equal(np.asarray(r.objective_history).view(np.uint64), h_ref.view(np.uint64))
+    assert r.counters.synchronized_merges == m_ref
