@@ -385,7 +385,7 @@ fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void* bias,
 // ------------------------------------------------------------------ update
 size_t fk_update_workspace(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d) {
   if (!valid_dt(dt) || B < 1 || N < 1 || K < 1 || d < 1) return 0;
-  return fk::update_workspace_bytes(B, N, K, d);
+  return fk::update_workspace_bytes(dt, B, N, K, d);
 }
 
 fk_status fk_update(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,

@@ -76,7 +76,7 @@ cudaError_t launch_assign_cuda_core_lowp(int dt, const void* X, const void* C, c
                                          cudaStream_t stream);
 
 // fk_update.cu
-size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d);
+size_t update_workspace_bytes(int dt, int64_t B, int64_t N, int64_t K, int64_t d);
 cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
                           int64_t K, int64_t d, int64_t chunk, int accumulate, double* sums,
                           int64_t* counts, int64_t* merges, void* ws, int num_sms,

@@ -1053,6 +1053,7 @@ static int64_t update_bpb(int64_t B, int64_t N, int64_t K, int num_sms) {
   return bpb < 1 ? 1 : bpb;
 }
 constexpr int kMaxSms = 256;  // workspace bound for any sm_100 part
+constexpr int64_t kF64MaxSpans = 1024;  // f64 pieces path: update_chunk >= N / 1024
 constexpr int kSegWarpsPerSm = 32;
 
 // Slice length of k_segsum: 32 warp slices per SM (same-box A/B,
@@ -1166,14 +1167,19 @@ struct UpdateWs {
   int32_t* inval;
 };
 
-static size_t update_ws_layout(int64_t B, int64_t N, int64_t K, int64_t d, int num_sms, void* base,
+static size_t update_ws_layout(int dt, int64_t B, int64_t N, int64_t K, int64_t d, int num_sms, void* base,
                                UpdateWs* ws) {
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const int64_t BK = B * K, P = B * N;
   const int64_t bpb = update_bpb(B, N, K, num_sms);
   const int64_t slices = (P + segsum_slice(P, num_sms) - 1) / segsum_slice(P, num_sms);
+  // segment partials: per-slice boundary partials, or the f64 path's pieces
+  // (B * (K + kF64MaxSpans) rows of d)
+  const int64_t spans = N < kF64MaxSpans ? N : kF64MaxSpans;
+  const size_t part = std::max((size_t)slices * 2 * d * 8,
+                               dt == DT_F64 ? (size_t)(B * (K + spans)) * d * 8 : (size_t)0);
   const size_t sz[7] = {al((size_t)B * bpb * K * 4), al((size_t)BK * 4), al((size_t)(BK + 1) * 8),
-                        al((size_t)P * 4),           al((size_t)BK * 4), al((size_t)slices * 2 * d * 8),
+                        al((size_t)P * 4),           al((size_t)BK * 4), al(part),
                         al((size_t)B * bpb * 4)};
   size_t total = 0;
   uint8_t* p = static_cast<uint8_t*>(base);
@@ -1194,9 +1200,9 @@ static size_t update_ws_layout(int64_t B, int64_t N, int64_t K, int64_t d, int n
   return total;
 }
 
-size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d) {
+size_t update_workspace_bytes(int dt, int64_t B, int64_t N, int64_t K, int64_t d) {
   // blocks and slices grow with the SM count: size for the largest sm_100 part
-  return update_ws_layout(B, N, K, d, kMaxSms, nullptr, nullptr);
+  return update_ws_layout(dt, B, N, K, d, kMaxSms, nullptr, nullptr);
 }
 
 // ------------------------------------------------------- serial f64 segsum
@@ -1208,10 +1214,76 @@ size_t update_workspace_bytes(int64_t B, int64_t N, int64_t K, int64_t d) {
 // merged into the key's sum in ascending span order, again from 0.0
 // (merge_segments).  A streamed chunk's result is added to the running sums
 // (PartialStats.combine, pipeline.py:250-257) when `accumulate`.
-// One warp per (key, 32-feature group): lane f walks the key's run and keeps
-// exactly that order; U rows are gathered ahead (independent loads) before
-// the dependent adds.  Bandwidth-bound when the clusters are balanced; the
-// longest cluster's run is the serial critical path.
+// Two kernels, so that a key's run is cut at the span boundaries into pieces
+// that are summed in parallel (the serial critical path is one piece, not one
+// cluster): k_seg_pieces, one warp per (key, piece, 32 features), sums its
+// piece serially from 0.0 in sorted order into slot key + span (a key's
+// pieces occupy consecutive spans, so slots never collide); k_seg_fold, one
+// thread per (key, feature), folds the key's pieces in span order from 0.0.
+// Rows are gathered U ahead of the dependent adds.
+template <int U>
+__global__ void __launch_bounds__(256)
+    k_seg_pieces(const double* __restrict__ X, const int32_t* __restrict__ order,
+                 const int64_t* __restrict__ off, int64_t BK, int64_t K, int d, int fgs,
+                 int64_t chunk, int64_t ns, int jw, double* __restrict__ part) {
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= BK * jw * fgs) return;
+  const int64_t key = warp / ((int64_t)jw * fgs);
+  const int64_t rem = warp - key * jw * fgs;
+  const int j0 = (int)(rem / fgs);
+  const int f = (int)(rem - (int64_t)j0 * fgs) * 32 + lane;
+  const bool act = f < d;
+  const int64_t b = key / K;
+  const int64_t s = off[key], e = off[key + 1], base = off[b * K];
+  if (e <= s) return;
+  const int64_t m0 = (s - base) / chunk, m1 = (e - 1 - base) / chunk;  // spans of the key's run
+  for (int64_t m = m0 + j0; m <= m1; m += jw) {
+    const int64_t p0 = s > base + m * chunk ? s : base + m * chunk;
+    const int64_t p1 = e < base + (m + 1) * chunk ? e : base + (m + 1) * chunk;
+    double acc = 0.0;
+    // the sorted-order indices of the next U rows are fetched while this
+    // batch's rows are in flight
+    int32_t ri[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) ri[u] = p0 + u < p1 ? __ldg(order + p0 + u) : 0;
+    for (int64_t q0 = p0; q0 < p1; q0 += U) {
+      double v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = (act && q0 + u < p1) ? __ldg(X + (int64_t)ri[u] * d + f) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) ri[u] = q0 + U + u < p1 ? __ldg(order + q0 + U + u) : 0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q0 + u < p1) acc = __dadd_rn(acc, v[u]);
+    }
+    if (act) part[((key - b * K) + b * (K + ns) + m) * d + f] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    k_seg_fold(const int64_t* __restrict__ off, int64_t BK, int64_t K, int d, int64_t chunk,
+               int64_t ns, const double* __restrict__ part, double* __restrict__ sums,
+               int accumulate) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= BK * d) return;
+  const int64_t key = i / d;
+  const int f = (int)(i - key * d);
+  const int64_t b = key / K;
+  const int64_t s = off[key], e = off[key + 1], base = off[b * K];
+  double tot = 0.0;
+  if (e > s) {
+    const int64_t m0 = (s - base) / chunk, m1 = (e - 1 - base) / chunk;
+    for (int64_t m = m0; m <= m1; ++m)
+      tot = __dadd_rn(tot, part[((key - b * K) + b * (K + ns) + m) * d + f]);
+  }
+  double* o = sums + key * d + f;
+  *o = accumulate ? __dadd_rn(*o, tot) : tot;
+}
+
+// Spans beyond what the piece slots hold (update_chunk << N / 4096): one warp
+// per (key, 32 features) walks the key's whole run, closing a segment at every
+// span boundary (same order, no partial storage).
 template <int U>
 __global__ void __launch_bounds__(256)
     k_segsum_serial(const double* __restrict__ X, const int32_t* __restrict__ order,
@@ -1254,6 +1326,7 @@ __global__ void __launch_bounds__(256)
     *o = accumulate ? __dadd_rn(*o, tot) : tot;
   }
 }
+
 
 static bool segsum_f64_serial() {
   static int v = -1;  // FK_SEGSUM_F64=parallel: the slice-parallel k_segsum for f64 (A/B)
@@ -1434,7 +1507,7 @@ cudaError_t launch_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, 
                            int64_t* off_out, void* ws, int num_sms, cudaStream_t s) {
   const int sms = num_sms < kMaxSms ? num_sms : kMaxSms;
   UpdateWs w;
-  update_ws_layout(B, N, K, 1, sms, ws, &w);
+  update_ws_layout(DT_F32, B, N, K, 1, sms, ws, &w);
   w.order = order_out;
   w.off = off_out;
   const int64_t bpb = update_bpb(B, N, K, sms);
@@ -1454,7 +1527,7 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   const int64_t BK = B * K, P = B * N;
   const int sms = num_sms < kMaxSms ? num_sms : kMaxSms;
   UpdateWs w;
-  update_ws_layout(B, N, K, d, sms, ws, &w);
+  update_ws_layout(dt, B, N, K, d, sms, ws, &w);
   const int64_t bpb = update_bpb(B, N, K, sms);
   const unsigned blocks = (unsigned)(B * bpb);
   cudaError_t e;
@@ -1475,9 +1548,23 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
     default:
       if (segsum_f64_serial()) {
         const int fgs = (int)((d + 31) / 32);
-        const int64_t threads = BK * fgs * 32;
-        k_segsum_serial<8><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-            (const double*)X, w.order, w.off, BK, K, (int)d, fgs, ch, sums, accumulate);
+        const int64_t ns = (N + ch - 1) / ch;  // spans per batch element
+        if (ns <= kF64MaxSpans) {
+          // piece warps per key: about the spans an average run touches (a
+          // longer run loops), so the grid stays near one warp per piece
+          int64_t jwe = (N + K * ch - 1) / (K * ch) + 1;
+          if (jwe > ns) jwe = ns;
+          const int jw = (int)(jwe < 1 ? 1 : (jwe > 64 ? 64 : jwe));
+          const int64_t threads = BK * jw * fgs * 32;
+          k_seg_pieces<16><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+              (const double*)X, w.order, w.off, BK, K, (int)d, fgs, ch, ns, jw, w.part);
+          k_seg_fold<<<(unsigned)((BK * d + 255) / 256), 256, 0, s>>>(w.off, BK, K, (int)d, ch, ns,
+                                                                    w.part, sums, accumulate);
+        } else {
+          const int64_t threads = BK * fgs * 32;
+          k_segsum_serial<16><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+              (const double*)X, w.order, w.off, BK, K, (int)d, fgs, ch, sums, accumulate);
+        }
         return cudaGetLastError();
       }
       return dispatch_segsum<double, double>(X, w, BK, P, d, sums, sms, s, ids, N, K);

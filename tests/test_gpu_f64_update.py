@@ -30,6 +30,7 @@ def rough_data(rng, B, N, d):
 @pytest.mark.parametrize("B,N,K,d,chunk", [
     (1, 1, 1, 1, 1), (1, 1000, 8, 16, 256), (2, 5000, 37, 33, 777), (1, 20000, 300, 64, 20000),
     (3, 4096, 64, 128, 1000), (1, 9000, 1, 5, 64), (1, 3000, 4000, 24, 512),
+    (1, 5000, 3, 8, 2),  # > 1024 spans: the single-walk kernel
 ])
 def test_update_f64_bitwise(ops, B, N, K, d, chunk):
     rng = np.random.default_rng(N + K + d)
