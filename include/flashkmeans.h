@@ -207,7 +207,7 @@ FK_API fk_status fk_row_norms(fk_dtype dt, const void* M, int64_t rows, int64_t 
  * equals numpy's np.sum(m, dtype=float64) bit for bit.                      */
 FK_API size_t fk_objective_workspace(int64_t B, int64_t N);
 /* The two halves of fk_objective for the device-resident loop:
- * fk_objective_partials writes B * ceil(N / 8192) fixed-order partials;
+ * fk_objective_partials writes B * ceil(N / 8192) partials (numpy's buffer order);
  * fk_loop_tail (one launch at the end of an iteration) reduces them into
  * objective[b] (bitwise fk_objective's result) and, when history is given,
  * into history[*history_row * B + b] (then ++*history_row: the row index

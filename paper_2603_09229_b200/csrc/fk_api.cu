@@ -444,7 +444,7 @@ fk_status fk_normalize_loop_tail(fk_dtype master_dt, const double* sums, const i
   return cuda_status(fk::launch_normalize_tail(
       master_dt, sums, counts, prev, out, operand_dt, operand_out, empty_mask, max_shift2, B, K, d,
       bias_out, fk::assign_tc_kpad(K), mind_dt == FK_F64 ? 1 : 0, mind, N, partials, objective,
-      history, history_row, changed_flag, merges, flags, counter,
+      history, history_row, changed_flag, merges, flags, counter, dev_info().sms,
       reinterpret_cast<cudaStream_t>(stream)));
 }
 

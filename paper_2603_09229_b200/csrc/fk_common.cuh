@@ -283,6 +283,140 @@ FK_DEV bool elect_one() {
   return pred != 0;
 }
 
+
+// ---------------------------------------------------------------------------
+// numpy's float64 reduction order for np.sum(m, dtype=float64) of a float32
+// row m (pipeline._objective_row, the objective of every non-f64 run): the
+// ufunc machinery casts the row through its 8192-element buffer
+// (np.getbufsize()) and adds each buffer's pairwise_sum_DOUBLE
+// (numpy/_core/src/umath/loops_utils.h.src: leaves of <= 128 values summed by
+// 8 interleaved accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+// above that a split at n/2 rounded down to a multiple of 8) into the running
+// sum in buffer order.  np_pairwise_block reproduces one buffer's pairwise sum
+// with a block of threads; the buffer sums are then folded in order from 0.0.
+// (Pinned by tests/test_gpu_kernels.py against numpy on inexact data.)
+constexpr int kNpBuf = 8192;
+constexpr int kNpLeaf = 128;
+constexpr int kNpDepth = 7;       // max recursion depth for n <= 8192
+constexpr int kNpMaxLeaves = 72;  // max leaves for n <= 8192 is 65
+
+__host__ __device__ inline int np_split(int n) {
+  const int h = n >> 1;
+  return h - (h & 7);
+}
+
+struct NpScratch {
+  double V[(2 << kNpDepth) - 1];  // node values, heap order
+  uint8_t kind[(2 << kNpDepth) - 1];  // 0 absent, 1 leaf, 2 internal
+  int16_t leaf_lo[kNpMaxLeaves], leaf_n[kNpMaxLeaves], leaf_v[kNpMaxLeaves];
+  int nleaf;
+};
+
+// Pairwise sum of src[0, n0) (n0 <= 8192, each value cast to double) by the
+// whole block (every thread calls it; >= 64 threads); the result is returned
+// to every thread.
+template <typename T>
+FK_DEV double np_leaf8(const T* __restrict__ src, int lo, int n, int sub) {
+  // numpy's leaf (8 <= n <= 128 or shorter): lane `sub` of an 8-lane group is
+  // accumulator r[sub]; its <= 16 loads issued before the serial adds
+  const int body = n >= 8 ? n - (n % 8) : 0;
+  double v[kNpLeaf / 8];
+#pragma unroll
+  for (int i = 0; i < kNpLeaf / 8; ++i) v[i] = 8 * i < body ? (double)src[lo + 8 * i + sub] : 0.0;
+  double r = v[0];
+#pragma unroll
+  for (int i = 1; i < kNpLeaf / 8; ++i)
+    if (8 * i < body) r = __dadd_rn(r, v[i]);
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+  r = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+  double res = body > 0 ? r : 0.0;  // lane sub == 0 adds the tail
+  if (sub == 0)
+    for (int i = body; i < n; ++i) res = __dadd_rn(res, (double)src[lo + i]);
+  return res;
+}
+
+template <typename T>
+__device__ double np_pairwise_block(const T* __restrict__ src, int n0, NpScratch& s) {
+  if (n0 == kNpBuf) {
+    // a full buffer: 64 leaves of 128 under a perfect binary tree
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane & 7;
+    const int nw = blockDim.x >> 5;
+    for (int L0 = warp * 4; L0 < kNpBuf / kNpLeaf; L0 += nw * 4) {
+      const int L = L0 + (lane >> 3);
+      const double v = np_leaf8(src, L * kNpLeaf, kNpLeaf, sub);
+      if (sub == 0) s.V[L] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      double x = __dadd_rn(s.V[2 * lane], s.V[2 * lane + 1]);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {  // left + right at every level
+        const double y = __shfl_down_sync(0xffffffffu, x, o);
+        if ((lane & (2 * o - 1)) == 0) x = __dadd_rn(x, y);
+      }
+      if (lane == 0) s.V[64] = x;
+    }
+    __syncthreads();
+    return s.V[64];
+  }
+  if (threadIdx.x == 0) s.nleaf = 0;
+  __syncthreads();
+  // A: classify the nodes of the recursion tree (heap index), list the leaves
+  for (int r = 0; r <= kNpDepth; ++r) {
+    const int cnt = 1 << r;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+      int lo = 0, n = n0;
+      bool exists = true;
+      for (int t = r - 1; t >= 0; --t) {
+        if (n <= kNpLeaf) {
+          exists = false;
+          break;
+        }
+        const int h = np_split(n);
+        if ((q >> t) & 1) {
+          lo += h;
+          n -= h;
+        } else {
+          n = h;
+        }
+      }
+      const int vi = cnt - 1 + q;
+      s.kind[vi] = !exists ? 0 : (n <= kNpLeaf ? 1 : 2);
+      if (exists && n <= kNpLeaf) {
+        const int k = atomicAdd(&s.nleaf, 1);
+        s.leaf_lo[k] = (int16_t)lo;
+        s.leaf_n[k] = (int16_t)n;
+        s.leaf_v[k] = (int16_t)vi;
+      }
+    }
+  }
+  __syncthreads();
+  // B: leaves, 8 lanes each (lane k = accumulator r[k], its <= 16 loads in
+  // flight before the serial adds), combined by xor shuffles 1, 2, 4
+  {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, sub = lane & 7;
+    const int nw = blockDim.x >> 5, nleaf = s.nleaf;
+    for (int L0 = warp * 4; L0 < nleaf; L0 += nw * 4) {
+      const int L = L0 + (lane >> 3);
+      const bool act = L < nleaf;
+      const double v = np_leaf8(src, act ? s.leaf_lo[L] : 0, act ? s.leaf_n[L] : 0, sub);
+      if (act && sub == 0) s.V[s.leaf_v[L]] = v;
+    }
+  }
+  __syncthreads();
+  // C: internal nodes bottom-up
+  for (int r = kNpDepth - 1; r >= 0; --r) {
+    const int cnt = 1 << r;
+    for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+      const int vi = cnt - 1 + q;
+      if (s.kind[vi] == 2) s.V[vi] = __dadd_rn(s.V[2 * vi + 1], s.V[2 * vi + 2]);
+    }
+    __syncthreads();
+  }
+  return s.V[0];
+}
+
 }  // namespace fk
 
 // One empty kernel per translation unit: its address identifies the unit's

@@ -94,7 +94,7 @@ cudaError_t launch_normalize_tail(int master_dt, const double* sums, const int64
                                   const void* mind, int64_t N, double* part, double* obj,
                                   double* hist, int64_t* hist_it, int32_t* changed,
                                   int64_t* merges, double* flags, unsigned int* counter,
-                                  cudaStream_t s);
+                                  int num_sms, cudaStream_t s);
 cudaError_t launch_objective_partials(int mind_is_f64, const void* mind, int64_t B, int64_t N,
                                       double* part, cudaStream_t s);
 cudaError_t launch_loop_tail(const double* part, int64_t B, int64_t N, double* obj, double* hist,

@@ -1603,9 +1603,21 @@ struct TailArgs {
   double* flags;
   unsigned int* counter;
   int obj_ready;  // obj[] already holds the objective (f64 min_dists: numpy's pairwise tree)
+  int64_t norm_blocks;  // blocks that normalize; the rest sum objective partials
 };
 
-constexpr int OBJ_BLOCK_N = 8192;  // = OBJ_BLOCK (k_obj_partial's block), defined below
+// Objective partials: numpy's order for np.sum(m, dtype=float64) of an f32
+// row (np_pairwise_block, fk_common.cuh): one partial per 8192-element buffer,
+// folded in buffer order from 0.0 (obj_fold).  f64 rows: launch_pairwise_total.
+constexpr int OBJ_BLOCK_N = kNpBuf;
+constexpr int TAIL_STAGE = 4096;  // objective partials the last block stages in shared memory
+
+// obj = ((0 + part[0]) + part[1]) + ... (numpy's running sum over its buffers)
+FK_DEV double obj_fold(const double* part, int64_t n) {
+  double acc = 0.0;
+  for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, part[i]);
+  return acc;
+}
 
 template <typename TM, typename TO, bool TAIL = false>
 __global__ void __launch_bounds__(256)
@@ -1613,153 +1625,151 @@ __global__ void __launch_bounds__(256)
                 const TM* __restrict__ prev, TM* __restrict__ out, TO* __restrict__ operand,
                 uint8_t* __restrict__ empty, double* max_shift2, int64_t BK, int64_t d,
                 __nv_bfloat16* __restrict__ bias, int64_t K, int64_t kpad, TailArgs ta = TailArgs{}) {
-  __shared__ double wmax[8];
-  // NORM_RW rows per warp, every load of a pass (64 columns of each row) issued
-  // before the first division so the latencies overlap, and 4x fewer blocks
-  // (and shift atomics).  Each element is read and written by the same thread
-  // only, so out may alias prev.
-  constexpr int RW = NORM_RW, NR = 2;
-  const int64_t row0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * RW;
-  const int lane = threadIdx.x & 31;
-  int64_t cnt[RW];
-  double sh[RW];
-  float nrm[RW];
+  // TAIL: blocks [0, norm_blocks) normalize, the others sum objective
+  // partials, concurrently (one block doing both would serialize them)
+  if (!TAIL || blockIdx.x < ta.norm_blocks) {
+    __shared__ double wmax[8];
+    // NORM_RW rows per warp, every load of a pass (64 columns of each row) issued
+    // before the first division so the latencies overlap, and 4x fewer blocks
+    // (and shift atomics).  Each element is read and written by the same thread
+    // only, so out may alias prev.
+    constexpr int RW = NORM_RW, NR = 2;
+    const int64_t row0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * RW;
+    const int lane = threadIdx.x & 31;
+    int64_t cnt[RW];
+    double sh[RW];
+    float nrm[RW];
 #pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    cnt[q] = row0 + q < BK ? counts[row0 + q] : 0;
-    sh[q] = 0.0;
-    nrm[q] = 0.f;
-  }
-  for (int64_t j0 = 0; j0 < d; j0 += 32 * NR) {
-    double sv[RW][NR];
-    TM pv[RW][NR];
+    for (int q = 0; q < RW; ++q) {
+      cnt[q] = row0 + q < BK ? counts[row0 + q] : 0;
+      sh[q] = 0.0;
+      nrm[q] = 0.f;
+    }
+    for (int64_t j0 = 0; j0 < d; j0 += 32 * NR) {
+      double sv[RW][NR];
+      TM pv[RW][NR];
 #pragma unroll
-    for (int q = 0; q < RW; ++q)
+      for (int q = 0; q < RW; ++q)
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const int64_t j = j0 + lane + 32 * r;
-        if (row0 + q < BK && j < d) {
-          sv[q][r] = sums[(row0 + q) * d + j];
-          pv[q][r] = prev[(row0 + q) * d + j];
-        }
-      }
-#pragma unroll
-    for (int q = 0; q < RW; ++q)
-#pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const int64_t j = j0 + lane + 32 * r;
-        if (row0 + q < BK && j < d) {
-          const int64_t o = (row0 + q) * d + j;
-          TM nv = pv[q][r];
-          if (cnt[q] > 0) nv = (TM)(sv[q][r] / (double)cnt[q]);  // correctly rounded, as numpy
-          out[o] = nv;
-          if (operand) {
-            const TO ov = (TO)(float)nv;
-            operand[o] = ov;
-            const float f = op_to_f32(ov);
-            nrm[q] = fmaf(f, f, nrm[q]);
+        for (int r = 0; r < NR; ++r) {
+          const int64_t j = j0 + lane + 32 * r;
+          if (row0 + q < BK && j < d) {
+            sv[q][r] = sums[(row0 + q) * d + j];
+            pv[q][r] = prev[(row0 + q) * d + j];
           }
-          const double df = (double)nv - (double)pv[q][r];
-          sh[q] += df * df;
+        }
+#pragma unroll
+      for (int q = 0; q < RW; ++q)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const int64_t j = j0 + lane + 32 * r;
+          if (row0 + q < BK && j < d) {
+            const int64_t o = (row0 + q) * d + j;
+            TM nv = pv[q][r];
+            if (cnt[q] > 0) nv = (TM)(sv[q][r] / (double)cnt[q]);  // correctly rounded, as numpy
+            out[o] = nv;
+            if (operand) {
+              const TO ov = (TO)(float)nv;
+              operand[o] = ov;
+              const float f = op_to_f32(ov);
+              nrm[q] = fmaf(f, f, nrm[q]);
+            }
+            const double df = (double)nv - (double)pv[q][r];
+            sh[q] += df * df;
+          }
+        }
+    }
+    if (lane == 0 && empty) {
+#pragma unroll
+      for (int q = 0; q < RW; ++q)
+        if (row0 + q < BK) empty[row0 + q] = cnt[q] > 0 ? 0 : 1;
+    }
+    if (bias) {
+#pragma unroll
+      for (int q = 0; q < RW; ++q) {
+        float acc = nrm[q];
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (row0 + q < BK && lane < 16) {
+          const int64_t b = (row0 + q) / K, k = row0 + q - b * K;
+          const float v = 0.5f * acc;
+          const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+          const float r1 = v - __bfloat162float(hi);
+          const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+          const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+          bias[(b * kpad + k) * 16 + lane] =
+              lane == 0 ? hi : lane == 1 ? mid : lane == 2 ? lo : __float2bfloat16(0.f);
         }
       }
-  }
-  if (lane == 0 && empty) {
+    }
+    if (max_shift2) {
+      double m = 0.0;
 #pragma unroll
-    for (int q = 0; q < RW; ++q)
-      if (row0 + q < BK) empty[row0 + q] = cnt[q] > 0 ? 0 : 1;
-  }
-  if (bias) {
-#pragma unroll
-    for (int q = 0; q < RW; ++q) {
-      float acc = nrm[q];
-      for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (row0 + q < BK && lane < 16) {
-        const int64_t b = (row0 + q) / K, k = row0 + q - b * K;
-        const float v = 0.5f * acc;
-        const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-        const float r1 = v - __bfloat162float(hi);
-        const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-        const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-        bias[(b * kpad + k) * 16 + lane] =
-            lane == 0 ? hi : lane == 1 ? mid : lane == 2 ? lo : __float2bfloat16(0.f);
+      for (int q = 0; q < RW; ++q) {
+        double v = sh[q];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        m = fmax(m, v);
       }
-    }
-  }
-  if (max_shift2) {
-    double m = 0.0;
-#pragma unroll
-    for (int q = 0; q < RW; ++q) {
-      double v = sh[q];
-      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      m = fmax(m, v);
-    }
-    if (lane == 0) wmax[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double mb = 0.0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mb = fmax(mb, wmax[w]);
-      // non-negative doubles order like their bit patterns
-      atomicMax((unsigned long long*)max_shift2, (unsigned long long)__double_as_longlong(mb));
+      if (lane == 0) wmax[threadIdx.x >> 5] = m;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double mb = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mb = fmax(mb, wmax[w]);
+        // non-negative doubles order like their bit patterns
+        atomicMax((unsigned long long*)max_shift2, (unsigned long long)__double_as_longlong(mb));
+      }
     }
   }
   if constexpr (TAIL) {
-    __shared__ double red[256];
+    __shared__ NpScratch nps;
     const int t = threadIdx.x;
-    for (int64_t ob = blockIdx.x; !ta.obj_ready && ob < ta.B * ta.nblk; ob += gridDim.x) {  // k_obj_partial
+    const int64_t nob_blocks = (int64_t)gridDim.x - ta.norm_blocks;
+    for (int64_t ob = (int64_t)blockIdx.x - ta.norm_blocks; !ta.obj_ready && ob >= 0 && ob < ta.B * ta.nblk;
+         ob += nob_blocks) {  // k_obj_partial
       const int64_t b = ob / ta.nblk, blk = ob - b * ta.nblk;
       const int64_t lo = blk * OBJ_BLOCK_N;
       const int64_t hi = (lo + OBJ_BLOCK_N < ta.N) ? lo + OBJ_BLOCK_N : ta.N;
-      double acc = 0.0;
-      if (ta.mind_f64) {
-        const double* m = reinterpret_cast<const double*>(ta.mind);
-        for (int64_t i = lo + t; i < hi; i += 256) acc += m[b * ta.N + i];
-      } else {
-        const float* m = reinterpret_cast<const float*>(ta.mind);
-        for (int64_t i = lo + t; i < hi; i += 256) acc += (double)m[b * ta.N + i];
-      }
-      __syncthreads();
-      red[t] = acc;
-      __syncthreads();
-      for (int s2 = 128; s2 > 0; s2 >>= 1) {
-        if (t < s2) red[t] += red[t + s2];
-        __syncthreads();
-      }
-      if (t == 0) ta.part[ob] = red[0];
+      const double v =
+          ta.mind_f64 ? np_pairwise_block(reinterpret_cast<const double*>(ta.mind) + b * ta.N + lo,
+                                          (int)(hi - lo), nps)
+                      : np_pairwise_block(reinterpret_cast<const float*>(ta.mind) + b * ta.N + lo,
+                                          (int)(hi - lo), nps);
+      if (t == 0) ta.part[ob] = v;
     }
     // the last block to arrive finishes the iteration
     __shared__ int s_last;
-    __threadfence();
+    __shared__ double tstage[TAIL_STAGE];
+    // what the last block reads from this one (the partials, by thread 0;
+    // the shift by atomics) is published by thread 0's fence alone: a fence in
+    // every thread would wait for all of the block's normalize stores
     __syncthreads();
-    if (t == 0) s_last = atomicAdd(ta.counter, 1u) == gridDim.x - 1;
+    if (t == 0) {
+      __threadfence();
+      s_last = atomicAdd(ta.counter, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
     if (s_last) {
       __threadfence();
-      const int lane2 = t & 31, w = t >> 5;
       const int64_t row = ta.hist ? __ldcg(ta.hist_it) : 0;
-      for (int64_t b = w; b < ta.B; b += 8) {  // k_loop_tail's tree, 8 warps
+      // every partial fetched in one round into shared memory when they fit
+      // (B * nblk <= TAIL_STAGE: 64 batch elements of 128K points), instead of
+      // one dependent L2 round trip per batch element a warp walks
+      const int64_t np = ta.obj_ready ? 0 : ta.B * ta.nblk;
+      const bool staged = np <= TAIL_STAGE;
+      if (staged) {
+        for (int64_t i = t; i < np; i += 256) tstage[i] = __ldcg(ta.part + i);
+        __syncthreads();
+      }
+      for (int64_t b = t; b < ta.B; b += 256) {  // one thread per batch element
+        double x;
         if (ta.obj_ready) {
-          if (lane2 == 0 && ta.hist) ta.hist[row * ta.B + b] = __ldcg(ta.obj + b);
-          continue;
-        }
-        double v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          double acc = 0.0;
-          for (int64_t i = lane2 + 32 * j; i < ta.nblk; i += 256) acc += __ldcg(ta.part + b * ta.nblk + i);
-          v[j] = acc;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] += v[j + 4];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) v[j] += v[j + 2];
-        v[0] += v[1];
-        double x = v[0];
-        for (int s2 = 16; s2; s2 >>= 1) x += __shfl_down_sync(0xffffffffu, x, s2);
-        if (lane2 == 0) {
+          x = __ldcg(ta.obj + b);
+        } else {
+          x = staged ? obj_fold(tstage + b * ta.nblk, ta.nblk) : 0.0;
+          if (!staged)
+            for (int64_t i = 0; i < ta.nblk; ++i) x = __dadd_rn(x, __ldcg(ta.part + b * ta.nblk + i));
           ta.obj[b] = x;
-          if (ta.hist) ta.hist[row * ta.B + b] = x;
         }
+        if (ta.hist) ta.hist[row * ta.B + b] = x;
       }
       __syncthreads();
       if (t == 0) {
@@ -1809,10 +1819,14 @@ template <typename TM>
 static cudaError_t norm_tail_dispatch(int operand_dt, const double* sums, const int64_t* counts,
                                       const void* prev, void* out, void* operand_out, uint8_t* empty,
                                       double* ms2, int64_t BK, int64_t d, void* bias, int64_t K,
-                                      int64_t kpad, const TailArgs& ta, cudaStream_t s) {
+                                      int64_t kpad, const TailArgs& ta_in, cudaStream_t s) {
   const int th = 256;
   const int64_t rows_per_block = (th / 32) * NORM_RW;
-  const unsigned grid = (unsigned)((BK + rows_per_block - 1) / rows_per_block);
+  TailArgs ta = ta_in;
+  ta.norm_blocks = (BK + rows_per_block - 1) / rows_per_block;
+  // + one block per objective partial (up to 1024; they loop beyond)
+  const int64_t nob = ta.obj_ready ? 0 : (ta.B * ta.nblk < 1024 ? ta.B * ta.nblk : 1024);
+  const unsigned grid = (unsigned)(ta.norm_blocks + nob);
   const TM* pv = (const TM*)prev;
   TM* ov = (TM*)out;
   __nv_bfloat16* bz = (__nv_bfloat16*)bias;
@@ -1842,7 +1856,33 @@ cudaError_t launch_normalize_tail(int master_dt, const double* sums, const int64
                                   const void* mind, int64_t N, double* part, double* obj,
                                   double* hist, int64_t* hist_it, int32_t* changed,
                                   int64_t* merges, double* flags, unsigned int* counter,
-                                  cudaStream_t s) {
+                                  int num_sms, cudaStream_t s) {
+  // Many centroid rows AND many objective blocks (config 4: 512 + 512 blocks
+  // at 2 resident per SM): the objective blocks would hold normalize-sized
+  // register slots for 1.7 more waves -- three launches instead (normalize,
+  // partials, loop tail: 13.4 vs 20.7 us at config 4, graph-replayed; the one
+  // launch wins where the rows are few, config 2: 10.5 vs 13.6 us).
+  // FK_TAIL=fused|split overrides (A/B).
+  static int tail_env = -2;
+  if (tail_env == -2) {
+    const char* e = getenv("FK_TAIL");
+    tail_env = !e ? -1 : (e[0] == 'f' ? 1 : e[0] == 's' ? 0 : -1);
+  }
+  if (!mind_f64) {
+    const int64_t norm_blocks = (B * K + 8 * NORM_RW - 1) / (8 * NORM_RW);
+    const int64_t nblk = (N + OBJ_BLOCK_N - 1) / OBJ_BLOCK_N;
+    const int64_t nob = B * nblk < 1024 ? B * nblk : 1024;
+    const bool split = tail_env >= 0 ? tail_env == 0
+                                     : (norm_blocks + nob > 2 * (int64_t)num_sms && 2 * norm_blocks > num_sms);
+    if (split) {
+      cudaError_t e = launch_normalize(master_dt, sums, counts, prev, out, operand_dt, operand_out, empty_mask,
+                                       max_shift2, B, K, d, bias_out, bias_kpad, s);
+      if (e == cudaSuccess) e = launch_objective_partials(0, mind, B, N, part, s);
+      if (e == cudaSuccess)
+        e = launch_loop_tail(part, B, N, obj, hist, hist_it, changed, max_shift2, merges, flags, s);
+      return e;
+    }
+  }
   TailArgs ta;
   ta.mind = mind;
   ta.mind_f64 = mind_f64;
@@ -1887,74 +1927,55 @@ cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* c
 constexpr int OBJ_BLOCK = OBJ_BLOCK_N;
 
 template <typename T>
-__global__ void k_obj_partial(const T* __restrict__ m, int64_t B, int64_t N, int64_t nblk,
-                              double* part) {
-  __shared__ double red[256];
+__global__ void __launch_bounds__(256) k_obj_partial(const T* __restrict__ m, int64_t B, int64_t N,
+                                                     int64_t nblk, double* part) {
+  __shared__ NpScratch nps;
   const int64_t b = blockIdx.y, blk = blockIdx.x;
   const int64_t lo = blk * OBJ_BLOCK;
   const int64_t hi = (lo + OBJ_BLOCK < N) ? lo + OBJ_BLOCK : N;
-  double acc = 0.0;
-  for (int64_t i = lo + threadIdx.x; i < hi; i += 256) acc += (double)m[b * N + i];
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) part[b * nblk + blk] = red[0];
+  const double v = np_pairwise_block(m + b * N + lo, (int)(hi - lo), nps);
+  if (threadIdx.x == 0) part[b * nblk + blk] = v;
 }
 
-__global__ void k_obj_final(const double* part, int64_t B, int64_t nblk, double* out) {
-  __shared__ double red[256];
-  const int64_t b = blockIdx.x;
-  double acc = 0.0;
-  for (int64_t i = threadIdx.x; i < nblk; i += 256) acc += part[b * nblk + i];
-  red[threadIdx.x] = acc;
+// The buffer partials of every batch element folded in order (one thread per
+// batch element, the partials staged in shared memory when they fit).
+FK_DEV double obj_fold_staged(const double* __restrict__ part, int64_t b, int64_t nblk, double* stage,
+                              bool staged) {
+  return staged ? obj_fold(stage + b * nblk, nblk) : obj_fold(part + b * nblk, nblk);
+}
+
+__global__ void __launch_bounds__(256) k_obj_final(const double* part, int64_t B, int64_t nblk,
+                                                   double* out) {
+  __shared__ double stage[TAIL_STAGE];
+  const bool staged = B * nblk <= TAIL_STAGE;
+  if (staged)
+    for (int64_t i = threadIdx.x; i < B * nblk; i += blockDim.x) stage[i] = part[i];
   __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[b] = red[0];
+  for (int64_t b = threadIdx.x; b < B; b += blockDim.x) out[b] = obj_fold_staged(part, b, nblk, stage, staged);
 }
 
 // End of one device-resident Lloyd iteration, one launch (LloydEngine): the
-// objective partials reduced in k_obj_final's fixed order into obj[b] and the
-// history row hist[(*it) * B + b] (*it advanced: the row index lives on the
-// device, so a replayed CUDA graph writes successive rows); flags = [changed,
-// max shift^2, merges] for the one host read; the three accumulators cleared
-// for the next iteration.
-__global__ void __launch_bounds__(1024)
+// objective partials folded in numpy's order into obj[b] and the history row
+// hist[(*it) * B + b] (*it advanced: the row index lives on the device, so a
+// replayed CUDA graph writes successive rows); flags = [changed, max shift^2,
+// merges] for the one host read; the three accumulators cleared for the next
+// iteration.
+__global__ void __launch_bounds__(256)
     k_loop_tail(const double* __restrict__ part, int64_t B, int64_t nblk, double* __restrict__ obj,
                 double* __restrict__ hist, int64_t* __restrict__ hist_it, int32_t* changed,
                 double* shift2, int64_t* merges, double* __restrict__ flags) {
-  // warp w reduces batch elements b = w, w + 32, ...: k_obj_final's 256-slot
-  // tree (slot t sums part[t], part[t+256], ... in order; then pairs t, t+s
-  // for s = 128 .. 1), lane l holding slots l + 32j -- the same additions, so
-  // the same double
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __shared__ double stage[TAIL_STAGE];
+  const bool staged = B * nblk <= TAIL_STAGE;
+  if (staged)
+    for (int64_t i = threadIdx.x; i < B * nblk; i += blockDim.x) stage[i] = part[i];
+  __syncthreads();
   const int64_t row = hist ? *hist_it : 0;
-  for (int64_t b = w; b < B; b += 32) {
-    double v[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      double acc = 0.0;
-      for (int64_t i = lane + 32 * j; i < nblk; i += 256) acc += part[b * nblk + i];
-      v[j] = acc;
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) v[j] += v[j + 4];  // s = 128
-#pragma unroll
-    for (int j = 0; j < 2; ++j) v[j] += v[j + 2];  // s = 64
-    v[0] += v[1];                                  // s = 32
-    double x = v[0];
-    for (int s = 16; s; s >>= 1) x += __shfl_down_sync(0xffffffffu, x, s);
-    if (lane == 0) {
-      obj[b] = x;
-      if (hist) hist[row * B + b] = x;
-    }
+  for (int64_t b = threadIdx.x; b < B; b += blockDim.x) {
+    const double x = obj_fold_staged(part, b, nblk, stage, staged);
+    obj[b] = x;
+    if (hist) hist[row * B + b] = x;
   }
-  __syncthreads();  // every warp read *hist_it before it moves
+  __syncthreads();  // every thread read *hist_it before it moves
   if (threadIdx.x == 0) {
     if (hist) *hist_it = row + 1;
     flags[0] = (double)*changed;
@@ -1981,7 +2002,7 @@ cudaError_t launch_loop_tail(const double* part, int64_t B, int64_t N, double* o
                              int64_t* hist_it, int32_t* changed, double* shift2, int64_t* merges,
                              double* flags, cudaStream_t s) {
   const int64_t nblk = (N + OBJ_BLOCK - 1) / OBJ_BLOCK;
-  k_loop_tail<<<1, 1024, 0, s>>>(part, B, nblk, obj, hist, hist_it, changed, shift2, merges, flags);
+  k_loop_tail<<<1, 256, 0, s>>>(part, B, nblk, obj, hist, hist_it, changed, shift2, merges, flags);
   return cudaGetLastError();
 }
 
@@ -2006,7 +2027,7 @@ cudaError_t launch_objective(int mind_is_f64, const void* mind, int64_t B, int64
     k_obj_partial<double><<<grid, 256, 0, s>>>((const double*)mind, B, N, nblk, part);
   else
     k_obj_partial<float><<<grid, 256, 0, s>>>((const float*)mind, B, N, nblk, part);
-  k_obj_final<<<(unsigned)B, 256, 0, s>>>(part, B, nblk, out);
+  k_obj_final<<<1, 256, 0, s>>>(part, B, nblk, out);
   return cudaGetLastError();
 }
 

@@ -310,7 +310,7 @@ def objective(mind: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tens
     return out
 
 
-OBJ_BLOCK = 8192  # elements per objective partial (fk_objective_partials)
+OBJ_BLOCK = 8192  # elements per objective partial: numpy's reduction buffer (fk_objective_partials)
 
 
 def objective_partials(mind: torch.Tensor, out: torch.Tensor) -> torch.Tensor:

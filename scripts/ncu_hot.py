@@ -1,5 +1,5 @@
 """Hot SASS instructions (stall samples) and the top stall reasons of one ncu report.
-usage: python scripts/ncu_hot.py report.ncu-rep [top]"""
+usage: python scripts/ncu_hot.py report.ncu-rep [top] [kernel-regex]"""
 import csv
 import io
 import subprocess
@@ -7,7 +7,8 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+kf = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+raw = subprocess.run(["ncu", "-i", rep, *kf, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(io.StringIO(raw)))
 h, v = r[0], r[2]
 keys = ["gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
@@ -20,7 +21,7 @@ st = [(float(v[i]), h[i]) for i in range(len(h))
       if "average_warps_issue_stalled" in h[i] and h[i].endswith("per_issue_active.ratio") and v[i]]
 for x in sorted(st, reverse=True)[:8]:
     print(f"  stall {x[1].split('stalled_')[1].split('_per')[0]:24s} {x[0]:.2f}")
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+src = subprocess.run(["ncu", "-i", rep, *kf, "--page", "source", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hh = rows[1]
 i = hh.index("Warp Stall Sampling (All Samples)")

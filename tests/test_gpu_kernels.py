@@ -202,11 +202,65 @@ def test_changed_flag(ops):
     assert int(flag.item()) == 1
 
 
-def test_objective(ops):
-    m = torch.rand((3, 100000), dtype=torch.float32)
-    o = ops.objective(m.cuda())
-    ref = np.array([np.sum(m[b].numpy(), dtype=np.float64) for b in range(3)])
-    np.testing.assert_allclose(o.cpu().numpy(), ref, rtol=1e-12)
+@pytest.mark.parametrize("N", [1, 7, 8, 129, 1000, 8191, 8192, 8193, 20000, 100000, 1 << 20])
+def test_objective_f32_is_numpys_order(ops, N):
+    """pipeline._objective_row on f32 min_dists: np.sum(m, dtype=float64) casts
+    through numpy's 8192-element buffer and adds each buffer's pairwise sum in
+    order -- reproduced addition for addition, on data whose f64 sums are NOT
+    exact (magnitudes over many binades), through both the standalone objective
+    and the engine's end-of-iteration launch (fused tail or the split path)."""
+    rng = np.random.default_rng(N)
+    m = (rng.random((3, N)) * np.exp(rng.uniform(-18, 10, (3, N)))).astype(np.float32)
+    ref = np.array([np.sum(m[b], dtype=np.float64) for b in range(3)])
+    out = ops.objective(torch.from_numpy(m).cuda()).cpu().numpy()
+    assert np.array_equal(out.view(np.uint64), ref.view(np.uint64))
+    part = torch.empty((3 * -(-N // ops.OBJ_BLOCK),), dtype=torch.float64, device="cuda")
+    ops.objective_partials(torch.from_numpy(m).cuda(), part)
+    for b in range(3):
+        acc = 0.0
+        for v in part.view(3, -1)[b].cpu().numpy():
+            acc = acc + v
+        assert np.float64(acc).view(np.uint64) == ref[b].view(np.uint64)
+
+
+@pytest.mark.parametrize("B,N,K", [(64, 16384, 256), (1, 100000, 1024), (3, 20000, 24)])
+@pytest.mark.parametrize("tail", ["fused", "split"])
+def test_loop_tail_objective_is_numpys_order(B, N, K, tail):
+    """The engine's end-of-iteration launch(es) write numpy's objective too, for
+    both forms (FK_TAIL=fused|split; run in a child so the switch is read fresh)."""
+    import subprocess
+    import sys
+
+    code = f"""
+import numpy as np, torch, sys
+sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})
+from paper_2603_09229_b200 import ops
+B, N, K, d = {B}, {N}, {K}, 8
+rng = np.random.default_rng(5)
+m = torch.from_numpy((rng.random((B, N)) * np.exp(rng.uniform(-18, 10, (B, N)))).astype(np.float32)).cuda()
+sums = torch.zeros((B, K, d), dtype=torch.float64, device="cuda")
+counts = torch.ones((B, K), dtype=torch.int64, device="cuda")
+prev = torch.zeros((B, K, d), dtype=torch.float32, device="cuda")
+out = torch.empty_like(prev)
+empty = torch.empty((B, K), dtype=torch.uint8, device="cuda")
+shift2 = torch.zeros((), dtype=torch.float64, device="cuda")
+nb = max(int(ops.N.lib().fk_objective_workspace(B, N)), B * -(-N // ops.OBJ_BLOCK) * 8)
+part = torch.empty((-(-nb // 8),), dtype=torch.float64, device="cuda")
+obj = torch.empty((B,), dtype=torch.float64, device="cuda")
+changed = torch.zeros((), dtype=torch.int32, device="cuda")
+merges = torch.zeros((), dtype=torch.int64, device="cuda")
+flags = torch.zeros(3, dtype=torch.float64, device="cuda")
+ctr = torch.zeros((1,), dtype=torch.int32, device="cuda")
+for _ in range(2):
+    ops.normalize_loop_tail(sums, counts, prev, out, None, empty, shift2, None, m, part, obj, changed, merges,
+                            flags, ctr)
+ref = np.array([np.sum(m[b].cpu().numpy(), dtype=np.float64) for b in range(B)])
+assert np.array_equal(obj.cpu().numpy().view(np.uint64), ref.view(np.uint64)), (obj.cpu().numpy() - ref)
+print("ok")
+"""
+    env = dict(__import__("os").environ, FK_TAIL=tail)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
 # ----------------------------------------------------------- stable sort / determinism

@@ -6,11 +6,13 @@ a world-1 NCCL group exercises the NCCL all-reduce itself.  What runs is the
 product path: fk_assign / fk_update / fk_stats_pack / fk_merges_from_counts /
 fk_normalize inside LloydEngine.exchange and the sharded streaming pass.
 
-Parity bar: float32 data -- every partial sum is exact in
-f64 -- gives the single-process run bit for bit (centroids, assignments,
-objective history, iteration count, merge counter); bf16 gives bit-exact
-counts and centroids within 1e-3 (row-norm relative) of the single-process
-iteration.
+Parity bar: float32 data gives the single-process run bit
+for bit (centroids, assignments, iteration count, merge counter; the streamed
+runs' objective history too, each chunk's objective having one contributor);
+the in-core sharded objective is the all-reduce of per-shard sums in numpy's
+order, equal to the single-process value up to a few ulps when those f64 sums
+are inexact.  bf16 gives bit-exact counts and centroids within 1e-3
+(row-norm relative) of the single-process iteration.
 """
 
 import os
@@ -57,7 +59,10 @@ def test_sharded_lloyd_f32_bitwise(backend, world):
     for c, _, hist, iters, merges in res:
         assert iters == ref.iterations_run
         assert np.array_equal(c, ref.centroids.numpy())
-        np.testing.assert_array_equal(hist, ref.objective_history)
+        # the objective is numpy's buffered pairwise order per shard, then the
+        # all-reduce of the shard sums: equal to the single-process (numpy)
+        # value only when the f64 sums are exact -- a few ulps otherwise
+        np.testing.assert_allclose(hist, ref.objective_history, rtol=1e-13, atol=0)
         assert merges == ref.counters.synchronized_merges
     assert np.array_equal(a, ref.assignments.numpy())
 
@@ -197,7 +202,7 @@ def test_sharded_lloyd_f32_split_path_bitwise(backend, world):
     for c, _, hist, iters, merges in res:
         assert iters == ref.iterations_run
         assert np.array_equal(c, ref.centroids.numpy())
-        np.testing.assert_array_equal(hist, ref.objective_history)
+        np.testing.assert_allclose(hist, ref.objective_history, rtol=1e-13, atol=0)  # see above
 
 
 def test_sharded_stream_run_f32_split_path_bitwise():
