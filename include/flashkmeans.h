@@ -170,6 +170,34 @@ FK_API fk_status fk_update(fk_dtype dt, const void* X, const int32_t* ids, int64
                     int64_t* counts, int64_t* merges_out, void* workspace, size_t workspace_bytes,
                     void* stream);
 
+/* The update's first pass folded into the assign (a Lloyd iteration's
+ * assign -> update pair on bf16/fp16 data; the counting step of
+ * counting_sort, _kernels.py:118-132, sort_inverse.py:67-78):
+ *   fk_update_hist_slots: where the block histogram table of an update
+ *     workspace lives -- hist_table (B * hist_bpb rows of K int32), hist_inval
+ *     (B * hist_bpb int32), the blocks per batch element and points per block,
+ *     and clear_words: the int32 words from hist_table on that must be zero
+ *     before the first fk_assign_hist (FK_EUNSUPPORTED for f32/f64 data or
+ *     K > 16384: use fk_update);
+ *   fk_assign_hist: fk_assign (bf16/fp16, tensor-core path) whose epilogue
+ *     also adds each row's id into that table (ids outside [0, K) into
+ *     hist_inval); the table must be zero on entry;
+ *   fk_update_prehist: fk_update without its histogram pass, reading the
+ *     table the assign built; it leaves the table zeroed again for the next
+ *     fk_assign_hist.  Results are bitwise those of fk_assign + fk_update.  */
+FK_API fk_status fk_update_hist_slots(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d,
+                                      void* workspace, int32_t** hist_table, int32_t** hist_inval,
+                                      int64_t* hist_bpb, int64_t* hist_per, int64_t* clear_words);
+FK_API fk_status fk_assign_hist(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B,
+                                int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
+                                const int32_t* idx_prev, int32_t* changed_flag, void* workspace,
+                                size_t workspace_bytes, int32_t* hist_table, int32_t* hist_inval,
+                                int64_t hist_bpb, int64_t hist_per, void* stream);
+FK_API fk_status fk_update_prehist(fk_dtype dt, const void* X, const int32_t* ids, int64_t B,
+                                   int64_t N, int64_t K, int64_t d, int64_t update_chunk,
+                                   int32_t accumulate, double* sums, int64_t* counts, int64_t* merges_out,
+                                   void* workspace, size_t workspace_bytes, void* stream);
+
 /* Stable argsort of the ids alone (argsort_assignments / counting_sort,
  * sort_inverse.py:67-78, _kernels.py:118-132): the order the update's segmented
  * reductions walk.  order_out (B*N int32): flat point indices b*N + i, grouped

@@ -58,6 +58,15 @@ def _declare(L):
     L.fk_update_workspace.argtypes = [ctypes.c_int, I64, I64, I64, I64]
     L.fk_update.restype = ctypes.c_int
     L.fk_update.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, I64, I32, P, P, P, P, SZ, P]
+    L.fk_update_prehist.restype = ctypes.c_int
+    L.fk_update_prehist.argtypes = [ctypes.c_int, P, P, I64, I64, I64, I64, I64, I32, P, P, P, P, SZ, P]
+    L.fk_update_hist_slots.restype = ctypes.c_int
+    L.fk_update_hist_slots.argtypes = [ctypes.c_int, I64, I64, I64, I64, P, ctypes.POINTER(P),
+                                       ctypes.POINTER(P), ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                       ctypes.POINTER(I64)]
+    L.fk_assign_hist.restype = ctypes.c_int
+    L.fk_assign_hist.argtypes = [ctypes.c_int, P, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P, P, I64,
+                                 I64, P]
     L.fk_argsort.restype = ctypes.c_int
     L.fk_argsort.argtypes = [P, I64, I64, I64, P, P, P, SZ, P]
     L.fk_normalize.restype = ctypes.c_int
@@ -103,7 +112,7 @@ EXPORTED = (
     "fk_assign_workspace", "fk_assign_bias_rows", "fk_assign_bias", "fk_assign", "fk_assign_xsplit_bytes",
     "fk_assign_xsplit", "fk_assign_split_workspace", "fk_assign_split", "fk_assign_split_fallback_rows",
     "fk_update_workspace",
-    "fk_update", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
+    "fk_update", "fk_update_prehist", "fk_update_hist_slots", "fk_assign_hist", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
     "fk_objective_partials", "fk_loop_tail", "fk_normalize_loop_tail", "fk_scatter",
     "fk_stats_pack", "fk_merges_from_counts", "fk_farthest_workspace", "fk_farthest",
     "fk_kmeanspp_workspace", "fk_kmeanspp",

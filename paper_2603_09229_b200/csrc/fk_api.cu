@@ -325,9 +325,36 @@ fk_status fk_assign_bias(fk_dtype dt, const void* C, int64_t B, int64_t K, int64
                                        reinterpret_cast<cudaStream_t>(stream)));
 }
 
+static fk_status assign_impl(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B,
+                             int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
+                             const int32_t* idx_prev, int32_t* changed_flag, void* ws, size_t ws_bytes,
+                             void* stream, int32_t* hist_table, int32_t* hist_inval, int64_t hist_bpb,
+                             int64_t hist_per);
+
 fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B, int64_t N,
                     int64_t K, int64_t d, int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
                     int32_t* changed_flag, void* ws, size_t ws_bytes, void* stream) {
+  return assign_impl(dt, X, C, bias, B, N, K, d, idx_out, mind_out, idx_prev, changed_flag, ws, ws_bytes,
+                     stream, nullptr, nullptr, 1, 1);
+}
+
+fk_status fk_assign_hist(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B,
+                         int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
+                         const int32_t* idx_prev, int32_t* changed_flag, void* ws, size_t ws_bytes,
+                         int32_t* hist_table, int32_t* hist_inval, int64_t hist_bpb, int64_t hist_per,
+                         void* stream) {
+  if (!hist_table || !hist_inval || hist_bpb < 1 || hist_per < 1 || hist_bpb * hist_per < N)
+    return FK_EINVAL;
+  if (!is_lowp(dt) || !tc_path(dt, d, X, C)) return FK_EUNSUPPORTED;
+  return assign_impl(dt, X, C, bias, B, N, K, d, idx_out, mind_out, idx_prev, changed_flag, ws, ws_bytes,
+                     stream, hist_table, hist_inval, hist_bpb, hist_per);
+}
+
+static fk_status assign_impl(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B,
+                             int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
+                             const int32_t* idx_prev, int32_t* changed_flag, void* ws, size_t ws_bytes,
+                             void* stream, int32_t* hist_table, int32_t* hist_inval, int64_t hist_bpb,
+                             int64_t hist_per) {
   if (!valid_dt(dt) || !shape_ok(B, N, K, d)) return FK_EINVAL;
   if (!X || !C || !idx_out || !mind_out) return FK_EINVAL;
   if (idx_prev && !changed_flag) return FK_EINVAL;
@@ -356,7 +383,8 @@ fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void* bias,
       if (st != FK_OK) return st;
       return cuda_status(fk::launch_assign_tc(fmt, X, C, cn, ext, B, N, K, d, idx_out,
                                               reinterpret_cast<float*>(mind_out), idx_prev,
-                                              changed_flag, di.sms, s));
+                                              changed_flag, di.sms, s, hist_table, hist_inval, hist_bpb,
+                                              hist_per));
     }
     fk_status st = cuda_status(fk::launch_cn_pad(dt, C, B, K, d, (int)K, cn, s));
     if (st != FK_OK) return st;
@@ -400,6 +428,34 @@ fk_status fk_update(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, i
   return cuda_status(fk::launch_update(dt, X, ids, B, N, K, d, update_chunk, accumulate, sums,
                                        counts, merges_out, ws, dev_info().sms,
                                        reinterpret_cast<cudaStream_t>(stream)));
+}
+
+fk_status fk_update_hist_slots(fk_dtype dt, int64_t B, int64_t N, int64_t K, int64_t d, void* ws,
+                               int32_t** hist_table, int32_t** hist_inval, int64_t* hist_bpb,
+                               int64_t* hist_per, int64_t* clear_words) {
+  if (!valid_dt(dt) || !shape_ok(B, N, K, d) || !ws || !hist_table || !hist_inval || !hist_bpb ||
+      !hist_per || !clear_words)
+    return FK_EINVAL;
+  if (!is_lowp(dt)) return FK_EUNSUPPORTED;
+  return fk::update_hist_slots(dt, B, N, K, d, dev_info().sms, ws, hist_table, hist_inval, hist_bpb,
+                               hist_per, clear_words)
+             ? FK_OK
+             : FK_EUNSUPPORTED;
+}
+
+fk_status fk_update_prehist(fk_dtype dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
+                            int64_t K, int64_t d, int64_t update_chunk, int32_t accumulate, double* sums,
+                            int64_t* counts, int64_t* merges_out, void* ws, size_t ws_bytes,
+                            void* stream) {
+  if (!valid_dt(dt) || !shape_ok(B, N, K, d)) return FK_EINVAL;
+  if (!X || !ids || !sums || !counts || update_chunk < 1) return FK_EINVAL;
+  if (!is_lowp(dt)) return FK_EUNSUPPORTED;
+  const size_t need = fk_update_workspace(dt, B, N, K, d);
+  if (!ws || ws_bytes < need) return FK_EWORKSPACE;
+  if (dev_info().major != 10) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_update(dt, X, ids, B, N, K, d, update_chunk, accumulate, sums, counts,
+                                       merges_out, ws, dev_info().sms,
+                                       reinterpret_cast<cudaStream_t>(stream), 1));
 }
 
 fk_status fk_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, int32_t* order_out,

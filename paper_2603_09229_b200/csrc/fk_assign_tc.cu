@@ -83,6 +83,13 @@ struct TcArgs {
   int32_t* cand_rec;         // records [row, n, chunk bases...], FK_SPLIT_REC ints each
   int32_t* cand_cnt;         // record count (device)
   int cand_cap;
+  // the update's block histograms, folded into the epilogue (fk_assign_hist):
+  // row i of batch element b adds 1 to hist_tab[(b * hist_bpb + i / hist_per) * K + id]
+  // (an id outside [0, K) to hist_inval[b * hist_bpb + i / hist_per]) -- the
+  // table k_hist would have built; nullptr: off
+  int32_t* hist_tab;
+  int32_t* hist_inval;
+  int hist_bpb, hist_per;
 };
 
 constexpr int SPLIT_NREC = 4;                  // near chunks kept per thread (per column half)
@@ -1061,6 +1068,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           } else {
             p.mind_out[o] = fmaxf(0.f, NEG ? fmaf(2.f, M, xn) : xn + M);
             if (p.idx_prev) ch = prev_id != idx;
+            if (p.hist_tab) {  // fire-and-forget reductions (RED), integer: order-free
+              const int64_t r = (int64_t)b * p.hist_bpb + grow / p.hist_per;
+              if (idx >= 0 && idx < p.K)
+                atomicAdd(p.hist_tab + r * p.K + idx, 1);
+              else
+                atomicAdd(p.hist_inval + r, 1);
+            }
           }
         }
         if (p.changed && __any_sync(0xffffffffu, ch) && lane == 0) atomicOr(p.changed, 1);
@@ -1194,8 +1208,13 @@ bool assign_tc_uses_ext(int fmt) { return assign_tc_bias_mode(fmt) == 1; }
 cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
                              const void* cn_ext, int64_t B, int64_t N, int64_t K, int64_t d,
                              int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
-                             int32_t* changed, int num_sms, cudaStream_t stream) {
+                             int32_t* changed, int num_sms, cudaStream_t stream, int32_t* hist_tab,
+                             int32_t* hist_inval, int64_t hist_bpb, int64_t hist_per) {
   TcArgs a;
+  a.hist_tab = hist_tab;
+  a.hist_inval = hist_inval;
+  a.hist_bpb = (int)hist_bpb;
+  a.hist_per = (int)(hist_per < 1 ? 1 : hist_per);
   a.B = (int)B;
   a.N = (int)N;
   a.K = (int)K;
@@ -1265,6 +1284,7 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     }
     return e;
   }
+  if (hist_tab) return cudaErrorInvalidValue;  // the single-CTA A/B kernel has no histogram fold
   CUtensorMap tmx, tmc;
   if (!make_map(&tmx, X, fmt, d, N, B, tc::BM)) return cudaErrorInvalidValue;
   if (!make_map(&tmc, C, fmt, d, K, B, tc::BN)) return cudaErrorInvalidValue;
@@ -1294,6 +1314,10 @@ cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* e
   if (ns < 1 || 2 * ns > 4 * tc2::KATOMS_MAX) return cudaErrorInvalidValue;
   const int64_t W = 32 * (int64_t)ns;
   TcArgs a;
+  a.hist_tab = nullptr;
+  a.hist_inval = nullptr;
+  a.hist_bpb = 1;
+  a.hist_per = 1;
   a.B = (int)B;
   a.N = (int)N;
   a.K = (int)K;

@@ -16,7 +16,9 @@ int assign_tc_bias_mode(int fmt);  // 0 epilogue, 1 bias-in-GEMM, 2 TMEM seed
 cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float* cn_pad,
                              const void* cn_ext, int64_t B, int64_t N, int64_t K, int64_t d,
                              int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
-                             int32_t* changed, int num_sms, cudaStream_t stream);
+                             int32_t* changed, int num_sms, cudaStream_t stream,
+                             int32_t* hist_tab = nullptr, int32_t* hist_inval = nullptr,
+                             int64_t hist_bpb = 1, int64_t hist_per = 1);
 
 constexpr int kSplitRecInts = 10;  // fk_assign_tc.cu FK_SPLIT_REC: [row, n, up to 8 chunk bases]
 cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* ext, int64_t B,
@@ -80,7 +82,9 @@ size_t update_workspace_bytes(int dt, int64_t B, int64_t N, int64_t K, int64_t d
 cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
                           int64_t K, int64_t d, int64_t chunk, int accumulate, double* sums,
                           int64_t* counts, int64_t* merges, void* ws, int num_sms,
-                          cudaStream_t stream);
+                          cudaStream_t stream, int prehist = 0);
+bool update_hist_slots(int dt, int64_t B, int64_t N, int64_t K, int64_t d, int num_sms, void* ws,
+                       int32_t** table, int32_t** inval, int64_t* bpb, int64_t* per, int64_t* words);
 cudaError_t launch_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, int32_t* order_out,
                            int64_t* off_out, void* ws, int num_sms, cudaStream_t stream);
 cudaError_t launch_normalize(int master_dt, const double* sums, const int64_t* counts,

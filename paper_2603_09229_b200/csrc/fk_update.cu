@@ -576,8 +576,25 @@ __global__ void __launch_bounds__(W * 32)
                    const int32_t* __restrict__ table, const int32_t* __restrict__ hist,
                    const int32_t* __restrict__ inval, int64_t B, int64_t chunk, int accumulate,
                    int64_t* __restrict__ off, int64_t* __restrict__ counts, int64_t* __restrict__ merges,
-                   int32_t* __restrict__ order, int rank_sort) {
+                   int32_t* __restrict__ order, int rank_sort, double* __restrict__ zero_sums,
+                   int64_t zero_n, int32_t* __restrict__ zero_arrive, int64_t arrive_n) {
   extern __shared__ __align__(16) uint8_t sw_sm[];
+  // block histograms folded into the assign (no k_hist): this pass clears the
+  // f64 sums and k_segsum's arrival counters instead
+  if (zero_sums || zero_arrive) {
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (zero_sums) {
+      if ((reinterpret_cast<uintptr_t>(zero_sums) & 15) == 0) {
+        double2* z2 = reinterpret_cast<double2*>(zero_sums);
+        for (int64_t i = t0; i < (zero_n >> 1); i += nt) z2[i] = make_double2(0.0, 0.0);
+        if ((zero_n & 1) && t0 == 0) zero_sums[zero_n - 1] = 0.0;
+      } else {
+        for (int64_t i = t0; i < zero_n; i += nt) zero_sums[i] = 0.0;
+      }
+    }
+    for (int64_t i = t0; i < arrive_n; i += nt) zero_arrive[i] = 0;
+  }
   // rows padded to K + 2 entries: the W rows of one key fall in different banks
   const int KS = (int)K + 2;
   uint16_t* tab = reinterpret_cast<uint16_t*>(sw_sm);                           // W * KS
@@ -838,7 +855,23 @@ struct SegMerge {
   double* part;     // [slices][2][d] f64 partials of segments spanning slices
   int32_t* arrive;  // [B*K] arrival counters (zeroed by k_hist)
   int64_t L, d;
+  int32_t* zero_i32;  // histogram folded into the assign: the block table + invalid
+  int64_t zero_n;     // counts, cleared here for the next assign (nullptr: none)
 };
+
+// k_segsum* run after the scatter, the last reader of the block table
+FK_DEV void seg_zero_table(const SegMerge& m) {
+  if (!m.zero_i32) return;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if ((reinterpret_cast<uintptr_t>(m.zero_i32) & 15) == 0) {
+    int4* z4 = reinterpret_cast<int4*>(m.zero_i32);
+    for (int64_t i = t0; i < (m.zero_n >> 2); i += nt) z4[i] = make_int4(0, 0, 0, 0);
+    for (int64_t i = (m.zero_n & ~int64_t(3)) + t0; i < m.zero_n; i += nt) m.zero_i32[i] = 0;
+  } else {
+    for (int64_t i = t0; i < m.zero_n; i += nt) m.zero_i32[i] = 0;
+  }
+}
 
 FK_DEV void seg_flush_boundary(const SegMerge& m, int64_t wg, int64_t p0, int64_t key, int64_t seg_lo,
                                int64_t seg_end, double* __restrict__ dst) {
@@ -872,6 +905,7 @@ __global__ void __launch_bounds__(256)
              const int64_t* __restrict__ off, int64_t BK, int64_t L, int64_t d,
              double* __restrict__ sums, const int32_t* __restrict__ ids, int64_t N, int64_t K,
              SegMerge mg) {
+  seg_zero_table(mg);
   constexpr int E = VecCvt<T>::E;
   constexpr int RPW = 32 / LPR;
   constexpr int NA = VPL * E;
@@ -982,11 +1016,134 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Segment-chained variant (default).  Same slices, same per-segment groups
+// and addition order as k_segsum, but the transitions between segments cost
+// no dependent loads: the segment ends come from a 32-key window of off[]
+// held one per lane (one refill per 32 keys), the indices of the NEXT group
+// -- this segment's next group or the next segment's first -- are prefetched
+// while the current group's rows are in flight (the old tail group and the
+// next segment's first group each waited for their indices, then for their
+// rows), and an owned segment of a non-accumulating update is stored without
+// reading the cleared sums back.  Positions are 32-bit (sorted points <
+// 2^31, as the scatter's flat offsets).
+template <typename T, typename A, int LPR, int VPL, int U>
+__global__ void __launch_bounds__(256, sizeof(A) == 8 ? 3 : 4)
+    k_segsum2(const T* __restrict__ X, const int32_t* __restrict__ order,
+              const int64_t* __restrict__ off, int64_t BK, int64_t L, int64_t d,
+              double* __restrict__ sums, const int32_t* __restrict__ ids, int64_t N, int64_t K,
+              SegMerge mg, int accumulate) {
+  seg_zero_table(mg);
+  constexpr int E = VecCvt<T>::E;
+  constexpr int RPW = 32 / LPR;
+  constexpr int NA = VPL * E;
+  constexpr int G = RPW * U;
+  const int lane = threadIdx.x & 31;
+  const int sub = lane / LPR, sl = lane % LPR;
+  const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int P = (int)off[BK];
+  if (wg * L >= P) return;
+  const int p0 = (int)(wg * L);
+  const int p1 = p0 + L < P ? p0 + (int)L : P;
+  const int32_t pt = order[p0];
+  const int pb = pt / (int)N;
+  int key = pb * (int)K + ids[pt];
+  int wb = key;  // window: lane i holds off[wb + 1 + i]
+  int win = wb + 1 + lane <= BK ? (int)off[wb + 1 + lane] : INT_MAX;
+  int seg_lo = (int)off[key];
+  int seg_end = __shfl_sync(0xffffffffu, win, 0);
+  auto end_of = [&](int k) -> int {
+    if (k - wb >= 32) {
+      wb = k;
+      win = wb + 1 + lane <= BK ? (int)off[wb + 1 + lane] : INT_MAX;
+    }
+    return __shfl_sync(0xffffffffu, win, k - wb);
+  };
+  A acc[NA];
+#pragma unroll
+  for (int e = 0; e < NA; ++e) acc[e] = (A)0;
+  int p = p0;
+  int lim = seg_end < p1 ? seg_end : p1;
+  int32_t ri[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int r = p + u * RPW + sub;
+    ri[u] = r < lim ? __ldg(order + r) : -1;
+  }
+  while (true) {
+    uint4 v[U][VPL];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const T* rp = X + (int64_t)(ri[u] < 0 ? 0 : ri[u]) * d;
+#pragma unroll
+      for (int q = 0; q < VPL; ++q)
+        v[u][q] = ri[u] >= 0 ? ldg_stream(rp + (q * LPR + sl) * E) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    const bool done = p + G >= lim;  // this group ends the segment's part of the slice
+    int nkey = key, nlo = seg_lo, nend = seg_end, nlim = lim, np = p + G;
+    if (done && lim < p1) {  // the next non-empty segment starts at lim
+      nlo = lim;
+      do nend = end_of(++nkey);
+      while (nend <= nlo);
+      nlim = nend < p1 ? nend : p1;
+      np = nlo;
+    }
+    if (!done || lim < p1) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int r = np + u * RPW + sub;
+        ri[u] = r < nlim ? __ldg(order + r) : -1;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int q = 0; q < VPL; ++q) VecCvt<T>::add(acc + q * E, v[u][q]);
+    if (done) {
+      // flush the segment's partial (one merge per segment; fixed shuffle tree)
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int e = 0; e < NA; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+      double* dst = sums + (int64_t)key * d;
+      if (seg_lo >= p0 && seg_end <= p1) {  // owned: the only writer of this key
+        if (sub == 0) {
+#pragma unroll
+          for (int q = 0; q < VPL; ++q)
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              double* o = dst + (int64_t)(q * LPR + sl) * E + e;
+              *o = __dadd_rn(accumulate ? *o : 0.0, (double)acc[q * E + e]);
+            }
+        }
+      } else {
+        double* pp = mg.part + (wg * 2 + (seg_lo <= p0 ? 0 : 1)) * d;
+        if (sub == 0) {
+#pragma unroll
+          for (int q = 0; q < VPL; ++q)
+#pragma unroll
+            for (int e = 0; e < E; ++e) pp[(int64_t)(q * LPR + sl) * E + e] = (double)acc[q * E + e];
+          __threadfence();
+        }
+        seg_flush_boundary(mg, wg, p0, key, seg_lo, seg_end, dst);
+      }
+#pragma unroll
+      for (int e = 0; e < NA; ++e) acc[e] = (A)0;
+      if (lim >= p1) break;
+      key = nkey;
+      seg_lo = nlo;
+      seg_end = nend;
+      lim = nlim;
+    }
+    p = np;
+  }
+}
+
 // Any row width: one warp per slice, lanes stride over the features.
 template <typename T>
 __global__ void k_segsum_generic(const T* __restrict__ X, const int32_t* __restrict__ order,
                                  const int64_t* __restrict__ off, int64_t BK, int64_t L, int64_t d,
                                  double* __restrict__ sums, SegMerge mg) {
+  seg_zero_table(mg);
   const int lane = threadIdx.x & 31;
   const int64_t wg = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t P = off[BK];
@@ -1060,14 +1217,30 @@ constexpr int kSegWarpsPerSm = 32;
 // profiles/r01_ab_segsum.txt: 64 -> 32 took config 2 from 67.8 to 64.1 us
 // and config 4 from 52 to 49.5 us, config 3 unchanged; 16 starves config 3
 // of bytes in flight), at least 64 points each.
-static int64_t segsum_slice(int64_t P, int num_sms) {
+static bool segsum_seq() {
+  static int seq_env = -1;  // FK_SEGSUM_SEQ=1: the per-segment k_segsum (A/B)
+  if (seq_env < 0) {
+    const char* e = getenv("FK_SEGSUM_SEQ");
+    seq_env = (e && e[0] == '1') ? 1 : 0;
+  }
+  return seq_env == 1;
+}
+// k_segsum2 for short segments only (<= 256 points per key on average:
+// config 4, 64 per key: update 59.0 -> 56.2 us); with long segments the
+// per-segment k_segsum's 8 row steps beat its 6 (config 2: 80.5 vs 86 us,
+// config 3: 464 vs 473 us; profiles/r02_ab_segsum2.txt)
+static bool segsum_chained(int64_t P, int64_t BK) { return !segsum_seq() && P <= 256 * BK; }
+// k_segsum2 with f64 accumulators (f32 / f64 data) holds 3 blocks per SM
+// (80 registers), the 2-byte types 4: one slice per resident warp
+static int64_t segsum_slice(int64_t P, int64_t BK, int num_sms, int dt) {
   static int wps = -1;  // FK_SEGSUM_WPS: warp slices per SM (A/B)
   if (wps < 0) {
     const char* e = getenv("FK_SEGSUM_WPS");
-    wps = e ? atoi(e) : kSegWarpsPerSm;
-    if (wps < 1 || wps > 64) wps = kSegWarpsPerSm;
+    wps = e ? atoi(e) : 0;
+    if (wps < 1 || wps > 64) wps = 0;
   }
-  const int64_t want = (int64_t)num_sms * wps;
+  const int w = wps ? wps : (segsum_chained(P, BK) && (dt == DT_F32 || dt == DT_F64)) ? 24 : kSegWarpsPerSm;
+  const int64_t want = (int64_t)num_sms * w;
   int64_t L = (P + want - 1) / want;
   return L < 64 ? 64 : L;
 }
@@ -1165,6 +1338,7 @@ struct UpdateWs {
   int32_t* arrive;
   double* part;
   int32_t* inval;
+  int64_t zero_n;  // int32 words from table through inval
 };
 
 static size_t update_ws_layout(int dt, int64_t B, int64_t N, int64_t K, int64_t d, int num_sms, void* base,
@@ -1172,15 +1346,16 @@ static size_t update_ws_layout(int dt, int64_t B, int64_t N, int64_t K, int64_t 
   auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
   const int64_t BK = B * K, P = B * N;
   const int64_t bpb = update_bpb(B, N, K, num_sms);
-  const int64_t slices = (P + segsum_slice(P, num_sms) - 1) / segsum_slice(P, num_sms);
+  const int64_t slices = (P + segsum_slice(P, BK, num_sms, dt) - 1) / segsum_slice(P, BK, num_sms, dt);
   // segment partials: per-slice boundary partials, or the f64 path's pieces
   // (B * (K + kF64MaxSpans) rows of d)
   const int64_t spans = N < kF64MaxSpans ? N : kF64MaxSpans;
   const size_t part = std::max((size_t)slices * 2 * d * 8,
                                dt == DT_F64 ? (size_t)(B * (K + spans)) * d * 8 : (size_t)0);
-  const size_t sz[7] = {al((size_t)B * bpb * K * 4), al((size_t)BK * 4), al((size_t)(BK + 1) * 8),
-                        al((size_t)P * 4),           al((size_t)BK * 4), al(part),
-                        al((size_t)B * bpb * 4)};
+  // table and inval adjacent: one range to clear when the assign builds them
+  const size_t sz[7] = {al((size_t)B * bpb * K * 4), al((size_t)B * bpb * 4), al((size_t)BK * 4),
+                        al((size_t)(BK + 1) * 8),    al((size_t)P * 4),       al((size_t)BK * 4),
+                        al(part)};
   size_t total = 0;
   uint8_t* p = static_cast<uint8_t*>(base);
   void* ptrs[7];
@@ -1190,12 +1365,13 @@ static size_t update_ws_layout(int dt, int64_t B, int64_t N, int64_t K, int64_t 
   }
   if (ws) {
     ws->table = (int32_t*)ptrs[0];
-    ws->hist = (int32_t*)ptrs[1];
-    ws->off = (int64_t*)ptrs[2];
-    ws->order = (int32_t*)ptrs[3];
-    ws->arrive = (int32_t*)ptrs[4];
-    ws->part = (double*)ptrs[5];
-    ws->inval = (int32_t*)ptrs[6];
+    ws->inval = (int32_t*)ptrs[1];
+    ws->hist = (int32_t*)ptrs[2];
+    ws->off = (int64_t*)ptrs[3];
+    ws->order = (int32_t*)ptrs[4];
+    ws->arrive = (int32_t*)ptrs[5];
+    ws->part = (double*)ptrs[6];
+    ws->zero_n = (int64_t)((sz[0] + (size_t)B * bpb * 4) / 4);
   }
   return total;
 }
@@ -1340,18 +1516,27 @@ static bool segsum_f64_serial() {
 template <typename T, typename A>
 static cudaError_t dispatch_segsum(const void* X, const UpdateWs& w, int64_t BK, int64_t P, int64_t d,
                                    double* sums, int num_sms, cudaStream_t s, const int32_t* ids,
-                                   int64_t N, int64_t K) {
+                                   int64_t N, int64_t K, int accumulate, bool clear_table) {
   const int th = 256;
-  const int64_t L = segsum_slice(P, num_sms);
+  const int64_t L = segsum_slice(P, BK, num_sms, sizeof(T) == 2 ? DT_BF16 : sizeof(T) == 4 ? DT_F32 : DT_F64);
   const int64_t warps = (P + L - 1) / L;
   const unsigned grid = (unsigned)((warps * 32 + th - 1) / th);
   const int64_t row_bytes = d * (int64_t)sizeof(T);
   const bool vec_ok = (row_bytes % 16) == 0;
   const int64_t nvec = row_bytes / 16;  // 16-byte vectors per row
   const T* x = (const T*)X;
-  const SegMerge mg{w.part, w.arrive, L, d};
-#define FK_SEG(LPR, VPL, U) \
-  k_segsum<T, A, LPR, VPL, U><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, ids, N, K, mg)
+  const SegMerge mg{w.part, w.arrive, L, d, clear_table ? w.table : nullptr, clear_table ? w.zero_n : 0};
+  const bool seq_env = !segsum_chained(P, BK);
+#define FK_SEG2(LPR, VPL, U, U2)                                                                        \
+  do {                                                                                                  \
+    if (seq_env)                                                                                        \
+      k_segsum<T, A, LPR, VPL, U><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, ids, N, K, mg); \
+    else                                                                                                \
+      k_segsum2<T, A, LPR, VPL, U2><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, ids, N, K,   \
+                                                        mg, accumulate);                                \
+  } while (0)
+  // k_segsum2 keeps 6 row steps where k_segsum had 8 (64 registers, no spills)
+#define FK_SEG(LPR, VPL, U) FK_SEG2(LPR, VPL, U, (U > 6 ? 6 : U))
   if (vec_ok) {
     switch (nvec) {
       case 1: FK_SEG(1, 1, 4); break;
@@ -1369,6 +1554,7 @@ static cudaError_t dispatch_segsum(const void* X, const UpdateWs& w, int64_t BK,
     k_segsum_generic<T><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, mg);
   }
 #undef FK_SEG
+#undef FK_SEG2
   return cudaGetLastError();
 }
 
@@ -1385,7 +1571,9 @@ static bool scatter_is_warp(int64_t K) {
 // counts, merges); the radix kernel needs k_scan to have run.
 static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t N, int64_t K,
                                          int64_t bpb, const UpdateWs& w, int64_t chunk, int accumulate,
-                                         int64_t* counts, int64_t* merges, cudaStream_t s) {
+                                         int64_t* counts, int64_t* merges, cudaStream_t s,
+                                         double* zero_sums = nullptr, int64_t zero_n = 0,
+                                         bool zero_arrive = false) {
   int bits = 1;
   while (bits < 31 && ((K - 1) >> bits) != 0) ++bits;
   const int np = (bits + 7) / 8;
@@ -1432,7 +1620,10 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
     }                                                                                              \
     k_scatter_warp<WV, CV><<<blocks, WV * 32, smem, s>>>(ids, N, K, (int)bpb, w.table, w.hist,     \
                                                          w.inval, B, chunk, accumulate, w.off,     \
-                                                         counts, merges, w.order, rank_sort);      \
+                                                         counts, merges, w.order, rank_sort,       \
+                                                         zero_sums, zero_n,                        \
+                                                         zero_arrive ? w.arrive : nullptr,         \
+                                                         zero_arrive ? B * K : 0);                 \
   } while (0)
 #define FK_SW(WV)        \
   do {                   \
@@ -1490,14 +1681,16 @@ static cudaError_t launch_scatter_stable(const int32_t* ids, int64_t B, int64_t 
 // and the stable scatter.
 static cudaError_t launch_sort_passes(const int32_t* ids, int64_t B, int64_t N, int64_t K, int64_t bpb,
                                       const UpdateWs& w, int64_t chunk, int accumulate, int64_t* counts,
-                                      int64_t* merges, cudaStream_t s) {
+                                      int64_t* merges, cudaStream_t s, double* zero_sums = nullptr,
+                                      int64_t zero_n = 0, bool zero_arrive = false) {
   const bool warp = scatter_is_warp(K);
   if (!(warp && bpb <= SW_COLS_BPB)) {
     const int64_t ktiles = (K + 31) / 32;
     k_colscan<<<(unsigned)(B * ktiles), dim3(32, 32), 0, s>>>(w.table, K, (int)bpb, ktiles, w.hist);
   }
   if (!warp) k_scan<<<(unsigned)B, 1024, 0, s>>>(w.hist, B, N, K, chunk, accumulate, w.off, counts, merges);
-  return launch_scatter_stable(ids, B, N, K, bpb, w, chunk, accumulate, counts, merges, s);
+  return launch_scatter_stable(ids, B, N, K, bpb, w, chunk, accumulate, counts, merges, s, zero_sums,
+                               zero_n, zero_arrive);
 }
 
 // The stable argsort alone (argsort_assignments, sort_inverse.py:67-78):
@@ -1520,10 +1713,30 @@ cudaError_t launch_argsort(const int32_t* ids, int64_t B, int64_t N, int64_t K, 
   return launch_sort_passes(ids, B, N, K, bpb, w, N, 0, nullptr, nullptr, s);
 }
 
+// The block histogram table inside an update workspace, for the assign to
+// build (fk_assign_hist): table (B * bpb rows of K int32), inval (B * bpb),
+// blocks per batch element and points per block.  False where the fold is not
+// offered (the radix scatter, K > SW_KMAX).
+bool update_hist_slots(int dt, int64_t B, int64_t N, int64_t K, int64_t d, int num_sms, void* ws,
+                       int32_t** table, int32_t** inval, int64_t* bpb_out, int64_t* per_out,
+                       int64_t* words) {
+  if (!scatter_is_warp(K)) return false;
+  const int sms = num_sms < kMaxSms ? num_sms : kMaxSms;
+  UpdateWs w;
+  update_ws_layout(dt, B, N, K, d, sms, ws, &w);
+  const int64_t bpb = update_bpb(B, N, K, sms);
+  *table = w.table;
+  *inval = w.inval;
+  *bpb_out = bpb;
+  *per_out = (N + bpb - 1) / bpb;
+  *words = w.zero_n;
+  return true;
+}
+
 cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, int64_t N,
                           int64_t K, int64_t d, int64_t chunk, int accumulate, double* sums,
                           int64_t* counts, int64_t* merges, void* ws, int num_sms,
-                          cudaStream_t s) {
+                          cudaStream_t s, int prehist) {
   const int64_t BK = B * K, P = B * N;
   const int sms = num_sms < kMaxSms ? num_sms : kMaxSms;
   UpdateWs w;
@@ -1531,20 +1744,29 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
   const int64_t bpb = update_bpb(B, N, K, sms);
   const unsigned blocks = (unsigned)(B * bpb);
   cudaError_t e;
-  const bool smem_keys = K <= HIST_SMEM_KEYS;
-  if (!smem_keys && (e = cudaMemsetAsync(w.table, 0, (size_t)B * bpb * K * 4, s)) != cudaSuccess)
-    return e;
-  // sums are cleared inside k_hist unless accumulating; so are the arrival counters
-  k_hist<<<blocks, 1024, smem_keys ? K * 4 : 0, s>>>(ids, N, K, (int)bpb, w.table,
-                                                     accumulate ? nullptr : sums, BK * d, w.arrive, BK,
-                                                     w.inval);
   const int64_t ch = chunk < 1 ? 1 : (chunk > N ? N : chunk);
-  if ((e = launch_sort_passes(ids, B, N, K, bpb, w, ch, accumulate, counts, merges, s)) != cudaSuccess)
-    return e;
+  if (prehist) {
+    // the assign built the block table (fk_assign_hist): no k_hist; the
+    // scatter clears the sums and arrival counters, k_segsum the table
+    if (!scatter_is_warp(K) || dt == DT_F64) return cudaErrorInvalidValue;
+    if ((e = launch_sort_passes(ids, B, N, K, bpb, w, ch, accumulate, counts, merges, s,
+                                accumulate ? nullptr : sums, BK * d, true)) != cudaSuccess)
+      return e;
+  } else {
+    const bool smem_keys = K <= HIST_SMEM_KEYS;
+    if (!smem_keys && (e = cudaMemsetAsync(w.table, 0, (size_t)B * bpb * K * 4, s)) != cudaSuccess)
+      return e;
+    // sums are cleared inside k_hist unless accumulating; so are the arrival counters
+    k_hist<<<blocks, 1024, smem_keys ? K * 4 : 0, s>>>(ids, N, K, (int)bpb, w.table,
+                                                       accumulate ? nullptr : sums, BK * d, w.arrive, BK,
+                                                       w.inval);
+    if ((e = launch_sort_passes(ids, B, N, K, bpb, w, ch, accumulate, counts, merges, s)) != cudaSuccess)
+      return e;
+  }
   switch (dt) {
-    case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, w, BK, P, d, sums, sms, s, ids, N, K);
-    case DT_F16: return dispatch_segsum<__half, float>(X, w, BK, P, d, sums, sms, s, ids, N, K);
-    case DT_F32: return dispatch_segsum<float, double>(X, w, BK, P, d, sums, sms, s, ids, N, K);
+    case DT_BF16: return dispatch_segsum<__nv_bfloat16, float>(X, w, BK, P, d, sums, sms, s, ids, N, K, accumulate, prehist != 0);
+    case DT_F16: return dispatch_segsum<__half, float>(X, w, BK, P, d, sums, sms, s, ids, N, K, accumulate, prehist != 0);
+    case DT_F32: return dispatch_segsum<float, double>(X, w, BK, P, d, sums, sms, s, ids, N, K, accumulate, prehist != 0);
     default:
       if (segsum_f64_serial()) {
         const int fgs = (int)((d + 31) / 32);
@@ -1567,7 +1789,7 @@ cudaError_t launch_update(int dt, const void* X, const int32_t* ids, int64_t B, 
         }
         return cudaGetLastError();
       }
-      return dispatch_segsum<double, double>(X, w, BK, P, d, sums, sms, s, ids, N, K);
+      return dispatch_segsum<double, double>(X, w, BK, P, d, sums, sms, s, ids, N, K, accumulate, prehist != 0);
   }
 }
 

@@ -8,6 +8,7 @@ tensors.  Nothing here computes on the host; nothing synchronizes.
 
 from __future__ import annotations
 
+import ctypes
 import os
 import threading
 
@@ -148,10 +149,49 @@ def split_auto(x: torch.Tensor, clusters: int) -> bool:
     return float(B) * n * clusters * d >= SPLIT_MIN_MACS
 
 
+class HistFold:
+    """An update workspace whose block histogram table the assign fills
+    (fk_assign_hist -> fk_update_prehist): the update's first pass (k_hist)
+    folded into the FlashAssign epilogue.  The table must be zero before an
+    assign adds into it; fk_update_prehist leaves it zeroed again, so only a
+    pair broken off after the assign (a speculative assign whose update never
+    ran) needs ``clear()``."""
+
+    def __init__(self, ws: torch.Tensor, table: int, inval: int, bpb: int, per: int, words: int):
+        self.ws, self.table, self.inval, self.bpb, self.per = ws, table, inval, bpb, per
+        off = table - ws.data_ptr()
+        self._clear = ws[off:off + 4 * words]
+
+    def clear(self) -> None:
+        self._clear.zero_()
+
+
+def hist_fold(x: torch.Tensor, clusters: int) -> HistFold | None:
+    """A HistFold for (B,N,d) bf16/fp16 data and K clusters, or None where the
+    fold is not offered (f32/f64 data, K > 16384, no tensor-core path)."""
+    dev = _require_cuda(x)
+    if x.dtype not in LOWP or x.dim() != 3:
+        return None
+    B, n, d = x.shape
+    K = int(clusters)
+    dt = fk_dtype(x.dtype)
+    L = N.lib()
+    ws = torch.zeros((int(L.fk_update_workspace(dt, B, n, K, d)),), dtype=torch.uint8, device=dev)
+    tab, inv = ctypes.c_void_p(), ctypes.c_void_p()
+    bpb, per, words = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    st = L.fk_update_hist_slots(dt, B, n, K, d, ws.data_ptr(), ctypes.byref(tab), ctypes.byref(inv),
+                                ctypes.byref(bpb), ctypes.byref(per), ctypes.byref(words))
+    if st == N.FK_EUNSUPPORTED:
+        return None
+    N.check(st, "fk_update_hist_slots")
+    return HistFold(ws, tab.value, inv.value, bpb.value, per.value, words.value)
+
+
 def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = None,
            changed: torch.Tensor | None = None, idx_out: torch.Tensor | None = None,
            mind_out: torch.Tensor | None = None, bias: torch.Tensor | None = None,
-           xsplit: torch.Tensor | None = None, dot_mode: str = "exact", path: str = "auto"):
+           xsplit: torch.Tensor | None = None, dot_mode: str = "exact", path: str = "auto",
+           hist: HistFold | None = None):
     """Nearest centroid per point: (ids int32 (B,N), min_dists (B,N)).
 
     min_dists is in the data dtype for float32/float64 data and float32 for
@@ -165,6 +205,8 @@ def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = Non
     ``assign_xsplit(x)``).  ``"fast"`` (the reference's relaxed mode) is
     served by the same certified path, so it returns the exact answer.  ``path``: "auto" | "split" | "mirror" (the exact
     CUDA-core kernel for every row) -- A/B and tests.
+    ``hist`` (bf16/fp16): also add the ids into that HistFold's block table
+    for a following ``update(..., hist=hist)``.
     """
     dev = _require_cuda(x, c)
     if x.dim() != 3 or c.dim() != 3 or x.shape[0] != c.shape[0] or x.shape[2] != c.shape[2]:
@@ -204,6 +246,15 @@ def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = Non
         return idx_out, mind_out
     need = L.fk_assign_workspace(dt, B, n, K, d)
     ws = _ws.get(dev, need, "assign")
+    if hist is not None:
+        st = L.fk_assign_hist(dt, x.data_ptr(), c.data_ptr(), None if bias is None else bias.data_ptr(),
+                              B, n, K, d, idx_out.data_ptr(), mind_out.data_ptr(),
+                              None if idx_prev is None else idx_prev.data_ptr(),
+                              None if changed is None else changed.data_ptr(),
+                              None if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                              hist.table, hist.inval, hist.bpb, hist.per, _stream(dev))
+        N.check(st, "fk_assign_hist")
+        return idx_out, mind_out
     st = L.fk_assign(dt, x.data_ptr(), c.data_ptr(), None if bias is None else bias.data_ptr(),
                      B, n, K, d, idx_out.data_ptr(),
                      mind_out.data_ptr(), None if idx_prev is None else idx_prev.data_ptr(),
@@ -216,11 +267,14 @@ def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = Non
 
 def update(x: torch.Tensor, ids: torch.Tensor, clusters: int, chunk: int | None = None,
            accumulate: bool = False, sums: torch.Tensor | None = None,
-           counts: torch.Tensor | None = None, merges: torch.Tensor | None = None):
+           counts: torch.Tensor | None = None, merges: torch.Tensor | None = None,
+           hist: HistFold | None = None):
     """Sort-inverse cluster statistics: (sums f64 (B,K,d), counts int64 (B,K)).
 
     ``merges`` (int64 device scalar, optional) is incremented by the segment
     count the reference's sort_inverse_update would record for ``chunk``.
+    ``hist``: the HistFold the preceding ``assign(..., hist=)`` filled (no
+    histogram pass here; the table is left zeroed).
     """
     dev = _require_cuda(x, ids)
     x = x.contiguous()
@@ -236,6 +290,13 @@ def update(x: torch.Tensor, ids: torch.Tensor, clusters: int, chunk: int | None 
         counts = torch.empty((B, K), dtype=torch.int64, device=dev)
     L = N.lib()
     need = L.fk_update_workspace(dt, B, n, K, d)
+    if hist is not None:
+        st = L.fk_update_prehist(dt, x.data_ptr(), ids.data_ptr(), B, n, K, d, int(chunk or n),
+                                 1 if accumulate else 0, sums.data_ptr(), counts.data_ptr(),
+                                 None if merges is None else merges.data_ptr(), hist.ws.data_ptr(),
+                                 hist.ws.numel(), _stream(dev))
+        N.check(st, "fk_update_prehist")
+        return sums, counts
     ws = _ws.get(dev, need, "update")
     st = L.fk_update(dt, x.data_ptr(), ids.data_ptr(), B, n, K, d, int(chunk or n),
                      1 if accumulate else 0, sums.data_ptr(), counts.data_ptr(),

@@ -23,6 +23,7 @@ centroid shift falls to shift_tol, or at max_iters.  B200 design:
 from __future__ import annotations
 
 import math
+import os
 import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -132,6 +133,10 @@ class LloydEngine:
             self._hist = None
             self._hist_row = torch.zeros((), dtype=torch.int64, device=dev)
             self._tail_ctr = torch.zeros((1,), dtype=torch.int32, device=dev)  # last-block counter
+            # the update's histogram pass folded into the assign epilogue
+            # (bf16/fp16, the pipelined run only; FK_HIST_FOLD=0 switches it off)
+            self._fold = ops.hist_fold(self.x, K) if (
+                self.xsplit is None and os.environ.get("FK_HIST_FOLD", "1") != "0") else None
             if self.dtype in LOW_PRECISION:
                 kpad = ops.N.lib().fk_assign_bias_rows(K)
                 self.bias = [torch.zeros((B, kpad, 16), dtype=torch.bfloat16, device=dev) for _ in range(2)]
@@ -266,10 +271,13 @@ class LloydEngine:
         def fn():
             if not self.fused:  # the fused tail leaves `changed` cleared
                 self.changed.zero_()
+            kw = self._assign_kw(csrc)
+            if self.fused and self._fold is not None:
+                kw["hist"] = self._fold
             self.be.assign(self.x, self.operand[csrc],
                            idx_prev=self.ids[slot ^ 1] if compare else None,
                            changed=self.changed if compare else None, idx_out=self.ids[slot],
-                           mind_out=self.mind, **self._assign_kw(csrc))
+                           mind_out=self.mind, **kw)
         self._graph(("a", slot, compare, csrc), fn)
 
     def enq_rest(self, slot: int, history_row: torch.Tensor | None = None, timers=None) -> None:
@@ -293,7 +301,8 @@ class LloydEngine:
             if timers is not None:  # bench: live per-kernel timing (eager only)
                 timers[0].record()
             self.be.update(self.x, self.ids[slot], self.K, self.chunk, sums=self.sums,
-                           counts=self.counts, merges=self.merges_it)
+                           counts=self.counts, merges=self.merges_it,
+                           **({} if self._fold is None else {"hist": self._fold}))
             if timers is not None:
                 timers[1].record()
             ops.normalize_loop_tail(
@@ -350,6 +359,8 @@ class LloydEngine:
         slot = 0
         it = 0
         if self.fused:  # the loop tail writes history rows through a device row index
+            if self._fold is not None:  # a speculative assign of an earlier run may have added
+                self._fold.clear()
             self._hist = history
             self._hist_row.zero_()
             self.changed.zero_()

@@ -190,6 +190,39 @@ def test_baseline_engine_agrees_on_separated_blobs():
     np.testing.assert_allclose(rf.centroids.numpy(), rb.centroids.numpy(), rtol=1e-12)
 
 
+@pytest.mark.parametrize("prec", ["bf16", "fp16"])
+def test_pipelined_runs_with_hist_fold_equal_stepwise(prec):
+    """bf16/fp16: LloydEngine.run folds the update's histogram pass into the
+    assign epilogue (fk_assign_hist / fk_update_prehist); iterate() does not.
+    Two consecutive runs (the first ends with a speculative assign whose table
+    the second must clear) equal the stepwise loop bit for bit."""
+    from paper_2603_09229_b200 import LloydEngine
+
+    x = fk.generate_dataset(3, 20000, 24, 32, 1.0, 7, prec).data.cuda()
+    c0 = torch.stack([x[b, :48] for b in range(3)]).float()
+    eng = LloydEngine(x, 48, 4096)
+    assert eng._fold is not None
+    eng.set_centroids(c0)
+    ref = LloydEngine(x, 48, 4096)
+    ref.set_centroids(c0)
+    # runs stopped by the shift test after one iteration leave a speculative
+    # assign behind (its histogram in the table); the next run clears it
+    for n_it in (1, 1, 3, 1, 2):
+        if n_it == 1:
+            its, slot, _ = eng.run(10, 1e30)
+        else:
+            its, slot, _ = eng.run(n_it, -1.0, stop_on_repeat=False)
+        assert its == n_it
+        for _ in range(n_it):
+            slot_b = ref.iterate()
+            ref.poll()
+            ref.commit()
+        torch.cuda.synchronize()
+        assert torch.equal(eng.centroids, ref.centroids)
+        assert torch.equal(eng.ids[slot], ref.ids[slot_b])
+        assert torch.equal(eng.counts, ref.counts)
+
+
 @pytest.mark.parametrize("stop_iter_cap", [3, 40])
 def test_pipelined_run_equals_stepwise_loop(stop_iter_cap):
     """LloydEngine.run queues the next assign before each poll (speculation);

@@ -378,3 +378,42 @@ def test_device_farthest_is_reference_order(ops, n, E, dtype, ties):
         v = m[b].double().numpy()
         ref = np.lexsort((np.arange(n), -v))[:E]
         assert np.array_equal(got[b], ref)
+
+
+# ----------------------------------------------------------- histogram fold
+@pytest.mark.parametrize("B,N,K,d,dtype", [
+    (1, 100_000, 1024, 128, torch.bfloat16),   # bpb > 16: k_colscan reads the folded table
+    (64, 16384, 256, 64, torch.float16),       # config 4's shape
+    (3, 20_001, 37, 32, torch.bfloat16),       # ragged N, odd K
+    (2, 50_000, 3000, 64, torch.float16),      # K beyond the shared-memory bins
+    (1, 3000, 9000, 16, torch.bfloat16),       # more keys than points per block
+])
+def test_hist_fold_equals_assign_then_update(ops, B, N, K, d, dtype):
+    """fk_assign_hist + fk_update_prehist == fk_assign + fk_update bit for bit
+    (ids, min_dists, sums, counts, merges), and the table is left zeroed for
+    the next assign (checked by running the pair twice)."""
+    g = torch.Generator(device="cuda").manual_seed(N + K)
+    x = (torch.randn((B, N, d), device="cuda", generator=g) * 3).to(dtype)
+    c = x[:, torch.randperm(N, device="cuda", generator=g)[:K]].contiguous()
+    ids_r, m_r = ops.assign(x, c)
+    mg_r = torch.zeros((), dtype=torch.int64, device="cuda")
+    s_r, n_r = ops.update(x, ids_r, K, 4096, merges=mg_r)
+    s_r, n_r = s_r.clone(), n_r.clone()
+    fold = ops.hist_fold(x, K)
+    assert fold is not None
+    for rep in range(2):
+        ids, m = ops.assign(x, c, hist=fold)
+        mg = torch.zeros((), dtype=torch.int64, device="cuda")
+        s, n = ops.update(x, ids, K, 4096, merges=mg, hist=fold)
+        assert torch.equal(ids, ids_r) and torch.equal(m, m_r)
+        assert torch.equal(n, n_r)
+        assert torch.equal(s.view(torch.int64), s_r.view(torch.int64))
+        assert int(mg) == int(mg_r)
+        assert int(fold._clear.count_nonzero()) == 0
+
+
+def test_hist_fold_offered_where_supported(ops):
+    x = torch.zeros((1, 1000, 32), dtype=torch.bfloat16, device="cuda")
+    assert ops.hist_fold(x, 16) is not None
+    assert ops.hist_fold(x.float(), 16) is None       # f32 data: the certified path, no fold
+    assert ops.hist_fold(x, 20_000) is None           # K beyond the warp-table scatter
