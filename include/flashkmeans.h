@@ -192,7 +192,13 @@ FK_API fk_status fk_assign_hist(fk_dtype dt, const void* X, const void* C, const
                                 int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
                                 const int32_t* idx_prev, int32_t* changed_flag, void* workspace,
                                 size_t workspace_bytes, int32_t* hist_table, int32_t* hist_inval,
-                                int64_t hist_bpb, int64_t hist_per, void* stream);
+                                int64_t hist_bpb, int64_t hist_per, const float* xnorm, void* stream);
+/* xnorm (optional, fk_assign_hist): (B, N) fp32 ||x||^2 of X written once per
+ * data set by fk_assign_row_norms (same K), which sums every row exactly as
+ * the tensor-core epilogue would from its shared-memory tile -- min_dists are
+ * bitwise unchanged and the epilogue skips that sum on every call.          */
+FK_API fk_status fk_assign_row_norms(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t K,
+                                     int64_t d, float* xnorm_out, void* stream);
 FK_API fk_status fk_update_prehist(fk_dtype dt, const void* X, const int32_t* ids, int64_t B,
                                    int64_t N, int64_t K, int64_t d, int64_t update_chunk,
                                    int32_t accumulate, double* sums, int64_t* counts, int64_t* merges_out,

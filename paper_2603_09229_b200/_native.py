@@ -66,7 +66,9 @@ def _declare(L):
                                        ctypes.POINTER(I64)]
     L.fk_assign_hist.restype = ctypes.c_int
     L.fk_assign_hist.argtypes = [ctypes.c_int, P, P, P, I64, I64, I64, I64, P, P, P, P, P, SZ, P, P, I64,
-                                 I64, P]
+                                 I64, P, P]
+    L.fk_assign_row_norms.restype = ctypes.c_int
+    L.fk_assign_row_norms.argtypes = [ctypes.c_int, P, I64, I64, I64, I64, P, P]
     L.fk_argsort.restype = ctypes.c_int
     L.fk_argsort.argtypes = [P, I64, I64, I64, P, P, P, SZ, P]
     L.fk_normalize.restype = ctypes.c_int
@@ -112,7 +114,7 @@ EXPORTED = (
     "fk_assign_workspace", "fk_assign_bias_rows", "fk_assign_bias", "fk_assign", "fk_assign_xsplit_bytes",
     "fk_assign_xsplit", "fk_assign_split_workspace", "fk_assign_split", "fk_assign_split_fallback_rows",
     "fk_update_workspace",
-    "fk_update", "fk_update_prehist", "fk_update_hist_slots", "fk_assign_hist", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
+    "fk_update", "fk_update_prehist", "fk_update_hist_slots", "fk_assign_hist", "fk_assign_row_norms", "fk_argsort", "fk_normalize", "fk_row_norms", "fk_objective_workspace", "fk_objective",
     "fk_objective_partials", "fk_loop_tail", "fk_normalize_loop_tail", "fk_scatter",
     "fk_stats_pack", "fk_merges_from_counts", "fk_farthest_workspace", "fk_farthest",
     "fk_kmeanspp_workspace", "fk_kmeanspp",

@@ -329,7 +329,7 @@ static fk_status assign_impl(fk_dtype dt, const void* X, const void* C, const vo
                              int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
                              const int32_t* idx_prev, int32_t* changed_flag, void* ws, size_t ws_bytes,
                              void* stream, int32_t* hist_table, int32_t* hist_inval, int64_t hist_bpb,
-                             int64_t hist_per);
+                             int64_t hist_per, const float* xnorm = nullptr);
 
 fk_status fk_assign(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B, int64_t N,
                     int64_t K, int64_t d, int32_t* idx_out, void* mind_out, const int32_t* idx_prev,
@@ -342,19 +342,27 @@ fk_status fk_assign_hist(fk_dtype dt, const void* X, const void* C, const void* 
                          int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
                          const int32_t* idx_prev, int32_t* changed_flag, void* ws, size_t ws_bytes,
                          int32_t* hist_table, int32_t* hist_inval, int64_t hist_bpb, int64_t hist_per,
-                         void* stream) {
+                         const float* xnorm, void* stream) {
   if (!hist_table || !hist_inval || hist_bpb < 1 || hist_per < 1 || hist_bpb * hist_per < N)
     return FK_EINVAL;
   if (!is_lowp(dt) || !tc_path(dt, d, X, C)) return FK_EUNSUPPORTED;
   return assign_impl(dt, X, C, bias, B, N, K, d, idx_out, mind_out, idx_prev, changed_flag, ws, ws_bytes,
-                     stream, hist_table, hist_inval, hist_bpb, hist_per);
+                     stream, hist_table, hist_inval, hist_bpb, hist_per, xnorm);
+}
+
+fk_status fk_assign_row_norms(fk_dtype dt, const void* X, int64_t B, int64_t N, int64_t K, int64_t d,
+                              float* out, void* stream) {
+  if (!valid_dt(dt) || !shape_ok(B, N, K, d) || !X || !out) return FK_EINVAL;
+  if (!is_lowp(dt) || !tc_path(dt, d, X, X)) return FK_EUNSUPPORTED;
+  return cuda_status(fk::launch_row_norms_tc(dt == FK_BF16 ? 1 : 0, X, B, N, K, d, out,
+                                             reinterpret_cast<cudaStream_t>(stream)));
 }
 
 static fk_status assign_impl(fk_dtype dt, const void* X, const void* C, const void* bias, int64_t B,
                              int64_t N, int64_t K, int64_t d, int32_t* idx_out, void* mind_out,
                              const int32_t* idx_prev, int32_t* changed_flag, void* ws, size_t ws_bytes,
                              void* stream, int32_t* hist_table, int32_t* hist_inval, int64_t hist_bpb,
-                             int64_t hist_per) {
+                             int64_t hist_per, const float* xnorm) {
   if (!valid_dt(dt) || !shape_ok(B, N, K, d)) return FK_EINVAL;
   if (!X || !C || !idx_out || !mind_out) return FK_EINVAL;
   if (idx_prev && !changed_flag) return FK_EINVAL;
@@ -384,7 +392,7 @@ static fk_status assign_impl(fk_dtype dt, const void* X, const void* C, const vo
       return cuda_status(fk::launch_assign_tc(fmt, X, C, cn, ext, B, N, K, d, idx_out,
                                               reinterpret_cast<float*>(mind_out), idx_prev,
                                               changed_flag, di.sms, s, hist_table, hist_inval, hist_bpb,
-                                              hist_per));
+                                              hist_per, xnorm));
     }
     fk_status st = cuda_status(fk::launch_cn_pad(dt, C, B, K, d, (int)K, cn, s));
     if (st != FK_OK) return st;

@@ -90,6 +90,10 @@ struct TcArgs {
   int32_t* hist_tab;
   int32_t* hist_inval;
   int hist_bpb, hist_per;
+  // (B, N) fp32 ||x||^2 precomputed by k_row_norms_tc with the epilogue's own
+  // arithmetic (X is fixed through a Lloyd run): loaded instead of summing the
+  // row from the shared-memory tile every row tile; nullptr: summed here
+  const float* xn_in;
 };
 
 constexpr int SPLIT_NREC = 4;                  // near chunks kept per thread (per column half)
@@ -870,6 +874,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       int prev_id = -2;
       if (p.idx_prev && (alt || wg == 0) && row0 + row < p.N)
         prev_id = __ldg(p.idx_prev + (size_t)b * p.N + row0 + row);
+      float xn_pre = 0.f;  // the precomputed ||x||^2 (owner warpgroup; the other adds 0)
+      if (!SPLIT && p.xn_in && (alt || wg == 0) && row0 + row < p.N)
+        xn_pre = __ldg(p.xn_in + (size_t)b * p.N + row0 + row);
       float M = __int_as_float(0x7f800000);
       float m2 = M;  // split: lower bound on the row's second-best score
       float smg = 0.f;  // split: certificate margin of this row
@@ -904,6 +911,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             xn = split_norm_ub(sA + slot * a_slot_bytes, row, p.katoms, p.ns, lane);
             smg = 0x1p-11f * fmaf(xn, cmx, cmx * cmx) + 0x1p-18f * xn * xn + 0x1p-100f;
             smg *= 1.0f + 0x1p-20f;
+          } else if (p.xn_in) {
+            xn = xn_pre;
           } else {
             xn = alt ? row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane)
                      : row_norm_smem<FMT>(sA + slot * a_slot_bytes, row, p.katoms, lane, 4 * wg,
@@ -1138,6 +1147,17 @@ static cudaError_t launch_pair_t(const CUtensorMap& tmx, const CUtensorMap& tmc,
   return cudaGetLastError();
 }
 
+// Rows of a single column tile (K <= 256) alternate tiles between the two
+// epilogue warpgroups; FK_ASSIGN_ALT=0 splits their columns instead (A/B)
+static bool pair_alt(int K) {
+  static int alt_env = -1;
+  if (alt_env < 0) {
+    const char* e = getenv("FK_ASSIGN_ALT");
+    alt_env = (e && e[0] == '0') ? 0 : 1;
+  }
+  return (K + tc2::BN - 1) / tc2::BN == 1 && alt_env;
+}
+
 template <int FMT, int BIAS>
 static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
                                const CUtensorMap& tmext, TcArgs a, int num_sms,
@@ -1148,13 +1168,62 @@ static cudaError_t launch_pair(const CUtensorMap& tmx, const CUtensorMap& tmc,
   int pairs = num_sms / 2;
   if (a.total_tiles < pairs) pairs = a.total_tiles;
   if (pairs <= 0) return cudaSuccess;
-  static int alt_env = -1;  // FK_ASSIGN_ALT=0: split single-column-tile rows across both WGs (A/B)
-  if (alt_env < 0) {
-    const char* e = getenv("FK_ASSIGN_ALT");
-    alt_env = (e && e[0] == '0') ? 0 : 1;
-  }
-  return (a.ncol == 1 && alt_env) ? launch_pair_t<FMT, BIAS, true>(tmx, tmc, tmext, a, pairs, stream)
-                                  : launch_pair_t<FMT, BIAS, false>(tmx, tmc, tmext, a, pairs, stream);
+  return pair_alt(a.K) ? launch_pair_t<FMT, BIAS, true>(tmx, tmc, tmext, a, pairs, stream)
+                       : launch_pair_t<FMT, BIAS, false>(tmx, tmc, tmext, a, pairs, stream);
+}
+
+// ---------------------------------------------------- row norms, epilogue order
+// ||x||^2 of every row exactly as the pair kernel's epilogue sums it from the
+// 128-byte-swizzled shared tile (row_norm_smem): lane = row % 32 reads
+// physical 16-byte chunk (j + lane) & 7, i.e. logical chunk
+// ((j + lane) & 7) ^ (row & 7), atoms in order, element pairs (lo, hi) by
+// fmaf; columns beyond d are the tile's zero fill.  ALT (one column tile):
+// one sum over j = 0..7; otherwise the two warpgroups' halves (j < 4, j >= 4)
+// added (wg0 + wg1) as the epilogue's merge does.
+template <int FMT>
+__global__ void __launch_bounds__(256)
+    k_row_norms_tc(const uint16_t* __restrict__ X, int64_t rows, int64_t N, int d, int alt,
+                   float* __restrict__ out) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const int grow = (int)(r % N);
+  const int lane = grow & 31, sw = grow & 7;
+  const uint16_t* xr = X + r * d;
+  const int katoms = (d + 63) / 64;
+  auto f = [&](int k) -> float {
+    if (k >= d) return 0.f;
+    const uint16_t h = xr[k];
+    if (FMT == 1) return __uint_as_float((uint32_t)h << 16);
+    return __half2float(__ushort_as_half(h));
+  };
+  auto part = [&](int j0, int j1) {
+    float acc = 0.f;
+    for (int ka = 0; ka < katoms; ++ka)
+      for (int j = j0; j < j1; ++j) {
+        const int base = ka * 64 + ((((j + lane) & 7) ^ sw) << 3);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float lo = f(base + 2 * e), hi = f(base + 2 * e + 1);
+          acc = fmaf(lo, lo, acc);
+          acc = fmaf(hi, hi, acc);
+        }
+      }
+    return acc;
+  };
+  out[r] = alt ? part(0, 8) : part(0, 4) + part(4, 8);
+}
+
+cudaError_t launch_row_norms_tc(int fmt, const void* X, int64_t B, int64_t N, int64_t K, int64_t d,
+                                float* out, cudaStream_t stream) {
+  const int64_t rows = B * N;
+  if (rows < 1) return cudaSuccess;
+  const unsigned grid = (unsigned)((rows + 255) / 256);
+  const int alt = pair_alt((int)K) ? 1 : 0;
+  if (fmt == 1)
+    k_row_norms_tc<1><<<grid, 256, 0, stream>>>((const uint16_t*)X, rows, N, (int)d, alt, out);
+  else
+    k_row_norms_tc<0><<<grid, 256, 0, stream>>>((const uint16_t*)X, rows, N, (int)d, alt, out);
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- host side
@@ -1209,8 +1278,10 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
                              const void* cn_ext, int64_t B, int64_t N, int64_t K, int64_t d,
                              int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
                              int32_t* changed, int num_sms, cudaStream_t stream, int32_t* hist_tab,
-                             int32_t* hist_inval, int64_t hist_bpb, int64_t hist_per) {
+                             int32_t* hist_inval, int64_t hist_bpb, int64_t hist_per,
+                             const float* xn_in) {
   TcArgs a;
+  a.xn_in = xn_in;
   a.hist_tab = hist_tab;
   a.hist_inval = hist_inval;
   a.hist_bpb = (int)hist_bpb;
@@ -1284,7 +1355,7 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     }
     return e;
   }
-  if (hist_tab) return cudaErrorInvalidValue;  // the single-CTA A/B kernel has no histogram fold
+  if (hist_tab || xn_in) return cudaErrorInvalidValue;  // the single-CTA A/B kernel: neither
   CUtensorMap tmx, tmc;
   if (!make_map(&tmx, X, fmt, d, N, B, tc::BM)) return cudaErrorInvalidValue;
   if (!make_map(&tmc, C, fmt, d, K, B, tc::BN)) return cudaErrorInvalidValue;
@@ -1314,6 +1385,7 @@ cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* e
   if (ns < 1 || 2 * ns > 4 * tc2::KATOMS_MAX) return cudaErrorInvalidValue;
   const int64_t W = 32 * (int64_t)ns;
   TcArgs a;
+  a.xn_in = nullptr;
   a.hist_tab = nullptr;
   a.hist_inval = nullptr;
   a.hist_bpb = 1;

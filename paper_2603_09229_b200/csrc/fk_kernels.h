@@ -18,7 +18,10 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
                              int32_t* idx_out, float* mind_out, const int32_t* idx_prev,
                              int32_t* changed, int num_sms, cudaStream_t stream,
                              int32_t* hist_tab = nullptr, int32_t* hist_inval = nullptr,
-                             int64_t hist_bpb = 1, int64_t hist_per = 1);
+                             int64_t hist_bpb = 1, int64_t hist_per = 1,
+                             const float* xn_in = nullptr);
+cudaError_t launch_row_norms_tc(int fmt, const void* X, int64_t B, int64_t N, int64_t K, int64_t d,
+                                float* out, cudaStream_t stream);
 
 constexpr int kSplitRecInts = 10;  // fk_assign_tc.cu FK_SPLIT_REC: [row, n, up to 8 chunk bases]
 cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* ext, int64_t B,

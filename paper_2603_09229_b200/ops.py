@@ -187,11 +187,29 @@ def hist_fold(x: torch.Tensor, clusters: int) -> HistFold | None:
     return HistFold(ws, tab.value, inv.value, bpb.value, per.value, words.value)
 
 
+def assign_row_norms(x: torch.Tensor, clusters: int) -> torch.Tensor | None:
+    """(B,N) fp32 ||x||^2 of bf16/fp16 data summed exactly as the tensor-core
+    epilogue sums it for K = ``clusters`` (fk_assign_row_norms), or None where
+    that path is not taken."""
+    dev = _require_cuda(x)
+    if x.dtype not in LOWP or x.dim() != 3:
+        return None
+    x = x.contiguous()
+    B, n, d = x.shape
+    out = torch.empty((B, n), dtype=torch.float32, device=dev)
+    st = N.lib().fk_assign_row_norms(fk_dtype(x.dtype), x.data_ptr(), B, n, int(clusters), d,
+                                     out.data_ptr(), _stream(dev))
+    if st == N.FK_EUNSUPPORTED:
+        return None
+    N.check(st, "fk_assign_row_norms")
+    return out
+
+
 def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = None,
            changed: torch.Tensor | None = None, idx_out: torch.Tensor | None = None,
            mind_out: torch.Tensor | None = None, bias: torch.Tensor | None = None,
            xsplit: torch.Tensor | None = None, dot_mode: str = "exact", path: str = "auto",
-           hist: HistFold | None = None):
+           hist: HistFold | None = None, xnorm: torch.Tensor | None = None):
     """Nearest centroid per point: (ids int32 (B,N), min_dists (B,N)).
 
     min_dists is in the data dtype for float32/float64 data and float32 for
@@ -206,7 +224,8 @@ def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = Non
     served by the same certified path, so it returns the exact answer.  ``path``: "auto" | "split" | "mirror" (the exact
     CUDA-core kernel for every row) -- A/B and tests.
     ``hist`` (bf16/fp16): also add the ids into that HistFold's block table
-    for a following ``update(..., hist=hist)``.
+    for a following ``update(..., hist=hist)``; ``xnorm`` (with ``hist``):
+    ``assign_row_norms(x, K)`` of this data, min_dists unchanged bitwise.
     """
     dev = _require_cuda(x, c)
     if x.dim() != 3 or c.dim() != 3 or x.shape[0] != c.shape[0] or x.shape[2] != c.shape[2]:
@@ -252,7 +271,8 @@ def assign(x: torch.Tensor, c: torch.Tensor, idx_prev: torch.Tensor | None = Non
                               None if idx_prev is None else idx_prev.data_ptr(),
                               None if changed is None else changed.data_ptr(),
                               None if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
-                              hist.table, hist.inval, hist.bpb, hist.per, _stream(dev))
+                              hist.table, hist.inval, hist.bpb, hist.per,
+                              None if xnorm is None else xnorm.data_ptr(), _stream(dev))
         N.check(st, "fk_assign_hist")
         return idx_out, mind_out
     st = L.fk_assign(dt, x.data_ptr(), c.data_ptr(), None if bias is None else bias.data_ptr(),

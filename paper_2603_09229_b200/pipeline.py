@@ -137,6 +137,10 @@ class LloydEngine:
             # (bf16/fp16, the pipelined run only; FK_HIST_FOLD=0 switches it off)
             self._fold = ops.hist_fold(self.x, K) if (
                 self.xsplit is None and os.environ.get("FK_HIST_FOLD", "1") != "0") else None
+            # ||x||^2 in the epilogue's own order, once per run (X is fixed):
+            # the epilogue loads it instead of summing the tile row each time
+            self._xn = ops.assign_row_norms(self.x, K) if (
+                self._fold is not None and os.environ.get("FK_ASSIGN_XNORM", "1") != "0") else None
             if self.dtype in LOW_PRECISION:
                 kpad = ops.N.lib().fk_assign_bias_rows(K)
                 self.bias = [torch.zeros((B, kpad, 16), dtype=torch.bfloat16, device=dev) for _ in range(2)]
@@ -274,6 +278,8 @@ class LloydEngine:
             kw = self._assign_kw(csrc)
             if self.fused and self._fold is not None:
                 kw["hist"] = self._fold
+                if self._xn is not None:
+                    kw["xnorm"] = self._xn
             self.be.assign(self.x, self.operand[csrc],
                            idx_prev=self.ids[slot ^ 1] if compare else None,
                            changed=self.changed if compare else None, idx_out=self.ids[slot],

@@ -417,3 +417,27 @@ def test_hist_fold_offered_where_supported(ops):
     assert ops.hist_fold(x, 16) is not None
     assert ops.hist_fold(x.float(), 16) is None       # f32 data: the certified path, no fold
     assert ops.hist_fold(x, 20_000) is None           # K beyond the warp-table scatter
+
+
+@pytest.mark.parametrize("B,N,K,d,dtype", [
+    (2, 5000, 200, 64, torch.float16),     # one column tile: the alternating epilogue
+    (3, 7001, 256, 96, torch.bfloat16),
+    (1, 20000, 1024, 128, torch.bfloat16),  # column halves merged across warpgroups
+    (2, 3000, 300, 200, torch.float16),     # 4 atoms, zero-filled tail
+    (4, 999, 64, 8, torch.bfloat16),
+])
+def test_precomputed_row_norms_keep_min_dists_bitwise(ops, B, N, K, d, dtype):
+    """fk_assign_row_norms sums ||x||^2 exactly as the tensor-core epilogue does
+    from its swizzled shared tile, so fk_assign_hist with xnorm returns the same
+    ids and min_dists bit for bit as the epilogue's own sum."""
+    g = torch.Generator(device="cuda").manual_seed(N + d)
+    x = (torch.randn((B, N, d), device="cuda", generator=g) * 2).to(dtype)
+    c = x[:, torch.randperm(N, device="cuda", generator=g)[:K]].contiguous()
+    ids_r, m_r = ops.assign(x, c)
+    xn = ops.assign_row_norms(x, K)
+    assert xn is not None and xn.shape == (B, N)
+    fold = ops.hist_fold(x, K)
+    ids, m = ops.assign(x, c, hist=fold, xnorm=xn)
+    ops.update(x, ids, K, N, hist=fold)  # consume the table
+    assert torch.equal(ids, ids_r)
+    assert torch.equal(m.view(torch.int32), m_r.view(torch.int32))
