@@ -433,7 +433,7 @@ def run_ours(args):
                      "peak_source": pk["src"] + " bf16_tflops (burst: the timed region is short)",
                      "algorithmic_flops_per_launch": flops, "ms_per_launch": t_assign,
                      "traffic": tr.get("fk_assign_tc", {}).get("dram_bytes")},
-        "roofline_update": {"bound": "hbm", "kernel": "fk_update (hist+scan+scatter+segsum)",
+        "roofline_update": {"bound": "hbm", "kernel": "fk_update (colscan+scatter+segsum; the block histogram is built in the assign epilogue)",
                             "achieved": upd_gbs, "peak": pk["hbm"], "unit": "GB/s", "frac": upd_gbs / pk["hbm"],
                             "algorithmic_bytes_per_launch": upd_bytes, "ms_per_launch": t_update,
                             "traffic": update_traffic(tr)},

@@ -1188,22 +1188,27 @@ __global__ void __launch_bounds__(256)
   if (r >= rows) return;
   const int grow = (int)(r % N);
   const int lane = grow & 31, sw = grow & 7;
-  const uint16_t* xr = X + r * d;
+  const uint4* xr = reinterpret_cast<const uint4*>(X + r * d);  // rows are 16-byte multiples
   const int katoms = (d + 63) / 64;
-  auto f = [&](int k) -> float {
-    if (k >= d) return 0.f;
-    const uint16_t h = xr[k];
-    if (FMT == 1) return __uint_as_float((uint32_t)h << 16);
-    return __half2float(__ushort_as_half(h));
-  };
   auto part = [&](int j0, int j1) {
     float acc = 0.f;
     for (int ka = 0; ka < katoms; ++ka)
       for (int j = j0; j < j1; ++j) {
-        const int base = ka * 64 + ((((j + lane) & 7) ^ sw) << 3);
+        const int lc = ka * 8 + (((j + lane) & 7) ^ sw);  // 16-byte chunk of the row
+        if (8 * lc >= d) continue;  // the tile's zero fill: fmaf(0, 0, acc) == acc
+        const uint4 w = __ldg(xr + lc);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float lo = f(base + 2 * e), hi = f(base + 2 * e + 1);
+          float lo, hi;
+          if (FMT == 1) {
+            lo = __uint_as_float(ws[e] << 16);
+            hi = __uint_as_float(ws[e] & 0xffff0000u);
+          } else {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ws[e]));
+            lo = f.x;
+            hi = f.y;
+          }
           acc = fmaf(lo, lo, acc);
           acc = fmaf(hi, hi, acc);
         }

@@ -1837,7 +1837,15 @@ constexpr int TAIL_STAGE = 4096;  // objective partials the last block stages in
 // obj = ((0 + part[0]) + part[1]) + ... (numpy's running sum over its buffers)
 FK_DEV double obj_fold(const double* part, int64_t n) {
   double acc = 0.0;
-  for (int64_t i = 0; i < n; ++i) acc = __dadd_rn(acc, part[i]);
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {  // loads ahead of the serial adds
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = part[i + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+  }
+  for (; i < n; ++i) acc = __dadd_rn(acc, part[i]);
   return acc;
 }
 
