@@ -1199,7 +1199,14 @@ static int64_t update_bpb(int64_t B, int64_t N, int64_t K, int num_sms) {
     if (bps < 1 || bps > 16) bps = 2;
   }
   int64_t bpb = ((int64_t)num_sms * bps + B - 1) / B;
-  const int64_t max_bpb = (N + SD_S - 1) / SD_S;
+  static int minpts = -1;  // FK_UPDATE_MINPTS: fewest points per block for the warp scatter (A/B)
+  if (minpts < 0) {
+    const char* e = getenv("FK_UPDATE_MINPTS");
+    minpts = e ? atoi(e) : SD_S;
+    if (minpts < 256 || minpts > SD_S) minpts = SD_S;
+  }
+  const int64_t per_min = K <= SW_KMAX ? minpts : SD_S;
+  const int64_t max_bpb = (N + per_min - 1) / per_min;
   if (bpb > max_bpb) bpb = max_bpb;
   if (K > HIST_SMEM_KEYS) {
     const int64_t cap = N / (2 * K);
