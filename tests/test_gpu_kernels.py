@@ -441,3 +441,26 @@ def test_precomputed_row_norms_keep_min_dists_bitwise(ops, B, N, K, d, dtype):
     ops.update(x, ids, K, N, hist=fold)  # consume the table
     assert torch.equal(ids, ids_r)
     assert torch.equal(m.view(torch.int32), m_r.view(torch.int32))
+
+
+def test_hist_fold_counts_invalid_rows(ops):
+    """Rows whose scores are all NaN get id -1 from the tensor-core assign; the
+    folded histogram counts them as invalid (hist_inval) exactly as k_hist
+    does, so the update skips them identically (offsets, sums, counts)."""
+    g = torch.Generator(device="cuda").manual_seed(3)
+    B, N, K, d = 2, 40000, 300, 64
+    x = torch.randn((B, N, d), device="cuda", generator=g).to(torch.bfloat16)
+    c = x[:, :K].clone()
+    x[0, 5:900:7] = float("nan")
+    x[1, -300:] = float("nan")
+    ids_r, m_r = ops.assign(x, c)
+    assert int((ids_r < 0).sum()) > 0
+    s_r, n_r = ops.update(x, ids_r, K, 4096)
+    s_r, n_r = s_r.clone(), n_r.clone()
+    fold = ops.hist_fold(x, K)
+    ids, m = ops.assign(x, c, hist=fold)
+    s, n = ops.update(x, ids, K, 4096, hist=fold)
+    assert torch.equal(ids, ids_r)
+    assert torch.equal(n, n_r)
+    assert torch.equal(s.view(torch.int64), s_r.view(torch.int64))
+    assert int(fold._clear.count_nonzero()) == 0
