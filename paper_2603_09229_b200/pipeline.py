@@ -138,9 +138,13 @@ class LloydEngine:
             self._fold = ops.hist_fold(self.x, K) if (
                 self.xsplit is None and os.environ.get("FK_HIST_FOLD", "1") != "0") else None
             # ||x||^2 in the epilogue's own order, once per run (X is fixed):
-            # the epilogue loads it instead of summing the tile row each time
+            # the epilogue loads it instead of summing the tile row every row
+            # tile -- worth its one pass over X where rows span few column
+            # tiles (K <= 1024: config 2 -15 us, config 4 -6 us per iteration;
+            # at config 3's 16 column tiles the gain is within noise)
+            xn_env = os.environ.get("FK_ASSIGN_XNORM", "auto")
             self._xn = ops.assign_row_norms(self.x, K) if (
-                self._fold is not None and os.environ.get("FK_ASSIGN_XNORM", "1") != "0") else None
+                self._fold is not None and xn_env != "0" and (K <= 1024 or xn_env == "1")) else None
             if self.dtype in LOW_PRECISION:
                 kpad = ops.N.lib().fk_assign_bias_rows(K)
                 self.bias = [torch.zeros((B, kpad, 16), dtype=torch.bfloat16, device=dev) for _ in range(2)]
