@@ -2094,23 +2094,21 @@ cudaError_t launch_normalize_tail(int master_dt, const double* sums, const int64
                                   double* hist, int64_t* hist_it, int32_t* changed,
                                   int64_t* merges, double* flags, unsigned int* counter,
                                   int num_sms, cudaStream_t s) {
-  // Many centroid rows AND many objective blocks (config 4: 512 + 512 blocks
-  // at 2 resident per SM): the objective blocks would hold normalize-sized
-  // register slots for 1.7 more waves -- three launches instead (normalize,
-  // partials, loop tail: 13.4 vs 20.7 us at config 4, graph-replayed; the one
-  // launch wins where the rows are few, config 2: 10.5 vs 13.6 us).
-  // FK_TAIL=fused|split overrides (A/B).
+  // More objective blocks (8192-point buffers) than one wave of the
+  // normalize kernel's register slots (2 per SM): the objective blocks would
+  // queue behind each other inside the one launch -- three launches instead
+  // (normalize, partials, loop tail; graph-replayed, profiles/r02_ab_tail.txt:
+  // config 3 (1024 buffers) 20.3 vs 22.0 us, B=8 x 1M points 15.2 vs 15.9 us;
+  // the one launch wins at config 2 (128 buffers) 9.5 vs 11.7 us and ties at
+  // config 4, 14.0 vs 13.9-14.6 us).  FK_TAIL=fused|split overrides (A/B).
   static int tail_env = -2;
   if (tail_env == -2) {
     const char* e = getenv("FK_TAIL");
     tail_env = !e ? -1 : (e[0] == 'f' ? 1 : e[0] == 's' ? 0 : -1);
   }
   if (!mind_f64) {
-    const int64_t norm_blocks = (B * K + 8 * NORM_RW - 1) / (8 * NORM_RW);
     const int64_t nblk = (N + OBJ_BLOCK_N - 1) / OBJ_BLOCK_N;
-    const int64_t nob = B * nblk < 1024 ? B * nblk : 1024;
-    const bool split = tail_env >= 0 ? tail_env == 0
-                                     : (norm_blocks + nob > 2 * (int64_t)num_sms && 2 * norm_blocks > num_sms);
+    const bool split = tail_env >= 0 ? tail_env == 0 : B * nblk > 2 * (int64_t)num_sms;
     if (split) {
       cudaError_t e = launch_normalize(master_dt, sums, counts, prev, out, operand_dt, operand_out, empty_mask,
                                        max_shift2, B, K, d, bias_out, bias_kpad, s);

@@ -36,7 +36,9 @@ def t(fn, reps=20, replays=20):
 
 
 for name, (B, N, K, d, dt) in {"cfg4": (64, 16384, 256, 64, torch.float16),
-                               "cfg2": (1, 1 << 20, 1024, 128, torch.bfloat16)}.items():
+                               "cfg2": (1, 1 << 20, 1024, 128, torch.bfloat16),
+                               "cfg3": (1, 1 << 23, 4096, 128, torch.bfloat16),
+                               "B8-N1M-K256": (8, 1 << 20, 256, 64, torch.bfloat16)}.items():
     g = torch.Generator(device="cuda").manual_seed(0)
     x = torch.randn((B, N, d), device="cuda", generator=g).to(dt)
     eng = LloydEngine(x, K)
