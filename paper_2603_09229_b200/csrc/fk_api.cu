@@ -444,7 +444,7 @@ fk_status fk_update_hist_slots(fk_dtype dt, int64_t B, int64_t N, int64_t K, int
   if (!valid_dt(dt) || !shape_ok(B, N, K, d) || !ws || !hist_table || !hist_inval || !hist_bpb ||
       !hist_per || !clear_words)
     return FK_EINVAL;
-  if (!is_lowp(dt)) return FK_EUNSUPPORTED;
+  if (!is_lowp(dt) || !fk::assign_tc_supported(d)) return FK_EUNSUPPORTED;  // no tensor-core assign to fold into
   return fk::update_hist_slots(dt, B, N, K, d, dev_info().sms, ws, hist_table, hist_inval, hist_bpb,
                                hist_per, clear_words)
              ? FK_OK

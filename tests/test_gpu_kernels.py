@@ -417,6 +417,28 @@ def test_hist_fold_offered_where_supported(ops):
     assert ops.hist_fold(x, 16) is not None
     assert ops.hist_fold(x.float(), 16) is None       # f32 data: the certified path, no fold
     assert ops.hist_fold(x, 20_000) is None           # K beyond the warp-table scatter
+    x20 = torch.zeros((1, 1000, 20), dtype=torch.bfloat16, device="cuda")
+    assert ops.hist_fold(x20, 16) is None             # d = 20: the CUDA-core assign, nothing to fold into
+
+
+def test_engine_without_tensor_core_path_runs(ops):
+    """bf16 with d = 20 (rows not 16-byte multiples): no fold, no precomputed
+    norms; the pipelined run still equals the stepwise loop."""
+    from paper_2603_09229_b200 import LloydEngine
+
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = (torch.randn((2, 3000, 20), device="cuda", generator=g) * 3).to(torch.bfloat16)
+    eng = LloydEngine(x, 12)
+    assert eng._fold is None and eng._xn is None
+    eng.set_centroids(x[:, :12].float())
+    ref = LloydEngine(x, 12)
+    ref.set_centroids(x[:, :12].float())
+    its, slot, _ = eng.run(3, -1.0, stop_on_repeat=False)
+    for _ in range(3):
+        sb = ref.iterate()
+        ref.poll()
+        ref.commit()
+    assert torch.equal(eng.centroids, ref.centroids) and torch.equal(eng.ids[slot], ref.ids[sb])
 
 
 @pytest.mark.parametrize("B,N,K,d,dtype", [
