@@ -68,6 +68,7 @@ struct TcArgs {
   int32_t* changed;
   int debug_mode;  // 0 normal; 1 epilogue skips math (MMA/TMA bound); 2 MMA skipped (epilogue bound)
   int epi2;        // 1: bias-in-GEMM epilogue processes 32-column chunks in pairs
+  int a_early;     // 1: the X slot is released right after the row tile's last data MMA
   unsigned long long* trace;  // debug timeline (FK_ASSIGN_TRACE), nullptr normally
   // split (f32/f64 data, fk_assign_split.cu): X and C are bf16 [hi | lo] rows
   // of 2*ns K=16 steps; the MMA runs hi.hi + hi.lo + lo.hi per step and the
@@ -446,11 +447,12 @@ constexpr int THREADS = 384;
 constexpr int KATOMS_MAX = 4;                               // d <= 256
 static_assert(2 * KATOMS_MAX * A_ATOM + 4 * B_STAGE <= OPS_BYTES, "d = 256 plan does not fit");
 static_assert(2 * 2 * A_ATOM + STAGES * B_STAGE <= OPS_BYTES, "d = 128 plan does not fit");
+static_assert(8 * A_ATOM + 4 * B_STAGE <= OPS_BYTES, "d = 64 plan does not fit");
 // (X slots, C stages) per K-atom count: deep X prefetch for short rows,
 // deep C prefetch otherwise, at least one column tile of C for d = 256.
 __host__ __device__ inline void operand_plan(int katoms, int& a_slots, int& b_stages) {
   if (katoms == 1) {
-    a_slots = 6;
+    a_slots = 8;  // 8 x 16 KB: X prefetch deep enough for short row tiles (config 4)
     b_stages = 4;
   } else if (katoms == 4) {
     a_slots = 2;
@@ -637,7 +639,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     if (AUG) tma_prefetch_desc(&tmext);
     for (int s = 0; s < A_SLOTS_MAX; ++s) {
       mbar_init(&a_full[s], 1);       // leader's expect_tx (both CTAs' bytes)
-      mbar_init(&a_empty[s], 1 + (ALT ? 4 : 8));  // pair-MMA commit + the row-norm warps
+      // pair-MMA commit + the row-norm warps (none with precomputed norms: the
+      // slot is free as soon as the MMA has read it)
+      mbar_init(&a_empty[s], 1 + ((!SPLIT && p.xn_in) ? 0 : (ALT ? 4 : 8)));
     }
     for (int s = 0; s < NBUF; ++s) {
       mbar_init(&t_full[s], 1);
@@ -682,12 +686,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       for (int t = pair; t < p.total_tiles; t += npairs) {
         const int b = t / p.tiles_per_batch;
         for (int c = 0; c < p.ncol; ++c, ++g) {
+          // debug mode 4 (bound analysis, wrong results): C and bias operands
+          // loaded once per ring slot, then reused as they are
+          // (5: the bias operand only, 6: C only)
+          const bool warm4 = g >= (uint32_t)(EXT_SLOTS + b_stages);
+          const bool skip4 = warm4 && (p.debug_mode == 4 || p.debug_mode == 6);
+          const bool skipx = warm4 && (p.debug_mode == 4 || p.debug_mode == 5);
           if (AUG) {
             const uint32_t slot = g % EXT_SLOTS;
             mbar_wait(&ext_empty[slot], ((g / EXT_SLOTS) & 1) ^ 1);
-            if (leader) mbar_arrive_expect_tx(&ext_full[slot], 2 * EXT_SLOT);
-            tma_load_3d_cg2(sExt + slot * EXT_SLOT, &tmext, mapa_shared(smem_u32(&ext_full[slot]), 0),
-                            0, c * BN + rank * BNH, b, kEvictLast);
+            if (skipx) {
+              if (leader) mbar_arrive(&ext_full[slot]);
+            } else {
+              if (leader) mbar_arrive_expect_tx(&ext_full[slot], 2 * EXT_SLOT);
+              tma_load_3d_cg2(sExt + slot * EXT_SLOT, &tmext, mapa_shared(smem_u32(&ext_full[slot]), 0),
+                              0, c * BN + rank * BNH, b, kEvictLast);
+            }
           } else {
             const uint32_t slot = g % CN_SLOTS;
             mbar_wait(&cn_empty[slot], ((g / CN_SLOTS) & 1) ^ 1);
@@ -697,15 +711,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           }
           for (int ka = 0; ka < p.katoms; ++ka) {
             mbar_wait(&b_empty[stage], sphase ^ 1);
-            if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * B_STAGE);
-            tma_load_3d_cg2(sB + stage * B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
-                            ka * 64, c * BN + rank * BNH, b, kEvictLast);
+            if (skip4) {
+              if (leader) mbar_arrive(&b_full[stage]);
+            } else {
+              if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * B_STAGE);
+              tma_load_3d_cg2(sB + stage * B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
+                              ka * 64, c * BN + rank * BNH, b, kEvictLast);
+            }
             if (++stage == b_stages) {
               stage = 0;
               sphase ^= 1;
             }
           }
-          if (pair == 0 && leader) trace_ev(p, g, 5);
+          if (pair == 0 && leader && p.debug_mode != 3) trace_ev(p, g, 5);
         }
       }
     }
@@ -719,6 +737,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         const int b = t / p.tiles_per_batch;
         const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
         mbar_wait(&a_empty[slot], ((j / a_slots) & 1) ^ 1);
+        // debug mode 3: event 5 records when this row tile's X load is issued
+        if (p.debug_mode == 3 && pair == 0 && leader) trace_ev(p, (uint32_t)(j * p.ncol), 5);
         if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
         const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
         for (int ka = 0; ka < p.katoms; ++ka)
@@ -781,6 +801,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                                  SEED || (ka | k) != 0);
               }
               tc_commit_cg2_mc(&b_empty[stage], 0x3);
+              // the row tile's last read of its X slot: release it now, ahead
+              // of the bias step and the accumulator commit (FK_ASSIGN_AEARLY=0:
+              // after them, A/B)
+              if (p.a_early && c == p.ncol - 1 && ka == p.katoms - 1) tc_commit_cg2_mc(&a_empty[slot], 0x3);
             }
             __syncwarp();
             if (++stage == b_stages) {
@@ -803,8 +827,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           __syncwarp();
           if (pair == 0 && lane == 0) trace_ev(p, g, 1);
         }
-        if (elect_one()) tc_commit_cg2_mc(&a_empty[slot], 0x3);
-        __syncwarp();
+        if (!p.a_early) {
+          if (elect_one()) tc_commit_cg2_mc(&a_empty[slot], 0x3);
+          __syncwarp();
+        }
       }
     }
   } else if (warp < 8) {
@@ -919,7 +945,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                                           4 * wg + 4);
           }
           __syncwarp();
-          if (lane == 0) mbar_arrive(&a_empty[slot]);
+          if (lane == 0 && (SPLIT || !p.xn_in)) mbar_arrive(&a_empty[slot]);
         }
         uint32_t cnp = 0;
         if (EPI) {
@@ -1312,6 +1338,8 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     // 2 and 4) and cost ~3% at K = 4096 (same-box A/B, profiles/r01_ab_epi2.txt)
     const char* e2 = getenv("FK_ASSIGN_EPI2");
     a.epi2 = e2 ? (e2[0] == '1') : (a.ncol <= 4);
+    const char* ae = getenv("FK_ASSIGN_AEARLY");
+    a.a_early = ae ? (ae[0] == '1') : 1;
   }
   a.trace = nullptr;
   a.ns = 0;
@@ -1412,6 +1440,8 @@ cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* e
     a.debug_mode = dm ? atoi(dm) : 0;
     const char* e2 = getenv("FK_ASSIGN_EPI2");
     a.epi2 = e2 ? (e2[0] == '1') : (a.ncol <= 4);
+    const char* ae = getenv("FK_ASSIGN_AEARLY");
+    a.a_early = ae ? (ae[0] == '1') : 1;
   }
   a.trace = nullptr;
   a.ns = ns;

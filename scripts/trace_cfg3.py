@@ -1,5 +1,5 @@
 """In-kernel timeline of one config-3 FlashAssign (FK_ASSIGN_TRACE), plain and with the
-engine's histogram fold + precomputed row norms (dev aid).  usage: python scripts/trace_cfg3.py"""
+engine's histogram fold + precomputed row norms (dev aid).  usage: python scripts/trace_cfg3.py [B N K d]"""
 import os
 import subprocess
 import sys
@@ -9,7 +9,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2603_09229_b200 import ops  # noqa: E402
 
-B, N, K, d = 1, 1 << 23, 4096, 128
+B, N, K, d = (int(v) for v in sys.argv[1:5]) if len(sys.argv) > 4 else (1, 1 << 23, 4096, 128)
 g = torch.Generator(device="cuda").manual_seed(0)
 x = torch.randn((B, N, d), device="cuda", generator=g).to(torch.bfloat16)
 c = x[:, torch.randperm(N, device="cuda", generator=g)[:K]].contiguous()
