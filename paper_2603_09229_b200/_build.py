@@ -60,6 +60,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     def compile_one(src):
         obj = os.path.join(OUT_DIR, os.path.basename(src)[:-3] + ".o")
         cmd = [cc, *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj]
+        if os.environ.get("FK_BUILD_TRACE") == "1":  # in-kernel timeline build (FK_ASSIGN_TRACE)
+            cmd.insert(-4, "-DFK_ASSIGN_TRACE_BUILD")
+        if os.environ.get("FK_BUILD_DEBUG") == "1":  # bound-analysis modes (FK_ASSIGN_DEBUG_MODE)
+            cmd.insert(-4, "-DFK_ASSIGN_DEBUG_BUILD")
         if verbose:
             cmd += ["-Xptxas", "-v"]
         r = subprocess.run(cmd, capture_output=True, text=True)

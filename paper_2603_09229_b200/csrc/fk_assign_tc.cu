@@ -68,7 +68,6 @@ struct TcArgs {
   int32_t* changed;
   int debug_mode;  // 0 normal; 1 epilogue skips math (MMA/TMA bound); 2 MMA skipped (epilogue bound)
   int epi2;        // 1: bias-in-GEMM epilogue processes 32-column chunks in pairs
-  int a_early;     // 1: the X slot is released right after the row tile's last data MMA
   unsigned long long* trace;  // debug timeline (FK_ASSIGN_TRACE), nullptr normally
   // split (f32/f64 data, fk_assign_split.cu): X and C are bf16 [hi | lo] rows
   // of 2*ns K=16 steps; the MMA runs hi.hi + hi.lo + lo.hi per step and the
@@ -103,9 +102,26 @@ static_assert(FK_SPLIT_REC == kSplitRecInts, "candidate record layout (fk_kernel
 
 // Debug timeline: events of pair 0 / tile window [TR_G0, TR_G0 + TR_N) only.
 constexpr int TR_G0 = 16, TR_N = 32, TR_EV = 8;
+// Bound-analysis modes (FK_ASSIGN_DEBUG_MODE) exist only in debug builds
+// (FK_BUILD_DEBUG=1 -> -DFK_ASSIGN_DEBUG_BUILD); elsewhere the mode is the
+// constant 0 and every check folds away.
+#ifdef FK_ASSIGN_DEBUG_BUILD
+FK_DEV int dbg_mode(const TcArgs& p) { return p.debug_mode; }
+#else
+FK_DEV constexpr int dbg_mode(const TcArgs&) { return 0; }
+#endif
+
+// Compiled in only for timeline builds (FK_BUILD_TRACE=1 -> -DFK_ASSIGN_TRACE_BUILD):
+// the role warps share their SM sub-partitions with ALU-bound epilogue warps,
+// so every instruction on the MMA warp's per-tile path costs issue slots it
+// waits for (the checks alone were ~20 instructions per tile).
+#ifdef FK_ASSIGN_TRACE_BUILD
 FK_DEV void trace_ev(const TcArgs& p, uint32_t g, int ev) {
   if (p.trace && g >= TR_G0 && g < TR_G0 + TR_N) p.trace[(g - TR_G0) * TR_EV + ev] = clock64();
 }
+#else
+FK_DEV void trace_ev(const TcArgs&, uint32_t, int) {}
+#endif
 
 // ||x||^2 of one row of the staged X tile over the 16-byte chunk positions
 // [j0, j1) of every K atom (the caller may split the 8 positions between
@@ -291,7 +307,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             tc_fence_after();
             const uint32_t aa = a_base + ka * tc::A_ATOM;
             const uint32_t bb = smem_u32(sB + stage * tc::B_STAGE);
-            if (p.debug_mode != 2) {
+            if (dbg_mode(p) != 2) {
 #pragma unroll
               for (int k = 0; k < 4; ++k)
                 tc_mma_f16(d_tmem, make_sdesc_sw128(aa + k * 32), make_sdesc_sw128(bb + k * 32),
@@ -342,7 +358,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         mbar_wait(&cn_full[cslot], (g / tc::CN_SLOTS) & 1);
         const uint32_t cnp = smem_u32(sCN + cslot * tc::BN + wg * 128);
         const int col0 = c * tc::BN + wg * 128;
-        if (p.debug_mode == 1) {
+        if (dbg_mode(p) == 1) {
           FK_TMEM_WAIT_LD(va);
           tc_fence_before();
           __syncwarp();
@@ -690,8 +706,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           // loaded once per ring slot, then reused as they are
           // (5: the bias operand only, 6: C only)
           const bool warm4 = g >= (uint32_t)(EXT_SLOTS + b_stages);
-          const bool skip4 = warm4 && (p.debug_mode == 4 || p.debug_mode == 6);
-          const bool skipx = warm4 && (p.debug_mode == 4 || p.debug_mode == 5);
+          const bool skip4 = warm4 && (dbg_mode(p) == 4 || dbg_mode(p) == 6);
+          const bool skipx = warm4 && (dbg_mode(p) == 4 || dbg_mode(p) == 5);
           if (AUG) {
             const uint32_t slot = g % EXT_SLOTS;
             mbar_wait(&ext_empty[slot], ((g / EXT_SLOTS) & 1) ^ 1);
@@ -723,7 +739,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               sphase ^= 1;
             }
           }
-          if (pair == 0 && leader && p.debug_mode != 3) trace_ev(p, g, 5);
+          if (pair == 0 && leader && dbg_mode(p) != 3) trace_ev(p, g, 5);
         }
       }
     }
@@ -731,14 +747,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     // ------------------------------------------------------------ X row-tile producer (both CTAs)
     if (lane == 0) {
       const uint32_t a_bytes = p.katoms * A_ATOM;
-      int j = 0;
+      int j = 0, aslot = 0;
+      uint32_t aphase = 0;
       for (int t = pair; t < p.total_tiles; t += npairs, ++j) {
-        const int slot = j % a_slots;
+        const int slot = aslot;  // j % a_slots, without a division per tile
+        const uint32_t aph = aphase;
+        if (++aslot == a_slots) {
+          aslot = 0;
+          aphase ^= 1;
+        }
         const int b = t / p.tiles_per_batch;
         const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
-        mbar_wait(&a_empty[slot], ((j / a_slots) & 1) ^ 1);
+        mbar_wait(&a_empty[slot], aph ^ 1);
         // debug mode 3: event 5 records when this row tile's X load is issued
-        if (p.debug_mode == 3 && pair == 0 && leader) trace_ev(p, (uint32_t)(j * p.ncol), 5);
+        if (dbg_mode(p) == 3 && pair == 0 && leader) trace_ev(p, (uint32_t)(j * p.ncol), 5);
+        if (dbg_mode(p) == 7 && j >= a_slots) {  // bound analysis: X tiles loaded once per slot
+          if (leader) mbar_arrive(&a_full[slot]);
+          continue;
+        }
         if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
         const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
         for (int ka = 0; ka < p.katoms; ++ka)
@@ -756,10 +782,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       const uint32_t idesc_ext = make_idesc_f16(1, 2 * BM, BN);
       const uint64_t aext_desc = make_sdesc_sw32(smem_u32(sAext));
       uint32_t stage = 0, sphase = 0, g = 0;
-      int i = 0;
-      for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
-        const int slot = i % a_slots;
-        mbar_wait(&a_full[slot], (i / a_slots) & 1);
+      int aslot = 0;
+      uint32_t aphase = 0;
+      for (int t = pair; t < p.total_tiles; t += npairs) {
+        const int slot = aslot;  // i % a_slots, without a division per tile
+        const uint32_t aph = aphase;
+        if (++aslot == a_slots) {
+          aslot = 0;
+          aphase ^= 1;
+        }
+        mbar_wait(&a_full[slot], aph);
         tc_fence_after();
         if (pair == 0 && lane == 0) trace_ev(p, g, 7);
         const uint32_t a_base = smem_u32(sA + slot * a_slot_bytes);
@@ -783,7 +815,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                   const int sc = 4 * ka + k;
-                  if (sc < 2 * p.ns && p.debug_mode != 2) {
+                  if (sc < 2 * p.ns && dbg_mode(p) != 2) {
                     const int sa = sc < p.ns ? sc : sc - p.ns;
                     const uint64_t ad = make_sdesc_sw128(a_base + (sa >> 2) * A_ATOM) + 2 * (sa & 3);
                     tc_mma_f16_cg2(d_tmem, ad, bdesc + 2 * k, idesc_main, sc != 0);
@@ -794,7 +826,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                     }
                   }
                 }
-              } else if (p.debug_mode != 2) {
+              } else if (dbg_mode(p) != 2) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)  // +32 B along K = +2 in the descriptor's address field
                   tc_mma_f16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc_main,
@@ -802,9 +834,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               }
               tc_commit_cg2_mc(&b_empty[stage], 0x3);
               // the row tile's last read of its X slot: release it now, ahead
-              // of the bias step and the accumulator commit (FK_ASSIGN_AEARLY=0:
-              // after them, A/B)
-              if (p.a_early && c == p.ncol - 1 && ka == p.katoms - 1) tc_commit_cg2_mc(&a_empty[slot], 0x3);
+              // of the bias step and the accumulator commit
+              if (c == p.ncol - 1 && ka == p.katoms - 1) tc_commit_cg2_mc(&a_empty[slot], 0x3);
             }
             __syncwarp();
             if (++stage == b_stages) {
@@ -818,7 +849,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             tc_fence_after();
             const uint64_t edesc = make_sdesc_sw32(smem_u32(sExt + es * EXT_SLOT));
             if (elect_one()) {
-              tc_mma_f16_cg2(d_tmem, aext_desc, edesc, idesc_ext, p.debug_mode != 2 ? 1u : 0u);
+              tc_mma_f16_cg2(d_tmem, aext_desc, edesc, idesc_ext, dbg_mode(p) != 2 ? 1u : 0u);
               tc_commit_cg2_mc(&ext_empty[es], 0x3);
             }
             __syncwarp();
@@ -826,10 +857,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           if (elect_one()) tc_commit_cg2_mc(&t_full[buf], 0x3);
           __syncwarp();
           if (pair == 0 && lane == 0) trace_ev(p, g, 1);
-        }
-        if (!p.a_early) {
-          if (elect_one()) tc_commit_cg2_mc(&a_empty[slot], 0x3);
-          __syncwarp();
         }
       }
     }
@@ -877,7 +904,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         if (!alt || (int)(g0 & 1) == wg) seed_and_release(g0);
     }
     uint32_t g = 0;
-    int i = 0;
+    int i = 0, aslot = 0;
     // (batch, tile-in-batch) of t, advanced without a division per tile
     int tb = pair / p.tiles_per_batch, tr_ = pair - tb * p.tiles_per_batch;
     const int step_b = npairs / p.tiles_per_batch, step_r = npairs - step_b * p.tiles_per_batch;
@@ -889,12 +916,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         tr_ -= p.tiles_per_batch;
         ++tb;
       }
+      const int slot = aslot;  // i % a_slots, without a division per tile
+      if (++aslot == a_slots) aslot = 0;
       if (alt && (i & 1) != wg) {  // the other warpgroup owns this tile
         ++g;
         continue;
       }
       const int row0 = trow * (2 * BM) + rank * BM;
-      const int slot = i % a_slots;
       // previous assignment of this row, loaded now so its HBM latency overlaps
       // the row tile's chunks instead of sitting at the end of the tile
       int prev_id = -2;
@@ -990,7 +1018,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           } else
             epi_chunk(v, cnp + 128 * ch, col0 + 32 * ch, M, best, bestv);
         };
-        if (p.debug_mode == 1) {
+        if (dbg_mode(p) == 1) {
           FK_TMEM_WAIT_LD(va);
           release_tmem();  // (debug mode 1 does not support SEED: garbage accumulators are fine for timing)
           if (EPI && lane == 0) mbar_arrive(&cn_empty[cslot]);
@@ -1338,8 +1366,6 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
     // 2 and 4) and cost ~3% at K = 4096 (same-box A/B, profiles/r01_ab_epi2.txt)
     const char* e2 = getenv("FK_ASSIGN_EPI2");
     a.epi2 = e2 ? (e2[0] == '1') : (a.ncol <= 4);
-    const char* ae = getenv("FK_ASSIGN_AEARLY");
-    a.a_early = ae ? (ae[0] == '1') : 1;
   }
   a.trace = nullptr;
   a.ns = 0;
@@ -1440,8 +1466,6 @@ cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* e
     a.debug_mode = dm ? atoi(dm) : 0;
     const char* e2 = getenv("FK_ASSIGN_EPI2");
     a.epi2 = e2 ? (e2[0] == '1') : (a.ncol <= 4);
-    const char* ae = getenv("FK_ASSIGN_AEARLY");
-    a.a_early = ae ? (ae[0] == '1') : 1;
   }
   a.trace = nullptr;
   a.ns = ns;
