@@ -4,7 +4,7 @@
 # (paper_2603_09229_b200/_lib/ab/libfk_withtrace.so via FK_LIB_PATH); tests first.
 cd "$(dirname "$0")/.."
 python -m pytest -q -x tests/test_gpu_kernels.py tests/test_gpu_split.py tests/test_gpu_api.py tests/test_gpu_edges.py 2>&1 | tail -1
-OLD=paper_2603_09229_b200/_lib/ab/libfk_withtrace.so
+OLD=${OLD:-paper_2603_09229_b200/_lib/ab/libfk_withtrace.so}
 for i in 1 2; do
   for lib in new old; do
     if [ $lib = old ]; then export FK_LIB_PATH=$OLD; else unset FK_LIB_PATH; fi
