@@ -696,7 +696,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     // ------------------------------------------------------------ producer (both CTAs)
     // C tiles (+ bias operand / ||c||^2 ring); X row tiles come from their own
     // warp below, so waiting for a free X slot never stalls the C prefetch.
-    if (lane == 0) {
+    // The whole warp runs the loop (barrier and index arithmetic on the uniform
+    // datapath, which the ALU-bound epilogue warps of this sub-partition do not
+    // contend for); one elected lane issues each copy.
+    {
       uint32_t stage = 0, sphase = 0;
       uint32_t g = 0;
       for (int t = pair; t < p.total_tiles; t += npairs) {
@@ -711,41 +714,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           if (AUG) {
             const uint32_t slot = g % EXT_SLOTS;
             mbar_wait(&ext_empty[slot], ((g / EXT_SLOTS) & 1) ^ 1);
-            if (skipx) {
-              if (leader) mbar_arrive(&ext_full[slot]);
-            } else {
-              if (leader) mbar_arrive_expect_tx(&ext_full[slot], 2 * EXT_SLOT);
-              tma_load_3d_cg2(sExt + slot * EXT_SLOT, &tmext, mapa_shared(smem_u32(&ext_full[slot]), 0),
-                              0, c * BN + rank * BNH, b, kEvictLast);
+            if (elect_one()) {
+              if (skipx) {
+                if (leader) mbar_arrive(&ext_full[slot]);
+              } else {
+                if (leader) mbar_arrive_expect_tx(&ext_full[slot], 2 * EXT_SLOT);
+                tma_load_3d_cg2(sExt + slot * EXT_SLOT, &tmext, mapa_shared(smem_u32(&ext_full[slot]), 0),
+                                0, c * BN + rank * BNH, b, kEvictLast);
+              }
             }
+            __syncwarp();
           } else {
             const uint32_t slot = g % CN_SLOTS;
             mbar_wait(&cn_empty[slot], ((g / CN_SLOTS) & 1) ^ 1);
-            mbar_arrive_expect_tx(&cn_full[slot], BN * 4);
-            bulk_load(sCN + slot * BN, p.cn + (size_t)b * p.kpad + (size_t)c * BN, BN * 4,
-                      &cn_full[slot]);
+            if (elect_one()) {
+              mbar_arrive_expect_tx(&cn_full[slot], BN * 4);
+              bulk_load(sCN + slot * BN, p.cn + (size_t)b * p.kpad + (size_t)c * BN, BN * 4,
+                        &cn_full[slot]);
+            }
+            __syncwarp();
           }
           for (int ka = 0; ka < p.katoms; ++ka) {
             mbar_wait(&b_empty[stage], sphase ^ 1);
-            if (skip4) {
-              if (leader) mbar_arrive(&b_full[stage]);
-            } else {
-              if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * B_STAGE);
-              tma_load_3d_cg2(sB + stage * B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
-                              ka * 64, c * BN + rank * BNH, b, kEvictLast);
+            if (elect_one()) {
+              if (skip4) {
+                if (leader) mbar_arrive(&b_full[stage]);
+              } else {
+                if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * B_STAGE);
+                tma_load_3d_cg2(sB + stage * B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
+                                ka * 64, c * BN + rank * BNH, b, kEvictLast);
+              }
             }
+            __syncwarp();
             if (++stage == b_stages) {
               stage = 0;
               sphase ^= 1;
             }
           }
-          if (pair == 0 && leader && dbg_mode(p) != 3) trace_ev(p, g, 5);
+          if (pair == 0 && leader && lane == 0 && dbg_mode(p) != 3) trace_ev(p, g, 5);
         }
       }
     }
   } else if (warp == W_INIT) {
     // ------------------------------------------------------------ X row-tile producer (both CTAs)
-    if (lane == 0) {
+    // (warp-wide loop, elected issue: as the C producer above)
+    {
       const uint32_t a_bytes = p.katoms * A_ATOM;
       int j = 0, aslot = 0;
       uint32_t aphase = 0;
@@ -760,16 +773,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
         mbar_wait(&a_empty[slot], aph ^ 1);
         // debug mode 3: event 5 records when this row tile's X load is issued
-        if (dbg_mode(p) == 3 && pair == 0 && leader) trace_ev(p, (uint32_t)(j * p.ncol), 5);
+        if (dbg_mode(p) == 3 && pair == 0 && leader && lane == 0) trace_ev(p, (uint32_t)(j * p.ncol), 5);
         if (dbg_mode(p) == 7 && j >= a_slots) {  // bound analysis: X tiles loaded once per slot
-          if (leader) mbar_arrive(&a_full[slot]);
+          if (elect_one() && leader) mbar_arrive(&a_full[slot]);
+          __syncwarp();
           continue;
         }
-        if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
-        const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
-        for (int ka = 0; ka < p.katoms; ++ka)
-          tma_load_3d_cg2(sA + slot * a_slot_bytes + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
-                          kEvictFirst);
+        if (elect_one()) {
+          if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
+          const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
+          for (int ka = 0; ka < p.katoms; ++ka)
+            tma_load_3d_cg2(sA + slot * a_slot_bytes + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
+                            kEvictFirst);
+        }
+        __syncwarp();
       }
     }
   } else if (warp == W_MMA) {
