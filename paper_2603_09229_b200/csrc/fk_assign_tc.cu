@@ -94,6 +94,9 @@ struct TcArgs {
   // arithmetic (X is fixed through a Lloyd run): loaded instead of summing the
   // row from the shared-memory tile every row tile; nullptr: summed here
   const float* xn_in;
+  // first row tile of this launch (the pair kernel beside the multicast quads
+  // takes the tiles after theirs); 0 otherwise
+  int tile0;
 };
 
 constexpr int SPLIT_NREC = 4;                  // near chunks kept per thread (per column half)
@@ -586,12 +589,16 @@ FK_DEV float split_norm_ub(const uint8_t* a_slot, int row, int katoms, int ns, i
 //              accumulate onto the seed.  No extra MMA step, no fp16 range
 //              issue, still a pure min-reduction epilogue.
 // BIAS = 0 (epilogue bias): bias added in the epilogue from a smem ring.
-template <int FMT, int BIAS, bool ALT, bool SPLIT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
-    fk_assign_tc2_kernel(const __grid_constant__ CUtensorMap tmx,
-                         const __grid_constant__ CUtensorMap tmc,
-                         const __grid_constant__ CUtensorMap tmext, const TcArgs p) {
+// MC (fk_assign_tc2q_kernel): a cluster of two CTA pairs that take the two
+//              row tiles of a tile pair in lockstep and share every C tile:
+//              each CTA loads half of its half-tile and multicasts it to the
+//              CTA of the same pair rank in the other pair, so C crosses L2
+//              once per two row tiles (B = 1, bias in the GEMM, K > 256).
+template <int FMT, int BIAS, bool ALT, bool SPLIT, bool MC>
+FK_DEV void assign_tc2_body(const CUtensorMap& tmx, const CUtensorMap& tmc,
+                            const CUtensorMap& tmext, const TcArgs& p) {
   using namespace tc2;
+  static_assert(!MC || (BIAS == 1 && !ALT && !SPLIT), "multicast pairs: bias in the GEMM only");
   constexpr bool AUG = BIAS == 1;   // bias as an extra MMA step
   constexpr bool SEED = BIAS == 2;  // bias seeded into TMEM by the epilogue
   constexpr bool EPI = BIAS == 0;   // bias added in the epilogue
@@ -630,10 +637,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   constexpr int W_PRODUCER = 8, W_MMA = 9, W_TMEM = 10, W_INIT = 11;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = MC ? (crank & 1u) : crank;  // rank within the pair
+  const uint32_t lead = MC ? (crank & 2u) : 0u;     // cluster rank of the pair's leader
+  const uint16_t pmask = (uint16_t)(0x3u << lead);  // this pair's two CTAs
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1;
   const int npairs = gridDim.x >> 1;
+  // row tiles of this pair: t_first, t_first + t_step, ... < t_end.  MC: the
+  // quad's pairs take tiles 2v and 2v + 1 of the same tile pair v, so t_end is
+  // rounded up to even and a pair may run one dummy tile (loads the last real
+  // tile, writes nothing) to keep the shared C stream in step.
+  const int t_first = MC ? 2 * (int)(blockIdx.x >> 2) + (int)(crank >> 1) : pair;
+  const int t_step = MC ? 2 * (int)(gridDim.x >> 2) : npairs;
+  const int t_end = MC ? ((p.total_tiles + 1) & ~1) : p.total_tiles;
   // X row-tile ring: the 64 KB A region holds 2 slots of 2 K-atoms (d <= 128)
   // or 4 slots of 1 atom (d <= 64): deeper prefetch when a row tile is short.
   // X row-tile ring + C stage ring share the 160 KB operand region: d <= 64
@@ -665,7 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&b_full[s], 1);
-      mbar_init(&b_empty[s], 1);
+      mbar_init(&b_empty[s], MC ? 2 : 1);  // MC: both pairs' MMAs read the stage
     }
     for (int s = 0; s < CN_SLOTS; ++s) {
       mbar_init(&cn_full[s], 1);
@@ -702,8 +719,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     {
       uint32_t stage = 0, sphase = 0;
       uint32_t g = 0;
-      for (int t = pair; t < p.total_tiles; t += npairs) {
-        const int b = t / p.tiles_per_batch;
+      for (int t = t_first; t < t_end; t += t_step) {
+        const int b = MC ? 0 : (p.tile0 + t) / p.tiles_per_batch;
         for (int c = 0; c < p.ncol; ++c, ++g) {
           // debug mode 4 (bound analysis, wrong results): C and bias operands
           // loaded once per ring slot, then reused as they are
@@ -719,7 +736,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                 if (leader) mbar_arrive(&ext_full[slot]);
               } else {
                 if (leader) mbar_arrive_expect_tx(&ext_full[slot], 2 * EXT_SLOT);
-                tma_load_3d_cg2(sExt + slot * EXT_SLOT, &tmext, mapa_shared(smem_u32(&ext_full[slot]), 0),
+                tma_load_3d_cg2(sExt + slot * EXT_SLOT, &tmext, mapa_shared(smem_u32(&ext_full[slot]), lead),
                                 0, c * BN + rank * BNH, b, kEvictLast);
               }
             }
@@ -741,8 +758,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                 if (leader) mbar_arrive(&b_full[stage]);
               } else {
                 if (leader) mbar_arrive_expect_tx(&b_full[stage], 2 * B_STAGE);
-                tma_load_3d_cg2(sB + stage * B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
-                                ka * 64, c * BN + rank * BNH, b, kEvictLast);
+                if constexpr (MC) {  // half of the half-tile, to this CTA and its twin
+                  const uint32_t pq = crank >> 1;
+                  tma_load_3d_cg2_mc(sB + stage * B_STAGE + pq * (B_STAGE / 2), &tmc,
+                                     mapa_shared(smem_u32(&b_full[stage]), lead),
+                                     (uint16_t)(0x5u << rank), ka * 64,
+                                     c * BN + rank * BNH + pq * (BNH / 2), b, kEvictLast);
+                } else {
+                  tma_load_3d_cg2(sB + stage * B_STAGE, &tmc, mapa_shared(smem_u32(&b_full[stage]), 0),
+                                  ka * 64, c * BN + rank * BNH, b, kEvictLast);
+                }
               }
             }
             __syncwarp();
@@ -762,15 +787,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       const uint32_t a_bytes = p.katoms * A_ATOM;
       int j = 0, aslot = 0;
       uint32_t aphase = 0;
-      for (int t = pair; t < p.total_tiles; t += npairs, ++j) {
+      for (int t = t_first; t < t_end; t += t_step, ++j) {
         const int slot = aslot;  // j % a_slots, without a division per tile
         const uint32_t aph = aphase;
         if (++aslot == a_slots) {
           aslot = 0;
           aphase ^= 1;
         }
-        const int b = t / p.tiles_per_batch;
-        const int row0 = (t - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
+        const int tt = p.tile0 + ((MC && t >= p.total_tiles) ? p.total_tiles - 1 : t);  // MC dummy: last tile
+        const int b = MC ? 0 : tt / p.tiles_per_batch;
+        const int row0 = (tt - b * p.tiles_per_batch) * (2 * BM) + rank * BM;
         mbar_wait(&a_empty[slot], aph ^ 1);
         // debug mode 3: event 5 records when this row tile's X load is issued
         if (dbg_mode(p) == 3 && pair == 0 && leader && lane == 0) trace_ev(p, (uint32_t)(j * p.ncol), 5);
@@ -781,7 +807,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         }
         if (elect_one()) {
           if (leader) mbar_arrive_expect_tx(&a_full[slot], 2 * a_bytes);
-          const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), 0);
+          const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), lead);
           for (int ka = 0; ka < p.katoms; ++ka)
             tma_load_3d_cg2(sA + slot * a_slot_bytes + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
                             kEvictFirst);
@@ -801,7 +827,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       uint32_t stage = 0, sphase = 0, g = 0;
       int aslot = 0;
       uint32_t aphase = 0;
-      for (int t = pair; t < p.total_tiles; t += npairs) {
+      for (int t = t_first; t < t_end; t += t_step) {
         const int slot = aslot;  // i % a_slots, without a division per tile
         const uint32_t aph = aphase;
         if (++aslot == a_slots) {
@@ -849,10 +875,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                   tc_mma_f16_cg2(d_tmem, adesc + 2 * k, bdesc + 2 * k, idesc_main,
                                  SEED || (ka | k) != 0);
               }
-              tc_commit_cg2_mc(&b_empty[stage], 0x3);
+              tc_commit_cg2_mc(&b_empty[stage], MC ? (uint16_t)0xF : pmask);  // MC: both pairs' producers
               // the row tile's last read of its X slot: release it now, ahead
               // of the bias step and the accumulator commit
-              if (c == p.ncol - 1 && ka == p.katoms - 1) tc_commit_cg2_mc(&a_empty[slot], 0x3);
+              if (c == p.ncol - 1 && ka == p.katoms - 1) tc_commit_cg2_mc(&a_empty[slot], pmask);
             }
             __syncwarp();
             if (++stage == b_stages) {
@@ -867,11 +893,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             const uint64_t edesc = make_sdesc_sw32(smem_u32(sExt + es * EXT_SLOT));
             if (elect_one()) {
               tc_mma_f16_cg2(d_tmem, aext_desc, edesc, idesc_ext, dbg_mode(p) != 2 ? 1u : 0u);
-              tc_commit_cg2_mc(&ext_empty[es], 0x3);
+              tc_commit_cg2_mc(&ext_empty[es], pmask);
             }
             __syncwarp();
           }
-          if (elect_one()) tc_commit_cg2_mc(&t_full[buf], 0x3);
+          if (elect_one()) tc_commit_cg2_mc(&t_full[buf], pmask);
           __syncwarp();
           if (pair == 0 && lane == 0) trace_ev(p, g, 1);
         }
@@ -888,7 +914,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     auto seed_and_release = [&](uint32_t g2) __attribute__((always_inline)) {
       const uint32_t sbuf = g2 % NBUF;
       const int i2 = (int)(g2 / p.ncol);
-      if (pair + i2 * npairs < p.total_tiles && (!alt || (i2 & 1) == wg)) {
+      if (t_first + i2 * t_step < t_end && (!alt || (i2 & 1) == wg)) {
         const uint32_t cs = g2 % CN_SLOTS;
         mbar_wait(&cn_full[cs], (g2 / CN_SLOTS) & 1);
         const uint32_t src = smem_u32(sCN + cs * BN + (alt ? 0 : wg * (BN / 2)));
@@ -912,7 +938,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         if (leader)
           mbar_arrive(&t_empty[sbuf]);
         else
-          mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[sbuf]), 0));
+          mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[sbuf]), lead));
       }
     };
     if (SEED) {
@@ -923,10 +949,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     uint32_t g = 0;
     int i = 0, aslot = 0;
     // (batch, tile-in-batch) of t, advanced without a division per tile
-    int tb = pair / p.tiles_per_batch, tr_ = pair - tb * p.tiles_per_batch;
-    const int step_b = npairs / p.tiles_per_batch, step_r = npairs - step_b * p.tiles_per_batch;
-    for (int t = pair; t < p.total_tiles; t += npairs, ++i) {
-      const int b = tb, trow = tr_;
+    int tb = (p.tile0 + t_first) / p.tiles_per_batch, tr_ = p.tile0 + t_first - tb * p.tiles_per_batch;
+    const int step_b = t_step / p.tiles_per_batch, step_r = t_step - step_b * p.tiles_per_batch;
+    for (int t = t_first; t < t_end; t += t_step, ++i) {
+      const bool dummy = MC && t >= p.total_tiles;  // MC: keeps the C stream in step, writes nothing
+      const int b = MC ? 0 : tb, trow = tr_;
       tb += step_b;
       tr_ += step_r;
       if (tr_ >= p.tiles_per_batch) {
@@ -943,10 +970,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       // previous assignment of this row, loaded now so its HBM latency overlaps
       // the row tile's chunks instead of sitting at the end of the tile
       int prev_id = -2;
-      if (p.idx_prev && (alt || wg == 0) && row0 + row < p.N)
+      if (p.idx_prev && (alt || wg == 0) && !dummy && row0 + row < p.N)
         prev_id = __ldg(p.idx_prev + (size_t)b * p.N + row0 + row);
       float xn_pre = 0.f;  // the precomputed ||x||^2 (owner warpgroup; the other adds 0)
-      if (!SPLIT && p.xn_in && (alt || wg == 0) && row0 + row < p.N)
+      if (!SPLIT && p.xn_in && (alt || wg == 0) && !dummy && row0 + row < p.N)
         xn_pre = __ldg(p.xn_in + (size_t)b * p.N + row0 + row);
       float M = __int_as_float(0x7f800000);
       float m2 = M;  // split: lower bound on the row's second-best score
@@ -1005,7 +1032,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             if (leader)
               mbar_arrive(&t_empty[buf]);
             else
-              mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[buf]), 0));
+              mbar_arrive_cluster(mapa_shared(smem_u32(&t_empty[buf]), lead));
           }
         };
         // split: keep the chunk if its minimum is within the margin of the
@@ -1139,7 +1166,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       if (alt || wg == 0) {
         const int grow = row0 + row;
         bool ch = false;
-        if (grow < p.N) {
+        if (!dummy && grow < p.N) {
           const size_t o = (size_t)b * p.N + grow;
           p.idx_out[o] = idx;
           if (SPLIT) {  // raw scores: the certify pass decides and computes the distance
@@ -1201,6 +1228,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
   }
 }
 
+template <int FMT, int BIAS, bool ALT, bool SPLIT>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
+    fk_assign_tc2_kernel(const __grid_constant__ CUtensorMap tmx,
+                         const __grid_constant__ CUtensorMap tmc,
+                         const __grid_constant__ CUtensorMap tmext, const TcArgs p) {
+  assign_tc2_body<FMT, BIAS, ALT, SPLIT, false>(tmx, tmc, tmext, p);
+  // launched beside the multicast quads (programmatic dependent launch): do
+  // not complete before them, so stream order after this kernel covers both
+  // (a no-op for an ordinary launch)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Two CTA pairs per cluster sharing the C stream by multicast (see MC above).
+template <int FMT>
+__global__ void __cluster_dims__(4, 1, 1) __launch_bounds__(tc2::THREADS, 1)
+    fk_assign_tc2q_kernel(const __grid_constant__ CUtensorMap tmx,
+                          const __grid_constant__ CUtensorMap tmc,
+                          const __grid_constant__ CUtensorMap tmext, const TcArgs p) {
+  // every quad is resident from the start: release the pair kernel that
+  // takes the SMs the 4-CTA clusters cannot use
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  assign_tc2_body<FMT, 1, false, false, true>(tmx, tmc, tmext, p);
+}
+
 template <int FMT, int BIAS, bool ALT, bool SPLIT = false>
 static cudaError_t launch_pair_t(const CUtensorMap& tmx, const CUtensorMap& tmc,
                                  const CUtensorMap& tmext, TcArgs a, int pairs,
@@ -1216,6 +1267,104 @@ static cudaError_t launch_pair_t(const CUtensorMap& tmx, const CUtensorMap& tmc,
   fk_assign_tc2_kernel<FMT, BIAS, ALT, SPLIT><<<2 * pairs, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(
       tmx, tmc, tmext, a);
   return cudaGetLastError();
+}
+
+// Multicast quads (fk_assign_tc2q_kernel): launched as many 4-CTA clusters as
+// fit at once (a GPC whose SM count is not a multiple of 4 leaves SMs idle),
+// at most one per tile pair.
+template <int FMT>
+static cudaError_t launch_quad(const CUtensorMap& tmx, const CUtensorMap& tmc,
+                               const CUtensorMap& tmc_pair, const CUtensorMap& tmext, TcArgs a,
+                               int num_sms, cudaStream_t stream) {
+  static int quads_dev[32] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto kern = fk_assign_tc2q_kernel<FMT>;
+  auto pk = fk_assign_tc2_kernel<FMT, 1, false, false>;
+  int& fit = quads_dev[dev & 31];
+  if (fit == 0) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES);
+    cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, tc2::SMEM_BYTES);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(num_sms & ~3));
+    cfg.blockDim = dim3(tc2::THREADS);
+    cfg.dynamicSmemBytes = tc2::SMEM_BYTES;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 4;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (const void*)kern, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = num_sms / 4;
+    }
+    fit = n;
+    if (getenv("FK_ASSIGN_MC_VERBOSE"))
+      fprintf(stderr, "fk_assign_tc2q: %d co-resident 4-CTA clusters (%d SMs)\n", n, num_sms);
+  }
+  a.tiles_per_batch = (a.N + 2 * tc2::BM - 1) / (2 * tc2::BM);
+  a.total_tiles = a.B * a.tiles_per_batch;
+  a.ncol = (a.K + tc2::BN - 1) / tc2::BN;
+  const int total = a.total_tiles;
+  int quads = fit;
+  if ((total + 1) / 2 < quads) quads = (total + 1) / 2;
+  if (quads <= 0) return cudaSuccess;
+  // the SMs no 4-CTA cluster can use run the pair kernel on the tiles after
+  // the quads' share, sized by the quads' measured per-SM advantage
+  int extra = (num_sms - 4 * fit) / 2;
+  {
+    static int extra_env = -2;
+    if (extra_env == -2) {
+      const char* e = getenv("FK_ASSIGN_MC_EXTRA");
+      extra_env = e ? atoi(e) : -1;
+    }
+    if (extra_env >= 0 && extra_env < extra) extra = extra_env;
+  }
+  int tq = total;
+  if (extra > 0 && quads == fit && total >= 8 * (quads + extra)) {
+    static double gain = -1.0;
+    if (gain < 0) {
+      const char* e = getenv("FK_ASSIGN_MC_GAIN");
+      gain = e ? atof(e) : 1.12;
+    }
+    const double wq = 4.0 * quads * gain, wp = 2.0 * extra;
+    tq = ((int)(total * wq / (wq + wp)) + 1) & ~1;
+    if (tq > total) tq = total;
+  } else {
+    extra = 0;
+  }
+  TcArgs aq = a;
+  aq.total_tiles = tq;
+  kern<<<4 * quads, tc2::THREADS, tc2::SMEM_BYTES, stream>>>(tmx, tmc, tmext, aq);
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess || tq >= total) return err;
+  TcArgs ap = a;
+  ap.tile0 = tq;
+  ap.total_tiles = total - tq;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * extra));
+  cfg.blockDim = dim3(tc2::THREADS);
+  cfg.dynamicSmemBytes = tc2::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, pk, tmx, tmc_pair, tmext, ap);
+}
+
+// FK_ASSIGN_MC=1: multicast quads where they apply (A/B switch)
+static bool assign_mc_enabled() {
+  static int mc_env = -1;
+  if (mc_env < 0) {
+    const char* e = getenv("FK_ASSIGN_MC");
+    mc_env = (e && e[0] == '1') ? 1 : 0;
+  }
+  return mc_env == 1;
 }
 
 // Rows of a single column tile (K <= 256) alternate tiles between the two
@@ -1357,6 +1506,7 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
                              int32_t* hist_inval, int64_t hist_bpb, int64_t hist_per,
                              const float* xn_in) {
   TcArgs a;
+  a.tile0 = 0;
   a.xn_in = xn_in;
   a.hist_tab = hist_tab;
   a.hist_inval = hist_inval;
@@ -1408,7 +1558,13 @@ cudaError_t launch_assign_tc(int fmt, const void* X, const void* C, const float*
       tmext = tmc2;  // unused
     }
     cudaError_t e;
-    if (fmt == 1)
+    const bool mc = bias == 1 && B == 1 && a.ncol >= 2 && assign_mc_enabled();
+    CUtensorMap tmcq;
+    if (mc && !make_map(&tmcq, C, fmt, d, K, B, tc2::BNH / 2)) return cudaErrorInvalidValue;
+    if (mc)
+      e = fmt == 1 ? launch_quad<1>(tmx2, tmcq, tmc2, tmext, a, num_sms, stream)
+                   : launch_quad<0>(tmx2, tmcq, tmc2, tmext, a, num_sms, stream);
+    else if (fmt == 1)
       e = bias == 1   ? launch_pair<1, 1>(tmx2, tmc2, tmext, a, num_sms, stream)
           : bias == 2 ? launch_pair<1, 2>(tmx2, tmc2, tmext, a, num_sms, stream)
                       : launch_pair<1, 0>(tmx2, tmc2, tmext, a, num_sms, stream);
@@ -1461,6 +1617,7 @@ cudaError_t launch_assign_tc_split(const void* X2, const void* C2, const void* e
   if (ns < 1 || 2 * ns > 4 * tc2::KATOMS_MAX) return cudaErrorInvalidValue;
   const int64_t W = 32 * (int64_t)ns;
   TcArgs a;
+  a.tile0 = 0;
   a.xn_in = nullptr;
   a.hist_tab = nullptr;
   a.hist_inval = nullptr;

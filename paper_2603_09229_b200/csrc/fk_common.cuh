@@ -219,6 +219,19 @@ FK_DEV void tma_load_3d_cg2(void* smem_dst, const void* desc, uint32_t bar_clust
       "l"(desc), "r"(bar_cluster_addr), "r"(c0), "r"(c1), "r"(c2), "l"(cache_hint)
       : "memory");
 }
+// 2-SM TMA multicast: the box lands at the same offset in every CTA of `mask`;
+// each destination's bytes are counted on the barrier at this offset in the
+// leader of the destination's own pair (`bar_cluster_addr` names the leader of
+// the issuing CTA's pair).
+FK_DEV void tma_load_3d_cg2_mc(void* smem_dst, const void* desc, uint32_t bar_cluster_addr,
+                               uint16_t mask, int c0, int c1, int c2, uint64_t cache_hint) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes."
+      "multicast::cluster.L2::cache_hint [%0], [%1, {%4, %5, %6}], [%2], %3, %7;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(desc), "r"(bar_cluster_addr), "h"(mask), "r"(c0), "r"(c1), "r"(c2), "l"(cache_hint)
+      : "memory");
+}
 template <int kCols>
 FK_DEV void tmem_alloc_cg2(uint32_t* dst_smem) {  // one warp in EACH CTA of the pair
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(

@@ -153,3 +153,39 @@ def test_config5_shape_fp16_k65536(ops, oracle):
     assert np.array_equal(counts.cpu().numpy(), c_ref)
     assert int(merges.item()) == m_ref
     np.testing.assert_allclose(sums.cpu().numpy(), s_ref, rtol=1e-6, atol=1e-4)
+
+
+_MC_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+from oracle import oracle as O
+from paper_2603_09229_b200 import ops
+shapes = [(1, 20000, 1000, 128, torch.bfloat16),   # quads only (few tile pairs)
+          (1, 4096 * 9 + 300, 529, 64, torch.float16),  # odd tile count: one dummy tile
+          (1, 90000 + 77, 300, 128, torch.bfloat16)]    # quads + pair kernel on the leftover SMs
+for i, (B, N, K, d, dt) in enumerate(shapes):
+    g = torch.Generator().manual_seed(100 + i)
+    x = torch.randint(-4, 5, (B, N, d), generator=g).to(dt)
+    c = torch.randint(-4, 5, (B, K, d), generator=g).to(dt)
+    a, m = ops.assign(x.cuda(), c.cuda())
+    a_ref, m_ref = O.assign(x.float().numpy(), c.float().numpy())
+    assert np.array_equal(a.cpu().numpy(), a_ref), (N, K, d)
+    assert np.array_equal(m.cpu().numpy(), m_ref), (N, K, d)
+print('mc ok')
+"""
+
+
+def test_multicast_quads_integer_grid_bitwise():
+    """The opt-in multicast-quad FlashAssign (FK_ASSIGN_MC=1: two CTA pairs
+    sharing each C tile, plus the pair kernel on the SMs no 4-CTA cluster can
+    use) equals the oracle bit for bit, ties included (the switch is read once
+    per process, hence the subprocess)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FK_ASSIGN_MC="1")
+    r = subprocess.run([sys.executable, "-c", _MC_SNIPPET], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "mc ok" in r.stdout, r.stderr[-2000:]
