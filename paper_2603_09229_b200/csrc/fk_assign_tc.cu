@@ -104,7 +104,10 @@ constexpr int FK_SPLIT_REC = 2 + 2 * SPLIT_NREC;
 static_assert(FK_SPLIT_REC == kSplitRecInts, "candidate record layout (fk_kernels.h)");
 
 // Debug timeline: events of pair 0 / tile window [TR_G0, TR_G0 + TR_N) only.
-constexpr int TR_G0 = 16, TR_N = 32, TR_EV = 8;
+constexpr int TR_N = 32, TR_EV = 8;
+#ifdef FK_ASSIGN_TRACE_BUILD
+constexpr int TR_G0 = 16;
+#endif
 // Bound-analysis modes (FK_ASSIGN_DEBUG_MODE) exist only in debug builds
 // (FK_BUILD_DEBUG=1 -> -DFK_ASSIGN_DEBUG_BUILD); elsewhere the mode is the
 // constant 0 and every check folds away.
