@@ -31,6 +31,15 @@
 #include <cstdio>
 #include <cstdlib>
 
+// A/B build knobs: L2 policy of the X row-tile loads and the tensor maps' L2
+// promotion (defaults are the measured choices)
+#ifndef FK_X_HINT
+#define FK_X_HINT kEvictFirst
+#endif
+#ifndef FK_TMAP_PROMO
+#define FK_TMAP_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+
 namespace fk {
 
 namespace tc {
@@ -813,7 +822,7 @@ FK_DEV void assign_tc2_body(const CUtensorMap& tmx, const CUtensorMap& tmc,
           const uint32_t bar = mapa_shared(smem_u32(&a_full[slot]), lead);
           for (int ka = 0; ka < p.katoms; ++ka)
             tma_load_3d_cg2(sA + slot * a_slot_bytes + ka * A_ATOM, &tmx, bar, ka * 64, row0, b,
-                            kEvictFirst);
+                            FK_X_HINT);
         }
         __syncwarp();
       }
@@ -1481,7 +1490,7 @@ static bool make_map(CUtensorMap* m, const void* base, int fmt, int64_t inner, i
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, fmt == 1 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                    3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, FK_TMAP_PROMO,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
