@@ -519,6 +519,44 @@ __global__ void __launch_bounds__(SD_T, 1)
 // ranges < 2^16 points (update_bpb).
 constexpr int SW_KMAX = 16384;            // W * (K + 2) * 2 bytes <= 64 KB, + K * 8 bytes of bases
 constexpr int SW_TABLE_BYTES = 65536;
+// Programmatic dependent launch (default; FK_PDL=0 turns it off for A/B): the
+// scatter and the segsum release their dependents as soon as every CTA of
+// theirs is resident, so the segsum / normalize CTAs are placed while the previous kernel drains; a
+// dependent waits for its predecessor's completion (and memory) before any
+// access.  Both instructions are no-ops for an ordinary launch.  Same-box A/B
+// (profiles/r02_ab_pdl.txt): config-4 update 57.1-57.6 -> 54.4-54.8 us and
+// the eagerly launched pipelined loop 3-5 us faster at configs 2/4; inside a
+// CUDA graph the inter-kernel gaps are already hidden (no change).
+FK_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+FK_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+FK_DEV void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+static bool pdl_on() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FK_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+template <typename... KArgs, typename... Args>
+static void launch_maybe_pdl(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                             cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_on() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k, ((KArgs)args)...);
+}
+
 constexpr int SW_U = 8;                   // 16-byte id vectors in flight per lane (counting)
 constexpr int SW_U3 = 16;                 // id loads in flight per lane (ranking)
 constexpr int SW_COLS_BPB = 16;           // up to this many blocks per batch element: no k_colscan
@@ -579,6 +617,7 @@ __global__ void __launch_bounds__(W * 32)
                    int32_t* __restrict__ order, int rank_sort, double* __restrict__ zero_sums,
                    int64_t zero_n, int32_t* __restrict__ zero_arrive, int64_t arrive_n) {
   extern __shared__ __align__(16) uint8_t sw_sm[];
+  pdl_trigger();
   // block histograms folded into the assign (no k_hist): this pass clears the
   // f64 sums and k_segsum's arrival counters instead
   if (zero_sums || zero_arrive) {
@@ -905,6 +944,7 @@ __global__ void __launch_bounds__(256)
              const int64_t* __restrict__ off, int64_t BK, int64_t L, int64_t d,
              double* __restrict__ sums, const int32_t* __restrict__ ids, int64_t N, int64_t K,
              SegMerge mg) {
+  pdl_enter();
   seg_zero_table(mg);
   constexpr int E = VecCvt<T>::E;
   constexpr int RPW = 32 / LPR;
@@ -1032,6 +1072,7 @@ __global__ void __launch_bounds__(256, sizeof(A) == 8 ? 3 : 4)
               const int64_t* __restrict__ off, int64_t BK, int64_t L, int64_t d,
               double* __restrict__ sums, const int32_t* __restrict__ ids, int64_t N, int64_t K,
               SegMerge mg, int accumulate) {
+  pdl_enter();
   seg_zero_table(mg);
   constexpr int E = VecCvt<T>::E;
   constexpr int RPW = 32 / LPR;
@@ -1537,10 +1578,10 @@ static cudaError_t dispatch_segsum(const void* X, const UpdateWs& w, int64_t BK,
 #define FK_SEG2(LPR, VPL, U, U2)                                                                        \
   do {                                                                                                  \
     if (seq_env)                                                                                        \
-      k_segsum<T, A, LPR, VPL, U><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, ids, N, K, mg); \
+      launch_maybe_pdl(k_segsum<T, A, LPR, VPL, U>, grid, th, 0, s, x, w.order, w.off, BK, L, d, sums, ids, N, K, mg); \
     else                                                                                                \
-      k_segsum2<T, A, LPR, VPL, U2><<<grid, th, 0, s>>>(x, w.order, w.off, BK, L, d, sums, ids, N, K,   \
-                                                        mg, accumulate);                                \
+      launch_maybe_pdl(k_segsum2<T, A, LPR, VPL, U2>, grid, th, 0, s, x, w.order, w.off, BK, L, d, sums, ids, N, K,   \
+                       mg, accumulate);                                \
   } while (0)
   // k_segsum2 keeps 6 row steps where k_segsum had 8 (64 registers, no spills)
 #define FK_SEG(LPR, VPL, U) FK_SEG2(LPR, VPL, U, (U > 6 ? 6 : U))
@@ -1864,6 +1905,7 @@ __global__ void __launch_bounds__(256)
                 __nv_bfloat16* __restrict__ bias, int64_t K, int64_t kpad, TailArgs ta = TailArgs{}) {
   // TAIL: blocks [0, norm_blocks) normalize, the others sum objective
   // partials, concurrently (one block doing both would serialize them)
+  pdl_wait();
   if (!TAIL || blockIdx.x < ta.norm_blocks) {
     __shared__ double wmax[8];
     // NORM_RW rows per warp, every load of a pass (64 columns of each row) issued
@@ -2068,21 +2110,20 @@ static cudaError_t norm_tail_dispatch(int operand_dt, const double* sums, const 
   TM* ov = (TM*)out;
   __nv_bfloat16* bz = (__nv_bfloat16*)bias;
   if (!operand_out)
-    k_normalize<TM, float, true><<<grid, th, 0, s>>>(sums, counts, pv, ov, nullptr, empty, ms2, BK, d,
-                                                     nullptr, K, kpad, ta);
+    launch_maybe_pdl(k_normalize<TM, float, true>, grid, th, 0, s, sums, counts, pv, ov, (float*)nullptr,
+                     empty, ms2, BK, d, (__nv_bfloat16*)nullptr, K, kpad, ta);
   else if (operand_dt == DT_BF16)
-    k_normalize<TM, __nv_bfloat16, true><<<grid, th, 0, s>>>(sums, counts, pv, ov,
-                                                             (__nv_bfloat16*)operand_out, empty, ms2,
-                                                             BK, d, bz, K, kpad, ta);
+    launch_maybe_pdl(k_normalize<TM, __nv_bfloat16, true>, grid, th, 0, s, sums, counts, pv, ov,
+                     (__nv_bfloat16*)operand_out, empty, ms2, BK, d, bz, K, kpad, ta);
   else if (operand_dt == DT_F16)
-    k_normalize<TM, __half, true><<<grid, th, 0, s>>>(sums, counts, pv, ov, (__half*)operand_out,
-                                                      empty, ms2, BK, d, bz, K, kpad, ta);
+    launch_maybe_pdl(k_normalize<TM, __half, true>, grid, th, 0, s, sums, counts, pv, ov,
+                     (__half*)operand_out, empty, ms2, BK, d, bz, K, kpad, ta);
   else if (operand_dt == DT_F32)
-    k_normalize<TM, float, true><<<grid, th, 0, s>>>(sums, counts, pv, ov, (float*)operand_out, empty,
-                                                     ms2, BK, d, nullptr, K, kpad, ta);
+    launch_maybe_pdl(k_normalize<TM, float, true>, grid, th, 0, s, sums, counts, pv, ov,
+                     (float*)operand_out, empty, ms2, BK, d, (__nv_bfloat16*)nullptr, K, kpad, ta);
   else
-    k_normalize<TM, double, true><<<grid, th, 0, s>>>(sums, counts, pv, ov, (double*)operand_out,
-                                                      empty, ms2, BK, d, nullptr, K, kpad, ta);
+    launch_maybe_pdl(k_normalize<TM, double, true>, grid, th, 0, s, sums, counts, pv, ov,
+                     (double*)operand_out, empty, ms2, BK, d, (__nv_bfloat16*)nullptr, K, kpad, ta);
   return cudaGetLastError();
 }
 
