@@ -486,3 +486,44 @@ def test_hist_fold_counts_invalid_rows(ops):
     assert torch.equal(n, n_r)
     assert torch.equal(s.view(torch.int64), s_r.view(torch.int64))
     assert int(fold._clear.count_nonzero()) == 0
+
+
+_PDL_SNIPPET = r"""
+import hashlib, sys, torch
+sys.path.insert(0, '.')
+from paper_2603_09229_b200 import LloydEngine, ops
+out = []
+for (B, N, K, d, dt) in [(64, 16384, 256, 64, torch.float16), (1, 1 << 20, 1024, 128, torch.bfloat16)]:
+    g = torch.Generator(device='cuda').manual_seed(5)
+    x = (torch.randn((B, N, d), device='cuda', generator=g) * 4).to(dt)
+    ids = torch.randint(0, K, (B, N), device='cuda', generator=g, dtype=torch.int32)
+    s, c = ops.update(x, ids, K, N)
+    eng = LloydEngine(x, K)
+    eng.set_centroids(x[:, :K].float())
+    h = torch.empty((8, B), dtype=torch.float64, device='cuda')
+    eng.run(3, -1.0, h, stop_on_repeat=False)
+    torch.cuda.synchronize()
+    for t in (s.view(torch.int64), c, eng.master[eng.cur], h[:3]):
+        out.append(hashlib.sha1(t.contiguous().cpu().numpy().tobytes()).hexdigest())
+print(' '.join(out))
+"""
+
+
+def test_update_chain_pdl_matches_ordinary_launches():
+    """Programmatic dependent launch along scatter -> segsum -> normalize/loop
+    tail (the default) gives the same bits as ordinary launches (FK_PDL=0):
+    update sums and counts, and three engine iterations (centroids and
+    objective history). Each setting runs in its own process (the switch is
+    read once)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for v in ("1", "0"):
+        r = subprocess.run([sys.executable, "-c", _PDL_SNIPPET], cwd=root, env=dict(os.environ, FK_PDL=v),
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        res.append(r.stdout.strip().splitlines()[-1])
+    assert res[0] == res[1]
