@@ -25,6 +25,9 @@
  *   - Every call is stream-ordered, never synchronizes the host and never
  *     allocates device memory: scratch comes from a caller-owned workspace
  *     sized by the matching *_workspace query.
+ *   - Inside one call, consecutive kernels may use programmatic dependent
+ *     launch (each waits for its predecessor's completion before touching
+ *     memory), so stream order toward the caller's later work is unchanged.
  *   - All data pointers are DEVICE pointers.  Layouts are batch-major,
  *     row-major: X (B,N,d), C (B,K,d), ids (B,N) int32, sums (B,K,d) f64,
  *     counts (B,K) int64 -- the reference's shapes and dtypes
